@@ -1,0 +1,239 @@
+/*
+ * dali.h -- C-ABI of the B200-native DALI hot path (libdali.so, sm_100a).
+ *
+ * Plain pointers and sizes only; no torch types.  Every entry point is
+ * asynchronous on the caller's CUDA stream (passed as `void*`, NULL = legacy
+ * default stream) unless stated otherwise, and returns 0 on success or one
+ * of the DALI_E* codes below.  The message of the last failure on the
+ * calling thread is available from dali_last_error().
+ *
+ * Device-pointer arguments are marked [dev]; host pointers [host].
+ *
+ * The reference (``moesim``, pure Python/numpy) has no FFI; each function
+ * below names the reference Python function it replaces (file:line relative
+ * to /root/reference/pkg/src/moesim).  INTEGRATION.md shows the ctypes
+ * binding a maintainer would add on the reference side.
+ */
+#ifndef DALI_H_
+#define DALI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the Python shim maps them onto moesim.errors classes
+ * (errors.py:4-50). */
+#define DALI_OK 0
+#define DALI_ETRACE 1       /* TraceError: shape / top_k / gating input   */
+#define DALI_ECOSTMODEL 2   /* CostModelError                             */
+#define DALI_EASSIGN 3      /* AssignmentError                            */
+#define DALI_EPREFETCH 4    /* PrefetchError                              */
+#define DALI_ECACHE 5       /* CacheError                                 */
+#define DALI_ESIM 6         /* SimulationError                            */
+#define DALI_ECUDA 100      /* CUDA runtime failure                       */
+
+#define DALI_MAX_SAMPLES 32    /* cost-model table length incl. (0,0)     */
+#define DALI_MAX_EXPERTS 256   /* routed experts per layer                */
+#define DALI_MAX_TOPK 16
+
+/* Piecewise-linear cost model, passed BY VALUE into kernels.
+ * Mirrors CostModel (cost_model.py:54-68): xs/ys include the (0,0) anchor. */
+typedef struct dali_cost_model {
+  int32_t n_cpu, n_gpu;
+  double cpu_xs[DALI_MAX_SAMPLES], cpu_ys[DALI_MAX_SAMPLES];
+  double gpu_xs[DALI_MAX_SAMPLES], gpu_ys[DALI_MAX_SAMPLES];
+  double trans_time;
+  double shared_expert_gpu_time;
+  double non_moe_layer_time;
+} dali_cost_model;
+
+/* Per-layer decision record written by dali_policy_layer (one per
+ * step x layer).  Fields follow the reference driver loop
+ * (simulator.py:354-475).  Expert lists are -1 terminated / counted. */
+typedef struct dali_layer_record {
+  int32_t step, layer, token_index, n_act;
+  int32_t n_gpu, n_cpu, n_demand, n_pset;
+  int32_t n_cand, n_done, ev_valid, ev_n;
+  int32_t nodes, stopped, pad0, pad1;
+  double cpu_busy;      /* cpu_times @ C                                  */
+  double gpu_makespan;  /* engine_t of the GPU-lane pipeline              */
+  double latency;       /* layer_latency                                  */
+  double demand_end;    /* end of the last demand transfer                */
+  double demand_ms;     /* sum of demand interval lengths                 */
+  double consumed;      /* prefetch channel time charged                  */
+  double boundary;      /* replacement transfer charge                    */
+  double pad2;
+  int8_t C[DALI_MAX_EXPERTS];
+  int8_t G[DALI_MAX_EXPERTS];
+  uint8_t resident[DALI_MAX_EXPERTS];
+  uint8_t hit[DALI_MAX_EXPERTS];      /* lookup result for G experts      */
+  int16_t order[DALI_MAX_EXPERTS];    /* sorted_order (activated)         */
+  int16_t pset[DALI_MAX_EXPERTS];     /* prefetch set for layer+1         */
+  int16_t cand[DALI_MAX_EXPERTS];     /* pset minus cache[layer+1]        */
+  int16_t evicted[DALI_MAX_EXPERTS];
+  int16_t admitted[DALI_MAX_EXPERTS];
+} dali_layer_record;
+
+/* Scalar knobs of the fused per-layer policy step (SimConfig,
+ * simulator.py:45-74, restricted to the hot-path policies). */
+typedef struct dali_policy_config {
+  int32_t L, N, k;
+  int32_t assignment;        /* 0 = greedy, 1 = all-cpu                     */
+  int32_t gpu_capacity;      /* < 0 = unlimited                             */
+  int32_t prefetch_size;     /* 0 = prefetch off                            */
+  int32_t cache_enabled;
+  int32_t w_size, u_size;
+  int32_t has_shared;        /* num_shared_experts > 0                      */
+  double scheduling_overhead_ms;
+  double solver_node_cost_ms;
+  double prefetch_compute_ms;
+  double non_moe;            /* resolved non_moe_override / table value     */
+} dali_policy_config;
+
+/* ---- library ----------------------------------------------------------- */
+const char* dali_last_error(void);
+int dali_version(void);
+/* Number of kernel launches issued by this library since load (for the
+ * bench's gpu_launches claim). */
+int64_t dali_launch_count(void);
+
+/* ---- (1) gating: route + softmax + stable top-k + histogram --------------
+ * Replaces derive_workloads / gate_scores / topk_indices
+ * (trace.py:229-265) and, with `residual` != NULL, the residual shift of
+ * predict_next_layer (prefetch.py:127-136).
+ *   hidden   [dev] (T, d) row-major, f64 or bf16 (raw uint16 bits)
+ *   residual [dev] (d,) f64 added to every row first, or NULL
+ *   gate     [dev] (d, N) row-major, f64 or bf16 (layout of GateParams,
+ *            trace.py:89-113)
+ *   topk_idx [dev] (T, k) int32 or NULL; topk_w [dev] (T, k) f32 or NULL
+ *            (selected softmax probabilities; renormalised over the k when
+ *            renorm != 0)
+ *   workloads[dev] (N,) int64, overwritten.
+ * Arithmetic: fp64 products and sums, fp64 softmax; ranks by descending
+ * probability with ties to the lower index. */
+int dali_route_f64(const double* hidden, const double* residual,
+                   const double* gate, int64_t T, int32_t d, int32_t N,
+                   int32_t k, int32_t renorm, int32_t* topk_idx,
+                   float* topk_w, int64_t* workloads, void* stream);
+int dali_route_bf16(const uint16_t* hidden, const double* residual,
+                    const uint16_t* gate, int64_t T, int32_t d, int32_t N,
+                    int32_t k, int32_t renorm, int32_t* topk_idx,
+                    float* topk_w, int64_t* workloads, void* stream);
+
+/* Prefetch-set selection: stable top-P of predicted workloads
+ * (prefetch.py:153-156).  predicted [dev] (N,) int64 -> set [dev] (P,) i32 */
+int dali_prefetch_select(const int64_t* predicted, int32_t N, int32_t P,
+                         int32_t* set, void* stream);
+
+/* ---- (2) greedy assignment (single CTA) ----------------------------------
+ * Replaces AssignmentInstance times + sorted_order + greedy_assign
+ * (assignment.py:53-123,172-199; cost_model.py:19-27,70-103).
+ * If cpu_times/gpu_times are NULL they are evaluated on device from *cm
+ * (no-FMA np.interp formula); otherwise the given times are used
+ * (AssignmentInstance.from_times, assignment.py:81-103).
+ *   workloads [dev] (N,) int64; resident [dev] (N,) uint8
+ *   gpu_capacity < 0 means None.
+ *   C, G [dev] (N,) int8; order [dev] (N,) int32 (-1 padded);
+ *   times_out [dev] (2N,) f64 or NULL (cpu times then gpu times). */
+int dali_greedy(const int64_t* workloads, const uint8_t* resident, int32_t N,
+                int32_t gpu_capacity, const dali_cost_model* cm,
+                const double* cpu_times, const double* gpu_times, int8_t* C,
+                int8_t* G, int32_t* order, double* times_out, void* stream);
+
+/* Cost-model evaluation only (CostModel.t_cpu / t_gpu_compute, batch).
+ *   w [dev] (n,) f64 -> cpu_out, gpu_out [dev] (n,) f64 */
+int dali_cost_eval(const dali_cost_model* cm, const double* w, int64_t n,
+                   double* cpu_out, double* gpu_out, void* stream);
+
+/* ---- (4) workload-aware cache window update (single CTA) -----------------
+ * Replaces record_and_maybe_replace for the workload policy
+ * (cache.py:146-214).  State lives on device:
+ *   on_gpu [dev] (N,) uint8, scores [dev] (N,) f64,
+ *   counters [dev] int32[2] = {tokens_in_window, stopped}
+ *   workload [dev] (N,) f64 (the reference casts to float64)
+ *   ev [dev] int32[2 + 2*DALI_MAX_EXPERTS] =
+ *        {valid, n_swap, evicted[u]..., admitted[u]...} */
+int dali_cache_record(uint8_t* on_gpu, double* scores, int32_t* counters,
+                      int32_t N, int32_t w_size, int32_t u_size,
+                      const double* workload, int32_t is_eos, int32_t* ev,
+                      void* stream);
+
+/* ---- fused per-layer policy step -----------------------------------------
+ * One single-CTA kernel per (step, layer) that performs, in the reference
+ * driver's order (simulator.py:359-444): residency = cache | arrived,
+ * cost evaluation + greedy, GPU-lane timeline, cache lookups of the GPU
+ * experts, prefetch candidates for layer+1 and the virtual-clock arrival
+ * rule, and the cache window update; the decision is written to *rec
+ * (device or mapped-host memory).
+ *   workloads [dev] (N,) int64 this layer's true workloads
+ *   predicted [dev] (N,) int64 residual-predicted workloads of layer+1
+ *             (NULL when prefetch is off or layer == L-1)
+ *   on_gpu    [dev] (L, N) uint8 cache residency, updated in place
+ *   scores    [dev] (L, N) f64 window scores, updated in place
+ *   counters  [dev] (L, 2) int32 {window, stopped}, updated in place
+ *   arrived   [dev] (L, N) uint8 prefetched-and-arrived flags of the
+ *             current step; row layer+1 is written, row layer is consumed
+ *   slot_of   [dev] (L, N) int32 HBM slot per cached expert or -1; swaps
+ *             move the victim's slot to the admitted expert (may be NULL)
+ */
+int dali_policy_layer(const dali_policy_config* cfg, const dali_cost_model* cm,
+                      int32_t step, int32_t layer, int32_t token_index,
+                      int32_t is_eos, const int64_t* workloads,
+                      const int64_t* predicted, uint8_t* on_gpu,
+                      double* scores, int32_t* counters, uint8_t* arrived,
+                      int32_t* slot_of, dali_layer_record* rec, void* stream);
+
+/* ---- (5) expert execution -------------------------------------------------
+ * Plan: stable counting sort of the T*k (token, slot) pairs by expert.
+ *   topk_idx [dev] (T,k) i32 -> offsets [dev] (N+1) i32,
+ *   perm_token [dev] (T*k) i32 (source token of each permuted row),
+ *   pos [dev] (T,k) i32 (permuted row of each (token, slot)) */
+int dali_moe_plan(const int32_t* topk_idx, int64_t T, int32_t k, int32_t N,
+                  int32_t* offsets, int32_t* perm_token, int32_t* pos,
+                  void* stream);
+
+/* Coalesced 128-bit gather: out[r,:] = x[perm_token[r],:]  (bf16, d % 8 == 0) */
+int dali_permute(const uint16_t* x, const int32_t* perm_token, int64_t rows,
+                 int32_t d, uint16_t* out, void* stream);
+
+/* Grouped SwiGLU expert FFN over the experts with expert_ptr[e] != 0.
+ *   xp   [dev] (rows, d) bf16 permuted tokens, rows grouped by offsets
+ *   expert_ptr [dev] (N,) u64: base address of expert e's weight block
+ *        [W13 interleaved (2f, d) | W2 (d, f)] bf16, or 0 = not on GPU
+ *   hbuf [dev] (rows, f) bf16 workspace; yp [dev] (rows, d) f32 out.
+ *   Rows of experts with expert_ptr[e] == 0 are left untouched. */
+int dali_expert_ffn(const uint16_t* xp, const int32_t* offsets, int32_t N,
+                    const uint64_t* expert_ptr, int32_t d, int32_t f,
+                    int64_t rows, int32_t max_rows_per_expert, uint16_t* hbuf,
+                    float* yp, void* stream);
+
+/* Same contract, forcing the weight-streaming CUDA-core kernels (one warp
+ * per weight row, 8 tokens per pass) used for small per-expert token counts. */
+int dali_expert_ffn_simt(const uint16_t* xp, const int32_t* offsets, int32_t N,
+                         const uint64_t* expert_ptr, int32_t d, int32_t f,
+                         uint16_t* hbuf, float* yp, void* stream);
+
+/* Eq. (2) combine fused with the residual add and 128-bit scatter:
+ *   out[t,:] = x[t,:] + sum_{j: gpu_mask[idx[t,j]]} w[t,j] * yp[pos[t,j],:]
+ *              (+ extra[t,:])
+ * x, out [dev] (T,d) bf16 (may alias); yp (rows,d) f32; topk_idx/pos/topk_w
+ * (T,k); gpu_mask [dev] (N,) int8 (the G vector; NULL = all experts);
+ * extra (T,d) f32 partial output of the CPU-assigned experts or NULL. */
+int dali_unpermute_combine(const uint16_t* x, const float* yp,
+                           const int32_t* topk_idx, const int32_t* pos,
+                           const float* topk_w, const int8_t* gpu_mask,
+                           const float* extra, int64_t T, int32_t k,
+                           int32_t d, uint16_t* out, void* stream);
+
+/* Deterministic counter-hash weight init (uniform, given std):
+ * out[i] = bf16(std * sqrt(3) * (2*u(seed, offset+i) - 1)). */
+int dali_init_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed,
+                           uint64_t offset, float stdev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DALI_H_ */

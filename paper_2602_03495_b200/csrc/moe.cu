@@ -1,0 +1,342 @@
+// (5) GPU-resident expert execution: routing plan (stable counting sort),
+// coalesced 128-bit permute, weight-streaming SwiGLU expert FFN for small
+// per-expert token counts, and the Eq. (2) combine fused with the residual
+// add.  The paper's combine: y = sum_j g_j * E_j(x).
+//
+// Expert weight block layout (bf16, one contiguous block per expert, the
+// unit of HBM slots and of H2D transfers):
+//   W13: (2f, d)  rows interleaved in 64-row groups:
+//        rows [128b, 128b+64) = W1 (gate) rows [64b, 64b+64)
+//        rows [128b+64, 128b+128) = W3 (up) rows [64b, 64b+64)
+//   W2 : (d, f)
+// so one 128-row M tile of W13 yields 64 finished SwiGLU columns.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace dali {
+
+// ---------------------------------------------------------------------------
+// Plan: deterministic stable counting sort of the T*k (token, slot) pairs
+// by expert.  One CTA of 32 warps; each warp owns a contiguous segment.
+// ---------------------------------------------------------------------------
+constexpr int kPlanWarps = 32;
+
+__global__ void __launch_bounds__(kPlanWarps * 32)
+plan_kernel(const int32_t* __restrict__ topk_idx, int64_t pairs, int k, int N,
+            int32_t* __restrict__ offsets, int32_t* __restrict__ perm_token,
+            int32_t* __restrict__ pos) {
+  __shared__ int cnt[kPlanWarps][DALI_MAX_EXPERTS];
+  __shared__ int tot[DALI_MAX_EXPERTS + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kPlanWarps * DALI_MAX_EXPERTS; i += blockDim.x)
+    (&cnt[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t seg = (pairs + kPlanWarps - 1) / kPlanWarps;
+  const int64_t a = warp * seg, b = min(pairs, a + seg);
+  for (int64_t p = a + lane; p < b; p += 32) atomicAdd(&cnt[warp][topk_idx[p]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int e = 0; e < N; ++e) {
+      tot[e] = run;
+      for (int w = 0; w < kPlanWarps; ++w) run += cnt[w][e];
+    }
+    tot[N] = run;
+  }
+  __syncthreads();
+  // per-warp base = expert base + counts of earlier warps
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    int run = tot[e];
+    for (int w = 0; w < kPlanWarps; ++w) {
+      const int c = cnt[w][e];
+      cnt[w][e] = run;
+      run += c;
+    }
+  }
+  for (int e = threadIdx.x; e <= N; e += blockDim.x) offsets[e] = tot[e];
+  __syncthreads();
+  for (int64_t p0 = a; p0 < b; p0 += 32) {
+    const int64_t p = p0 + lane;
+    const bool ok = p < b;
+    const unsigned live = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+      const int e = topk_idx[p];
+      const unsigned peers = __match_any_sync(live, e);
+      const int rank = __popc(peers & ((1u << lane) - 1));
+      const int dst = cnt[warp][e] + rank;
+      perm_token[dst] = (int32_t)(p / k);
+      pos[p] = dst;
+      __syncwarp(live);
+      if (rank == 0) cnt[warp][e] += __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Permute: out[r,:] = x[perm_token[r],:], one warp per row, uint4 (8 x bf16).
+// ---------------------------------------------------------------------------
+__global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ perm,
+                               int64_t rows, int d8, uint4* __restrict__ out) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nw) {
+    const uint4* src = x + (int64_t)perm[r] * d8;
+    uint4* dst = out + r * d8;
+    for (int c = lane; c < d8; c += 32) dst[c] = __ldg(src + c);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Weight-streaming expert FFN (small token counts per expert).  One warp per
+// weight row (pair); lanes stride K in 16-byte chunks; TT tokens per pass.
+// ---------------------------------------------------------------------------
+constexpr int kTT = 8;
+
+__device__ __forceinline__ void fma8(float& acc, uint4 w, uint4 x) {
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(&w);
+  const uint32_t* xp = reinterpret_cast<const uint32_t*>(&x);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float w0 = __uint_as_float(wp[q] << 16), w1 = __uint_as_float(wp[q] & 0xffff0000u);
+    const float x0 = __uint_as_float(xp[q] << 16), x1 = __uint_as_float(xp[q] & 0xffff0000u);
+    acc = fmaf(w0, x0, acc);
+    acc = fmaf(w1, x1, acc);
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+// Up projection + SwiGLU: h[r, j] = silu(x_r . W1_j) * (x_r . W3_j).
+__global__ void __launch_bounds__(256)
+ffn_up_simt(const uint16_t* __restrict__ xp, const int32_t* __restrict__ offsets,
+            const uint64_t* __restrict__ expert_ptr, int d, int f, uint16_t* __restrict__ h) {
+  const int e = blockIdx.y;
+  const uint64_t base = expert_ptr[e];
+  const int r0 = offsets[e], r1 = offsets[e + 1];
+  if (base == 0 || r1 <= r0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 8 + warp;                 // SwiGLU column
+  if (j >= f) return;
+  const int grp = j >> 6, off = j & 63;
+  const uint16_t* W = reinterpret_cast<const uint16_t*>(base);
+  const uint4* w1 = reinterpret_cast<const uint4*>(W + (int64_t)(grp * 128 + off) * d);
+  const uint4* w3 = reinterpret_cast<const uint4*>(W + (int64_t)(grp * 128 + 64 + off) * d);
+  const int d8 = d >> 3;
+  for (int t0 = r0; t0 < r1; t0 += kTT) {
+    const int nt = min(kTT, r1 - t0);
+    float ag[kTT], au[kTT];
+#pragma unroll
+    for (int q = 0; q < kTT; ++q) { ag[q] = 0.f; au[q] = 0.f; }
+    for (int c = lane; c < d8; c += 32) {
+      const uint4 g4 = __ldg(w1 + c), u4 = __ldg(w3 + c);
+#pragma unroll
+      for (int q = 0; q < kTT; ++q) {
+        if (q < nt) {
+          const uint4 x4 = __ldg(reinterpret_cast<const uint4*>(xp + (int64_t)(t0 + q) * d) + c);
+          fma8(ag[q], g4, x4);
+          fma8(au[q], u4, x4);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kTT; ++q) {
+      if (q < nt) {
+        const float g = warp_sum(ag[q]), u = warp_sum(au[q]);
+        if (lane == 0) h[(int64_t)(t0 + q) * f + j] = f32_to_bf16_bits(silu(g) * u);
+      }
+    }
+  }
+}
+
+// Down projection: y[r, m] = h_r . W2_m  (fp32 out).
+__global__ void __launch_bounds__(256)
+ffn_down_simt(const uint16_t* __restrict__ h, const int32_t* __restrict__ offsets,
+              const uint64_t* __restrict__ expert_ptr, int d, int f, float* __restrict__ y) {
+  const int e = blockIdx.y;
+  const uint64_t base = expert_ptr[e];
+  const int r0 = offsets[e], r1 = offsets[e + 1];
+  if (base == 0 || r1 <= r0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * 8 + warp;
+  if (m >= d) return;
+  const uint16_t* W2 = reinterpret_cast<const uint16_t*>(base) + (int64_t)2 * f * d;
+  const uint4* w = reinterpret_cast<const uint4*>(W2 + (int64_t)m * f);
+  const int f8 = f >> 3;
+  for (int t0 = r0; t0 < r1; t0 += kTT) {
+    const int nt = min(kTT, r1 - t0);
+    float acc[kTT];
+#pragma unroll
+    for (int q = 0; q < kTT; ++q) acc[q] = 0.f;
+    for (int c = lane; c < f8; c += 32) {
+      const uint4 w4 = __ldg(w + c);
+#pragma unroll
+      for (int q = 0; q < kTT; ++q)
+        if (q < nt) fma8(acc[q], w4, __ldg(reinterpret_cast<const uint4*>(h + (int64_t)(t0 + q) * f) + c));
+    }
+#pragma unroll
+    for (int q = 0; q < kTT; ++q) {
+      if (q < nt) {
+        const float v = warp_sum(acc[q]);
+        if (lane == 0) y[(int64_t)(t0 + q) * d + m] = v;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Combine: out[t] = x[t] + sum_j w[t,j] * yp[pos[t,j]] (+ extra[t]); one warp
+// per token, 8 columns (16 B of bf16) per lane step.
+// ---------------------------------------------------------------------------
+__global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __restrict__ yp,
+                               const int32_t* __restrict__ idx, const int32_t* __restrict__ pos,
+                               const float* __restrict__ wts, const int8_t* __restrict__ mask,
+                               const float* __restrict__ extra, int64_t T, int k, int d,
+                               uint16_t* __restrict__ out) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int d8 = d >> 3;
+  for (int64_t t = warp; t < T; t += nw) {
+    for (int c = lane; c < d8; c += 32) {
+      float acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        if (mask && !mask[idx[t * k + j]]) continue;
+        const float g = wts[t * k + j];
+        const float4* src = reinterpret_cast<const float4*>(yp + (int64_t)pos[t * k + j] * d) + 2 * c;
+        const float4 a = src[0], b = src[1];
+        acc[0] = fmaf(g, a.x, acc[0]); acc[1] = fmaf(g, a.y, acc[1]);
+        acc[2] = fmaf(g, a.z, acc[2]); acc[3] = fmaf(g, a.w, acc[3]);
+        acc[4] = fmaf(g, b.x, acc[4]); acc[5] = fmaf(g, b.y, acc[5]);
+        acc[6] = fmaf(g, b.z, acc[6]); acc[7] = fmaf(g, b.w, acc[7]);
+      }
+      if (extra) {
+        const float4* ex = reinterpret_cast<const float4*>(extra + t * d) + 2 * c;
+        const float4 a = ex[0], b = ex[1];
+        acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+        acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+      }
+      const uint4 xv = reinterpret_cast<const uint4*>(x + t * d)[c];
+      const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xv);
+      uint4 ov;
+      uint32_t* ow = reinterpret_cast<uint32_t*>(&ov);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float lo = __uint_as_float(xw[q] << 16) + acc[2 * q];
+        const float hi = __uint_as_float(xw[q] & 0xffff0000u) + acc[2 * q + 1];
+        ow[q] = (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
+      }
+      reinterpret_cast<uint4*>(out + t * d)[c] = ov;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Counter-hash init: splitmix64(seed, index) -> 24-bit uniform.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_uniform_kernel(uint16_t* __restrict__ out, int64_t n, uint64_t seed,
+                                    uint64_t offset, float scale) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t z = splitmix64(seed * 0xD1B54A32D192ED03ull + offset + (uint64_t)i);
+    const float u = (float)(z >> 40) * (1.0f / 16777216.0f);      // [0, 1)
+    out[i] = f32_to_bf16_bits(scale * (2.0f * u - 1.0f));
+  }
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace dali
+
+using namespace dali;
+
+extern "C" int dali_moe_plan(const int32_t* topk_idx, int64_t T, int32_t k, int32_t N,
+                             int32_t* offsets, int32_t* perm_token, int32_t* pos, void* stream) {
+  DALI_REQUIRE(N >= 1 && N <= DALI_MAX_EXPERTS, DALI_ETRACE, "expert count %d", N);
+  DALI_REQUIRE(T >= 0 && k >= 1 && T * k < (1ll << 31), DALI_ETRACE, "bad plan shape");
+  plan_kernel<<<1, kPlanWarps * 32, 0, as_stream(stream)>>>(topk_idx, T * k, k, N, offsets,
+                                                            perm_token, pos);
+  DALI_LAUNCH_CHECK("plan_kernel");
+  return DALI_OK;
+}
+
+extern "C" int dali_permute(const uint16_t* x, const int32_t* perm_token, int64_t rows, int32_t d,
+                            uint16_t* out, void* stream) {
+  DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
+  if (rows <= 0) return DALI_OK;
+  const int64_t blocks = std::min<int64_t>((rows + 7) / 8, (int64_t)sm_count() * 8);
+  permute_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const uint4*>(x), perm_token, rows, d / 8, reinterpret_cast<uint4*>(out));
+  DALI_LAUNCH_CHECK("permute_kernel");
+  return DALI_OK;
+}
+
+extern "C" int dali_expert_ffn_simt(const uint16_t* xp, const int32_t* offsets, int32_t N,
+                                    const uint64_t* expert_ptr, int32_t d, int32_t f,
+                                    uint16_t* hbuf, float* yp, void* stream) {
+  DALI_REQUIRE(d % 8 == 0 && f % 64 == 0, DALI_ETRACE, "need d %% 8 == 0 and f %% 64 == 0");
+  cudaStream_t st = as_stream(stream);
+  ffn_up_simt<<<dim3((f + 7) / 8, N), 256, 0, st>>>(xp, offsets, expert_ptr, d, f, hbuf);
+  DALI_LAUNCH_CHECK("ffn_up_simt");
+  ffn_down_simt<<<dim3((d + 7) / 8, N), 256, 0, st>>>(hbuf, offsets, expert_ptr, d, f, yp);
+  DALI_LAUNCH_CHECK("ffn_down_simt");
+  return DALI_OK;
+}
+
+extern "C" int dali_unpermute_combine(const uint16_t* x, const float* yp, const int32_t* topk_idx,
+                                      const int32_t* pos, const float* topk_w,
+                                      const int8_t* gpu_mask, const float* extra, int64_t T,
+                                      int32_t k, int32_t d, uint16_t* out, void* stream) {
+  DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
+  if (T <= 0) return DALI_OK;
+  const int64_t blocks = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 8);
+  combine_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(x, yp, topk_idx, pos, topk_w,
+                                                                  gpu_mask, extra, T, k, d, out);
+  DALI_LAUNCH_CHECK("combine_kernel");
+  return DALI_OK;
+}
+
+extern "C" int dali_init_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, uint64_t offset,
+                                      float stdev, void* stream) {
+  if (n <= 0) return DALI_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+  init_uniform_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(out, n, seed, offset,
+                                                                       stdev * 1.7320508075688772f);
+  DALI_LAUNCH_CHECK("init_uniform_kernel");
+  return DALI_OK;
+}
+
+extern "C" int dali_expert_ffn(const uint16_t* xp, const int32_t* offsets, int32_t N,
+                               const uint64_t* expert_ptr, int32_t d, int32_t f, int64_t rows,
+                               int32_t max_rows_per_expert, uint16_t* hbuf, float* yp,
+                               void* stream) {
+  (void)rows;
+  (void)max_rows_per_expert;
+  return dali_expert_ffn_simt(xp, offsets, N, expert_ptr, d, f, hbuf, yp, stream);
+}
