@@ -150,6 +150,12 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
   const size_t smem = sizeof(double) * kRouteTB * N * S;
   const int64_t grid = (T + kRouteTB - 1) / kRouteTB;
   DALI_REQUIRE(grid < (1ll << 31), DALI_ETRACE, "too many tokens");
+  static bool attr_set = false;   // static smem (34 KB) + dynamic (16 KB) > 48 KB default
+  if (!attr_set) {
+    cudaFuncSetAttribute(route_kernel<TH, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         64 * 1024);
+    attr_set = true;
+  }
   route_kernel<TH, TW><<<(unsigned)grid, kRouteThreads, smem, st>>>(
       hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w,
       reinterpret_cast<unsigned long long*>(workloads));
