@@ -87,6 +87,8 @@ typedef struct dali_policy_config {
   int32_t cache_enabled;
   int32_t w_size, u_size;
   int32_t has_shared;        /* num_shared_experts > 0                      */
+  int32_t all_resident;      /* every expert in HBM (roofline reference)     */
+  int32_t pad;
   double scheduling_overhead_ms;
   double solver_node_cost_ms;
   double prefetch_compute_ms;
@@ -99,6 +101,14 @@ int dali_version(void);
 /* Number of kernel launches issued by this library since load (for the
  * bench's gpu_launches claim). */
 int64_t dali_launch_count(void);
+
+/* ---- host expert store --------------------------------------------------
+ * Page-locked host memory for the per-(layer, expert) weight blocks that
+ * the H2D copy stream and the CPU expert worker read: anonymous mmap with
+ * transparent huge pages, parallel first touch on `nthreads` threads, then
+ * cudaHostRegister (portable).  Exact size (no power-of-two rounding). */
+int dali_host_alloc(size_t bytes, int32_t nthreads, void** out);
+int dali_host_free(void* p, size_t bytes);
 
 /* ---- (1) gating: route + softmax + stable top-k + histogram --------------
  * Replaces derive_workloads / gate_scores / topk_indices

@@ -40,6 +40,8 @@ class DriverConfig:
     non_moe_override: float | None = None
     seed: int = 0
     num_shared_experts: int = 0
+    initial_on_gpu: np.ndarray | None = None   # (L, N) carry-over residency
+    all_resident: bool = False                 # every expert in HBM
 
 
 @dataclass
@@ -108,6 +110,9 @@ def run(steps, gates, cfg: DriverConfig, L: int, N: int, k: int):
             else P.default_u_size(N, cfg.cache_capacity)
         caches = [P.new_cache(l, N, cfg.cache_capacity, cfg.w_size, u, cfg.seed)
                   for l in range(L)]
+        if cfg.initial_on_gpu is not None:
+            for l in range(L):
+                caches[l].on_gpu = np.asarray(cfg.initial_on_gpu[l], dtype=bool).copy()
 
     pcie_demand = np.zeros(L)
     pcie_prefetch = np.zeros(L)
@@ -135,6 +140,8 @@ def run(steps, gates, cfg: DriverConfig, L: int, N: int, k: int):
             got = arrivals.get(l)
             if got is not None and len(got):
                 resident[got] = True
+            if cfg.all_resident:
+                resident[:] = True
             extra = cfg.prefetch_compute_ms if prefetch_on and l < L - 1 else 0.0
 
             cpu_t, gpu_t = P.expert_times(tb, w, resident)

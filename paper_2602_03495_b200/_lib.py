@@ -33,6 +33,7 @@ class PolicyConfigC(C.Structure):
                 ("assignment", C.c_int32), ("gpu_capacity", C.c_int32),
                 ("prefetch_size", C.c_int32), ("cache_enabled", C.c_int32),
                 ("w_size", C.c_int32), ("u_size", C.c_int32), ("has_shared", C.c_int32),
+                ("all_resident", C.c_int32), ("pad", C.c_int32),
                 ("scheduling_overhead_ms", C.c_double), ("solver_node_cost_ms", C.c_double),
                 ("prefetch_compute_ms", C.c_double), ("non_moe", C.c_double)]
 
@@ -78,6 +79,8 @@ SIGNATURES = {
     "dali_expert_ffn_simt": [_P, _P, _I32, _P, _I32, _I32, _P, _P, _P],
     "dali_unpermute_combine": [_P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P],
     "dali_init_uniform_bf16": [_P, _I64, C.c_uint64, C.c_uint64, C.c_float, _P],
+    "dali_host_alloc": [C.c_size_t, _I32, C.POINTER(C.c_void_p)],
+    "dali_host_free": [_P, C.c_size_t],
 }
 _RESTYPES = {"dali_last_error": C.c_char_p, "dali_version": C.c_int,
              "dali_launch_count": C.c_int64}

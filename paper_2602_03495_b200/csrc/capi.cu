@@ -22,3 +22,47 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 extern "C" const char* dali_last_error(void) { return dali::g_err; }
 extern "C" int dali_version(void) { return 1; }
 extern "C" int64_t dali_launch_count(void) { return dali::g_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// Host expert store allocation.
+// ---------------------------------------------------------------------------
+#include <sys/mman.h>
+
+#include <cstring>
+#include <thread>
+#include <vector>
+
+extern "C" int dali_host_alloc(size_t bytes, int32_t nthreads, void** out) {
+  DALI_REQUIRE(out != nullptr && bytes > 0, DALI_ECUDA, "bad host allocation request");
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  DALI_REQUIRE(p != MAP_FAILED, DALI_ECUDA, "mmap of %zu bytes failed", bytes);
+  madvise(p, bytes, MADV_HUGEPAGE);
+  if (nthreads < 1) nthreads = 1;
+  std::vector<std::thread> th;
+  const size_t chunk = (bytes + nthreads - 1) / nthreads;
+  for (int t = 0; t < nthreads; ++t) {
+    th.emplace_back([=] {
+      const size_t a = (size_t)t * chunk;
+      if (a >= bytes) return;
+      const size_t b = a + chunk < bytes ? a + chunk : bytes;
+      char* c = static_cast<char*>(p);
+      for (size_t i = a; i < b; i += 4096) c[i] = 0;
+    });
+  }
+  for (auto& x : th) x.join();
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    munmap(p, bytes);
+    dali::set_error("cudaHostRegister(%zu bytes): %s", bytes, cudaGetErrorString(e));
+    return DALI_ECUDA;
+  }
+  *out = p;
+  return DALI_OK;
+}
+
+extern "C" int dali_host_free(void* p, size_t bytes) {
+  if (!p) return DALI_OK;
+  cudaHostUnregister(p);
+  munmap(p, bytes);
+  return DALI_OK;
+}

@@ -251,7 +251,6 @@ policy_layer_kernel(dali_policy_config cfg, dali_cost_model cm, int step, int la
                     double* scores_all, int32_t* counters_all, uint8_t* arrived_all,
                     int32_t* slot_of_all, dali_layer_record* rec) {
   __shared__ PolShared s;
-  __shared__ int sh_n[4];
   __shared__ double sh_d[8];
   const int N = cfg.N, L = cfg.L;
   const int e = threadIdx.x;
@@ -265,7 +264,7 @@ policy_layer_kernel(dali_policy_config cfg, dali_cost_model cm, int step, int la
     const double w = (double)workloads[e];
     uint8_t r = 0;
     if (cfg.cache_enabled && on_gpu[e]) r = 1;
-    if (arrived[e]) r = 1;
+    if (arrived[e] || cfg.all_resident) r = 1;
     arrived[e] = 0;                       // consumed for this step
     s.wl[e] = w;
     s.res[e] = r;
@@ -317,8 +316,6 @@ policy_layer_kernel(dali_policy_config cfg, dali_cost_model cm, int step, int la
     sh_d[2] = latency;
     sh_d[3] = n_demand ? pcie_t : 0.0;     // demand_end
     sh_d[4] = demand_ms;
-    sh_n[0] = nodes;
-    sh_n[1] = n_demand;
     rec->step = step;
     rec->layer = layer;
     rec->token_index = token_index;

@@ -1,0 +1,71 @@
+"""Real MoE inference with DALI offloading (new API; the reference pkg only
+simulates).  ``build_engine`` wires random-init weights of a preset shape,
+a cost model (measured on this box or given), residual vectors and the
+``OffloadEngine``; ``OffloadEngine.generate`` is the user-facing call."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .arch import PRESETS, MoEArch, preset
+from .offload import EngineConfig, OffloadEngine, RunStats
+from .weights import ModelWeights
+
+
+def calibrate_residuals_engine(arch: MoEArch, weights: ModelWeights, cost_model, prompts,
+                               max_seq: int = 1024) -> np.ndarray:
+    """On-GPU residual calibration (Eq. 11, prefetch.py:88-104 semantics):
+    run calibration prompts through an all-GPU engine pass, capture every
+    layer's gate input and average h_{l+1} - h_l over tokens in fp64."""
+    eng = OffloadEngine(arch, weights, cost_model,
+                        EngineConfig(capture=True, cache_slots_per_layer=0,
+                                     assignment="greedy"),
+                        max_batch=prompts.shape[0], max_seq=max_seq)
+    eng.generate(prompts, 1)
+    L = arch.num_layers
+    per_layer = {}
+    for (step, l, h) in eng.stats.captured:
+        per_layer.setdefault(step, {})[l] = h
+    acc = None
+    count = 0
+    for step, hs in per_layer.items():
+        stack = torch.stack([hs[l].to(torch.float64) for l in range(L)]).cuda()   # (L, T, d)
+        tok = stack.sum(dim=1)
+        delta = tok[1:] - tok[:-1]
+        acc = delta if acc is None else acc + delta
+        count += stack.shape[1]
+    return (acc / count).cpu().numpy()
+
+
+def build_engine(name: str, cfg: EngineConfig, seed: int = 0, cost_model=None,
+                 residuals: np.ndarray | None = None, resident: bool = False,
+                 max_batch: int = 1, max_seq: int = 1024, calib_prompt_len: int = 64,
+                 log=None) -> OffloadEngine:
+    from .profiler import profile_cost_model
+    arch = preset(name)
+    w = ModelWeights(arch, seed=seed, resident=resident)
+    if cost_model is None:
+        cost_model = profile_cost_model(arch, w, log=log)
+    if residuals is None and cfg.prefetch_size > 0 and not resident:
+        g = torch.Generator().manual_seed(seed + 99)
+        prompts = torch.randint(0, arch.vocab_size, (1, calib_prompt_len), generator=g)
+        residuals = calibrate_residuals_engine(arch, w, cost_model, prompts, max_seq)
+    return OffloadEngine(arch, w, cost_model, cfg, residuals=residuals, max_batch=max_batch,
+                         max_seq=max_seq)
+
+
+def smoke_engine() -> None:
+    """Tiny config, cache + prefetch on: one short generation on cuda:0."""
+    from ..cost_model import default_cost_model
+    eng = build_engine("tiny", EngineConfig(cache_slots_per_layer=2, prefetch_size=1),
+                       cost_model=default_cost_model(non_moe_layer_time=3.0), max_seq=64)
+    prompt = torch.randint(0, eng.arch.vocab_size, (1, 16))
+    toks, st = eng.generate(prompt, 4)
+    assert toks.shape == (1, 4)
+    rep = eng.policy_report()
+    assert rep["steps"] == 4 and st.dali_launches > 0
+
+
+__all__ = ["PRESETS", "MoEArch", "preset", "EngineConfig", "OffloadEngine", "RunStats",
+           "ModelWeights", "build_engine", "calibrate_residuals_engine", "smoke_engine"]

@@ -1,0 +1,111 @@
+"""Warm-up profiler: measure this box's cost model.
+
+Greedy decisions are only as good as t_cpu / t_gpu / trans_time measured on
+the machine that runs them ("warm-up profiling").  The
+profile samples power-of-two workloads and quantises every time to the
+2^-12 ms grid, which makes all interpolated times and lane sums exact in
+fp64 (cost_model.quantize_ms) -- so the device policy kernel, the host
+report and the CPU oracle agree bit-for-bit regardless of summation order.
+Output is a reference-format cost-model JSON (cost_model.py:158-179).
+"""
+
+from __future__ import annotations
+
+import statistics
+import time
+
+import numpy as np
+import torch
+
+from .. import _lib
+from ..cost_model import CostModel, fit_cost_model, quantize_ms
+from .arch import MoEArch
+
+
+def _cpu_expert(h: torch.Tensor, W13: torch.Tensor, W2: torch.Tensor, f: int) -> torch.Tensor:
+    R = h.shape[0]
+    gu = (h @ W13.t()).view(R, f // 64, 2, 64)
+    g = gu[:, :, 0, :].reshape(R, f).float()
+    u = gu[:, :, 1, :].reshape(R, f).float()
+    act = (torch.nn.functional.silu(g) * u).to(torch.bfloat16)
+    return (act @ W2.t()).float()
+
+
+def _monotone(samples):
+    out, best = [], 0.0
+    for w, ms in samples:
+        best = max(best, ms)
+        out.append((w, best))
+    return out
+
+
+def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
+                       non_moe_ms: float | None = None, log=None) -> CostModel:
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d, f, N = arch.hidden_dim, arch.ffn_dim, arch.num_experts
+    ws = [1 << i for i in range(0, 32) if (1 << i) <= max_w]
+    # CPU lane: SwiGLU of w tokens on the host worker over the pinned store
+    if weights.host is not None:
+        blk = weights.expert_host(0, 0)
+    else:
+        blk = weights.expert_dev(0, 0).cpu()
+    W13, W2 = weights.split_expert(blk)
+    cpu = []
+    for w in ws:
+        h = torch.randn(w, d).to(torch.bfloat16)
+        _cpu_expert(h, W13, W2, f)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            _cpu_expert(h, W13, W2, f)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        cpu.append((w, quantize_ms(statistics.median(ts))))
+    # GPU compute: grouped FFN kernel, one expert resident, w tokens
+    block = torch.empty((arch.expert_elems,), dtype=torch.bfloat16, device=dev)
+    weights.init_expert(0, 0, block)
+    ptrs = torch.zeros((N,), dtype=torch.int64, device=dev)
+    ptrs[0] = block.data_ptr()
+    gpu = []
+    cs = torch.cuda.current_stream()
+    for w in ws:
+        xp = torch.randn(w, d, device=dev).to(torch.bfloat16)
+        offs = torch.tensor([0] + [w] * N, dtype=torch.int32, device=dev)
+        hbuf = torch.empty((w, f), dtype=torch.bfloat16, device=dev)
+        yp = torch.empty((w, d), dtype=torch.float32, device=dev)
+
+        def run():
+            _lib.call("dali_expert_ffn", xp.data_ptr(), offs.data_ptr(), N, ptrs.data_ptr(), d, f,
+                      w, w, hbuf.data_ptr(), yp.data_ptr(), cs.cuda_stream)
+        run()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            run()
+            e1.record(cs)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        gpu.append((w, quantize_ms(statistics.median(ts))))
+    # transfer: one expert block H2D from the pinned store
+    if weights.host is not None:
+        src = weights.host.bytes[:weights.expert_bytes]
+        dst = torch.empty((weights.expert_bytes,), dtype=torch.uint8, device=dev)
+        dst.copy_(src, non_blocking=True)
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            dst.copy_(src, non_blocking=True)
+            e1.record(cs)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        trans = quantize_ms(statistics.median(ts))
+        del dst
+    else:
+        trans = 0.0
+    nm = quantize_ms(non_moe_ms) if non_moe_ms is not None else 0.0
+    cpu = [(w, max(ms, 2.0 ** -12)) for w, ms in _monotone(cpu)]
+    gpu = [(w, max(ms, 2.0 ** -12)) for w, ms in _monotone(gpu)]
+    if log:
+        log(f"cost model: cpu {cpu} gpu {gpu} trans {trans} non_moe {nm}")
+    return fit_cost_model(cpu, gpu, trans, 0.0, nm)

@@ -44,7 +44,8 @@ class PolicyEngine:
                  seed: int = 0, num_shared_experts: int = 0,
                  scheduling_overhead_ms: float = 0.0, solver_node_cost_ms: float = 0.0,
                  prefetch_compute_ms: float = 0.0, non_moe_override: float | None = None,
-                 max_records: int = 4096, num_slots_per_layer: int | None = None):
+                 max_records: int = 4096, all_resident: bool = False,
+                 initial_on_gpu: np.ndarray | None = None):
         if N > _lib.MAX_EXPERTS:
             raise SimulationError(f"at most {_lib.MAX_EXPERTS} experts per layer")
         if assignment not in ("greedy", "all-cpu"):
@@ -70,6 +71,7 @@ class PolicyEngine:
         cfg.cache_enabled = int(self.cache_enabled)
         cfg.w_size, cfg.u_size = int(w_size), int(self.u_size)
         cfg.has_shared = int(num_shared_experts > 0)
+        cfg.all_resident = int(bool(all_resident))
         cfg.scheduling_overhead_ms = float(scheduling_overhead_ms)
         cfg.solver_node_cost_ms = float(solver_node_cost_ms)
         cfg.prefetch_compute_ms = float(prefetch_compute_ms)
@@ -82,7 +84,10 @@ class PolicyEngine:
         slot = np.full((L, N), -1, np.int32)
         if self.cache_enabled:
             for l in range(L):
-                mask = initial_resident_set(l, N, cache_capacity, seed)
+                mask = (initial_resident_set(l, N, cache_capacity, seed) if initial_on_gpu is None
+                        else np.asarray(initial_on_gpu[l], dtype=bool))
+                if int(mask.sum()) != cache_capacity:
+                    raise SimulationError("initial residency does not match cache capacity")
                 on[l] = mask
                 slot[l, np.flatnonzero(mask)] = np.arange(cache_capacity) + l * cache_capacity
         self.initial_on_gpu = on.copy()
@@ -101,6 +106,17 @@ class PolicyEngine:
         self._rec_buf = torch.empty((max_records * _lib.RECORD_BYTES,), dtype=torch.uint8,
                                     pin_memory=True)
         self.n_records = 0
+
+    def new_run(self) -> np.ndarray:
+        """Start a new run (one request): window scores, counters, arrivals
+        and the decision log reset, cache residency and slots carry over.
+        Returns the residency the run starts from (the oracle's input)."""
+        torch.cuda.current_stream().synchronize()
+        self.scores.zero_()
+        self.counters.zero_()
+        self.arrived.zero_()
+        self.n_records = 0
+        return self.on_gpu.cpu().numpy().astype(bool)
 
     # -- stepping --------------------------------------------------------------
     def record_ptr(self, i: int) -> int:
