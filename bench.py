@@ -1,0 +1,337 @@
+"""Benchmark: DALI offloaded MoE inference, Mixtral-8x7B shape, 24 GB expert cache.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dali|reference]
+
+One "step" = one request: prefill of --prefill tokens (B=--batch) followed by
+--decode generated tokens (BASELINE.json configs[1]: prefill 512 / decode
+128, random-init weights, synthetic prompts).  ``value`` is the whole-job
+decode throughput (tokens/s over all ranks) with prompts resident in HBM;
+``e2e`` repeats the timed requests through the user-facing
+``OffloadEngine.generate`` with host prompts and a host read of every
+generated token.  Multi-GPU (torchrun): independent request streams per GPU
+("replicas only", no collective); time = max over ranks.
+
+--impl reference times the reference's CPU path (oracle/cpu_reference.py:
+reference gating + every expert on the host cores) on a bounded layer
+sample, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.25)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        busy = [float(r[0]) for r in self.rows
+                if r[0].replace(".", "").isdigit() and r[6].isdigit() and int(r[6]) > 0]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(busy or sm) if (busy or sm) else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit()
+                else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+ARCH_DIMS = {
+    "mixtral-8x7b": dict(d=4096, f=14336, N=8, k=2, H=32, KV=8, hd=128, norm_topk=True),
+    "tiny": dict(d=256, f=512, N=8, k=2, H=4, KV=2, hd=64, norm_topk=True),
+}
+ARCH_LAYERS = {"mixtral-8x7b": 32, "tiny": 4}
+
+
+def cpu_reference(args, steps: int, warmup: int):
+    from oracle.cpu_reference import run_sample
+    dims, L = ARCH_DIMS[args.model], ARCH_LAYERS[args.model]
+    dec = min(args.decode - 1, 16)
+    res = None
+    for i in range(max(warmup, 0) + max(steps, 1)):
+        r = run_sample(dims, L, args.prefill, dec, batch=args.batch,
+                       sample_layers=min(2, L), seed=i)
+        if i >= warmup:
+            res = r if res is None else {**r, **{k: res[k] + r[k] for k in
+                                                  ("prefill_tokens_per_s", "decode_tokens_per_s")}}
+    n = max(steps, 1)
+    res["prefill_tokens_per_s"] /= n
+    res["decode_tokens_per_s"] /= n
+    return res
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    t0 = time.time()
+    r = cpu_reference(args, args.steps, args.warmup)
+    wall = time.time() - t0
+    v = r["decode_tokens_per_s"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(wall * 1e3 / max(args.steps + args.warmup, 1), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic", "config": config_dict(args, ws),
+        "prefill_tokens_per_s": round(r["prefill_tokens_per_s"], 3),
+        "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": r["threads"],
+                         "kind": "port", "sample": r["sample"]},
+        "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "decode tokens/s, Mixtral-8x7B shape, 24 GB HBM expert cache (prefill tokens/s + hit rate reported)"
+
+
+def config_dict(args, ws):
+    return {"workload": f"{args.model} random-init, prefill {args.prefill} + decode {args.decode} "
+                        f"per request, B={args.batch}, expert cache {args.cache_gb} GB HBM, "
+                        f"prefetch {args.prefetch}, w_size 4",
+            "global_batch": args.batch * ws, "prefill": args.prefill, "decode": args.decode,
+            "cache_gb": args.cache_gb, "parallelism": f"replicas{ws}",
+            "l2": "working set (352 MB expert blocks streamed per layer) >> 126 MB L2; no flush"}
+
+
+def run_dali(args, ws, rank, local):
+    from paper_2602_03495_b200 import _lib
+    from paper_2602_03495_b200.engine import EngineConfig, build_engine
+
+    t_setup = time.time()
+    cfg = EngineConfig(cache_gb=args.cache_gb, prefetch_size=args.prefetch, w_size=4,
+                       seed=0, time_ffn=True)
+    eng = build_engine(args.model, cfg, seed=0, max_batch=args.batch,
+                       max_seq=args.prefill + args.decode + 8, log=log if rank == 0 else None)
+    log(f"rank {rank}: setup {time.time() - t_setup:.1f}s, slots/layer {eng.slots_per_layer}, "
+        f"cost model {eng.cm.to_dict()}")
+    V = eng.arch.vocab_size
+    g = torch.Generator().manual_seed(1000 + rank)
+    n_req = args.warmup + 2 * args.steps
+    prompts = [torch.randint(0, V, (args.batch, args.prefill), generator=g) for _ in range(n_req)]
+
+    def request(p, host_io):
+        toks, st = eng.generate(p if host_io else p.cuda(), args.decode, host_io=host_io)
+        rep = eng.policy_report()
+        return st, rep
+
+    for i in range(args.warmup):
+        st, rep = request(prompts[i], True)
+        log(f"warmup {i}: prefill {st.prefill_tokens / st.prefill_ms * 1e3:.1f} tok/s, decode "
+            f"{st.decode_tokens / max(st.decode_ms, 1e-9) * 1e3:.2f} tok/s, hit {rep['cache_hit_rate']}")
+
+    def timed(host_io, offset):
+        dev_prompts = [p.cuda() for p in prompts[offset:offset + args.steps]] if not host_io \
+            else prompts[offset:offset + args.steps]
+        barrier(ws)
+        torch.cuda.synchronize()
+        cs = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = _lib.launch_count()
+        stats, reps = [], []
+        with ClockSampler(local) as clk:
+            e0.record(cs)
+            for p in dev_prompts:
+                toks, st = eng.generate(p, args.decode, host_io=host_io)
+                stats.append(st)
+                reps.append(eng.policy_report())
+            e1.record(cs)
+            torch.cuda.synchronize()
+        barrier(ws)
+        launches = _lib.launch_count() - l0
+        ms = max_over_ranks(e0.elapsed_time(e1), ws)
+        return ms, stats, reps, launches, clk.summary()
+
+    ms_v, st_v, rep_v, launches, clocks = timed(False, args.warmup)
+    ms_e, st_e, rep_e, _, _ = timed(True, args.warmup + args.steps)
+
+    def agg(stats):
+        dec_t = sum(s.decode_tokens for s in stats)
+        dec_ms = sum(s.decode_ms for s in stats)
+        pre_t = sum(s.prefill_tokens for s in stats)
+        pre_ms = sum(s.prefill_ms for s in stats)
+        dec = sum_over_ranks(dec_t, ws) / (max_over_ranks(dec_ms, ws) / 1e3)
+        pre = sum_over_ranks(pre_t, ws) / (max_over_ranks(pre_ms, ws) / 1e3)
+        return dec, pre
+
+    dec_v, pre_v = agg(st_v)
+    dec_e, pre_e = agg(st_e)
+    hits = [(r["cache_hit_rate"], len(r["cache_hit_rate_per_group"])) for r in rep_v]
+    lookups_hit = 0.0
+    # overall hit rate across requests = mean of per-request rates weighted equally
+    hit = float(np.mean([h for h, _ in hits if h is not None])) if hits else None
+    acc1 = [np.mean(list(r["prefetch_accuracy_top1"].values())) for r in rep_v
+            if r["prefetch_accuracy_top1"]]
+    # roofline: dominant kernel = grouped expert FFN (weight streaming, HBM-bound)
+    ev = [e for s in st_v for e in s.ffn_events]
+    durs = [a.elapsed_time(b) for a, b, _, _ in ev]
+    byts = [by for _, _, by, _ in ev]
+    peak, pk_kind = peaks()
+    avg_ms = float(np.mean(durs)) if durs else None
+    avg_b = float(np.mean(byts)) if byts else None
+    achieved = (avg_b / (avg_ms / 1e3) / 1e9) if durs else None
+    total_ffn_ms = float(np.sum(durs)) if durs else 0.0
+    h2d_step = int(np.mean([args.batch * args.prefill * 8 for _ in st_e]))
+    d2h_step = int(args.batch * 8 * args.decode)
+
+    cpu_base = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = cpu_reference(args, 1, 0)
+        cpu_base = {"value": round(r["decode_tokens_per_s"], 4), "unit": "tokens/s",
+                    "cores": r["threads"], "kind": "port", "sample": r["sample"],
+                    "prefill_tokens_per_s": round(r["prefill_tokens_per_s"], 3)}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(dec_v, 4), "unit": "tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_v / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, uniform random prompt ids)",
+            "config": config_dict(args, ws),
+            "prefill_tokens_per_s": round(pre_v, 3),
+            "cache_hit_rate": hit,
+            "prefetch_accuracy_top1": float(np.mean(acc1)) if acc1 else None,
+            "policy_virtual_clock_tokens_per_s": float(np.mean([r["tokens_per_second"]
+                                                                for r in rep_v])),
+            "pcie_h2d_bytes_per_step": int(np.mean([s.h2d_bytes for s in st_v])),
+            "cpu_expert_calls_per_step": float(np.mean([s.cpu_expert_calls for s in st_v])),
+            "gpu_expert_calls_per_step": float(np.mean([s.gpu_expert_calls for s in st_v])),
+            "e2e": {"value": round(dec_e, 4), "unit": "tokens/s",
+                    "prefill_tokens_per_s": round(pre_e, 3),
+                    "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": "dali_expert_ffn (grouped SwiGLU)",
+                         "achieved": round(achieved, 2) if achieved else None,
+                         "peak": peak, "peak_kind": pk_kind, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4) if achieved else None,
+                         "traffic": None, "launches": len(durs),
+                         "avg_launch_ms": avg_ms, "algorithmic_bytes_per_launch": avg_b,
+                         "share_of_step": round(total_ffn_ms / ms_v, 4) if ms_v else None},
+            "clocks": clocks,
+            "cpu_baseline": cpu_base,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dali", choices=["dali", "reference"])
+    ap.add_argument("--model", default="mixtral-8x7b", choices=sorted(ARCH_DIMS))
+    ap.add_argument("--prefill", type=int, default=512)
+    ap.add_argument("--decode", type=int, default=128)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--cache-gb", type=float, default=24.0)
+    ap.add_argument("--prefetch", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_dali(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,128 @@
+"""CPU reference arm (TEST / BASELINE INFRASTRUCTURE; never the GPU path).
+
+The reference (``moesim``) only simulates; its CPU restatement of the
+path, timed on the GPU box's host cores, is the paper's "Naive" hybrid
+baseline with no GPU: gating by the reference algorithm
+(fp64 softmax + stable top-k, oracle.policy.route restating
+trace.py:229-265) and every routed expert executed on the CPU, plus the
+same attention.  torch CPU (oneDNN, AMX-bf16) with all host threads.
+
+Bounded sample: ``layers`` of the model's L layers are materialised and
+timed, and times are scaled by L / layers (the layers are identical in
+shape and cost), so a 32-layer Mixtral-8x7B number needs only
+layers x 8 experts of host memory and finishes in seconds.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import time
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import policy as P
+
+
+class CpuMoE:
+    def __init__(self, d, f, N, k, H, KV, hd, layers, norm_topk, seed=0, max_seq=1024):
+        torch.manual_seed(seed)
+        self.d, self.f, self.N, self.k, self.H, self.KV, self.hd = d, f, N, k, H, KV, hd
+        self.layers, self.norm_topk = layers, norm_topk
+        bf = torch.bfloat16
+        tile = (torch.rand(1 << 20) * 2 - 1).to(bf)
+
+        def rnd(shape, std):
+            n = math.prod(shape)
+            reps = (n + tile.numel() - 1) // tile.numel()
+            t = tile.repeat(reps)[:n].view(shape) * (std * math.sqrt(3))
+            return t.contiguous()
+
+        self.wqkv = [rnd(((H + 2 * KV) * hd, d), d ** -0.5) for _ in range(layers)]
+        self.wo = [rnd((d, H * hd), (H * hd) ** -0.5) for _ in range(layers)]
+        rng = np.random.default_rng(seed)
+        self.router = []
+        for _ in range(layers):
+            g = rng.normal(size=(d, N)) * (0.4 / math.sqrt(d))
+            g *= rng.permutation(np.linspace(0.15, 1.85, N))[None, :]
+            self.router.append(g)
+        self.w13 = [[rnd((2 * f, d), d ** -0.5) for _ in range(N)] for _ in range(layers)]
+        self.w2 = [[rnd((d, f), f ** -0.5) for _ in range(N)] for _ in range(layers)]
+        self.max_seq = max_seq
+
+    def reset(self, B):
+        self.kc = [torch.zeros(B, self.KV, self.max_seq, self.hd, dtype=torch.bfloat16)
+                   for _ in range(self.layers)]
+        self.vc = [torch.zeros_like(c) for c in self.kc]
+        self.pos = 0
+
+    def _attn(self, l, x, B, S):
+        H, KV, hd = self.H, self.KV, self.hd
+        qkv = x @ self.wqkv[l].t()
+        q = qkv[:, :H * hd].view(B, S, H, hd).transpose(1, 2)
+        kk = qkv[:, H * hd:(H + KV) * hd].view(B, S, KV, hd).transpose(1, 2)
+        vv = qkv[:, (H + KV) * hd:].view(B, S, KV, hd).transpose(1, 2)
+        p = self.pos
+        self.kc[l][:, :, p:p + S] = kk
+        self.vc[l][:, :, p:p + S] = vv
+        o = F.scaled_dot_product_attention(q, self.kc[l][:, :, :p + S], self.vc[l][:, :, :p + S],
+                                           is_causal=(S > 1), enable_gqa=(H != KV))
+        return o.transpose(1, 2).reshape(B * S, H * hd) @ self.wo[l].t()
+
+    def _moe(self, l, h):
+        idx, score, _ = P.route(h.double().numpy(), self.router[l], self.k)
+        if self.norm_topk:
+            score = score / score.sum(axis=1, keepdims=True)
+        y = torch.zeros(h.shape, dtype=torch.float32)
+        f = self.f
+        for e in range(self.N):
+            tok, slot = np.nonzero(idx == e)
+            if len(tok) == 0:
+                continue
+            xr = h[torch.from_numpy(tok)]
+            gu = (xr @ self.w13[l][e].t()).view(len(tok), f // 64, 2, 64)
+            g = gu[:, :, 0].reshape(len(tok), f).float()
+            u = gu[:, :, 1].reshape(len(tok), f).float()
+            out = ((F.silu(g) * u).to(torch.bfloat16) @ self.w2[l][e].t()).float()
+            y.index_add_(0, torch.from_numpy(tok),
+                         out * torch.from_numpy(score[tok, slot]).float()[:, None])
+        return y
+
+    def step(self, x, B, S):
+        """One pass of the sampled layers over (B*S, d) bf16 activations."""
+        for l in range(self.layers):
+            xn = x.float()
+            xn = (xn * torch.rsqrt(xn.pow(2).mean(-1, keepdim=True) + 1e-5)).to(torch.bfloat16)
+            x = x + self._attn(l, xn, B, S)
+            h = x.float()
+            h = (h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + 1e-5)).to(torch.bfloat16)
+            x = (x.float() + self._moe(l, h)).to(torch.bfloat16)
+        self.pos += S
+        return x
+
+
+def run_sample(arch_dims: dict, total_layers: int, prefill: int, decode_steps: int, batch=1,
+               sample_layers=2, threads=None, seed=0):
+    """Time prefill and decode of the sampled layers; return scaled tokens/s."""
+    threads = threads or len(os.sched_getaffinity(0))
+    torch.set_num_threads(threads)
+    m = CpuMoE(layers=sample_layers, seed=seed, max_seq=prefill + decode_steps + 1, **arch_dims)
+    m.reset(batch)
+    g = torch.Generator().manual_seed(seed)
+    x = (torch.randn(batch * prefill, arch_dims["d"], generator=g)).to(torch.bfloat16)
+    t0 = time.perf_counter()
+    m.step(x, batch, prefill)
+    t_pre = (time.perf_counter() - t0) * total_layers / sample_layers
+    t0 = time.perf_counter()
+    for _ in range(decode_steps):
+        x = torch.randn(batch, arch_dims["d"], generator=g).to(torch.bfloat16)
+        m.step(x, batch, 1)
+    t_dec = (time.perf_counter() - t0) * total_layers / sample_layers
+    return {"prefill_tokens_per_s": batch * prefill / t_pre,
+            "decode_tokens_per_s": batch * decode_steps / t_dec,
+            "threads": threads,
+            "sample": f"{sample_layers} of {total_layers} layers (time x{total_layers}/"
+                      f"{sample_layers}), prefill {prefill} x B{batch}, {decode_steps} decode "
+                      f"steps, all experts on CPU, fp64 reference gating"}

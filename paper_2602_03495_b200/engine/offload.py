@@ -58,6 +58,7 @@ class EngineConfig:
     staging_slots: int | None = None
     capture: bool = False                   # keep gate inputs for oracle replay
     max_records: int = 16384
+    time_ffn: bool = False                  # CUDA events around every expert-FFN launch
 
 
 @dataclass
@@ -78,6 +79,7 @@ class RunStats:
     workloads: dict = field(default_factory=dict)   # (step, layer) -> realised workloads
     topk: dict = field(default_factory=dict)        # (step, layer) -> (T, k) experts (capture)
     logits: list = field(default_factory=list)      # per step (B, V) fp32 (capture)
+    ffn_events: list = field(default_factory=list)  # (start, end, algorithmic bytes, rows)
     steps_meta: list = field(default_factory=list)  # (token_index, tokens, eos)
 
 
@@ -252,8 +254,18 @@ class OffloadEngine:
             for ev in waits:
                 cs.wait_event(ev)
             hbuf = torch.empty((T * k, f), dtype=torch.bfloat16, device=self.dev)
+            if self.cfg.time_ffn:
+                t0 = torch.cuda.Event(enable_timing=True)
+                t0.record(cs)
             _lib.call("dali_expert_ffn", xp.data_ptr(), offsets.data_ptr(), N, pd.data_ptr(), d,
                       f, T * k, T, hbuf.data_ptr(), yp.data_ptr(), cs.cuda_stream)
+            if self.cfg.time_ffn:
+                t1 = torch.cuda.Event(enable_timing=True)
+                t1.record(cs)
+                n_rows = int(sum(int(self.stats.workloads[(step, l)][e]) for e in G))
+                # algorithmic bytes: each GPU expert's weights once + activations
+                byts = len(G) * self.w.expert_bytes + n_rows * (d * 2 + 2 * f * 2 + d * 4)
+                self.stats.ffn_events.append((t0, t1, byts, n_rows))
             self.stats.gpu_expert_calls += len(G)
         ffn_done = torch.cuda.Event()
         ffn_done.record(cs)
@@ -356,27 +368,32 @@ class OffloadEngine:
         self.kv.len = pos + 1
         return logits
 
-    def generate(self, prompt: torch.Tensor, max_new_tokens: int, time_it: bool = True):
-        """Greedy generation for one request.  ``prompt`` (B, S) int64 on the
-        HOST; the generated tokens come back to the host every step (the
-        end-to-end path a user sees).  Returns (tokens (B, n) int64 cpu, stats)."""
+    def generate(self, prompt: torch.Tensor, max_new_tokens: int, host_io: bool = True):
+        """Greedy generation for one request.
+
+        host_io=True (the end-to-end path a user sees): ``prompt`` (B, S)
+        int64 on the HOST, copied in inside the timed region, and every
+        generated token is read back to the host as it is produced.
+        host_io=False: ``prompt`` already in HBM and tokens stay on device.
+        Returns (tokens (B, n) int64, stats)."""
         B, S = prompt.shape
         self.start_request(B)
         l0 = _lib.launch_count()
         cs = torch.cuda.current_stream()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(cs)
-        p_dev = prompt.to(self.dev, non_blocking=True)
+        p_dev = prompt.to(self.dev, non_blocking=True) if host_io else prompt
+        fetch = (lambda t: t.to("cpu")) if host_io else (lambda t: t)
         logits = self.prefill(p_dev, is_eos=(max_new_tokens <= 1))
         nxt = logits.argmax(-1)
-        out = [nxt.to("cpu")]
+        out = [fetch(nxt)]
         if self.cfg.capture:
             self.stats.logits.append(logits.float().cpu())
         e1.record(cs)
         for i in range(max_new_tokens - 1):
             logits = self.decode(nxt, is_eos=(i == max_new_tokens - 2))
             nxt = logits.argmax(-1)
-            out.append(nxt.to("cpu"))
+            out.append(fetch(nxt))
             if self.cfg.capture:
                 self.stats.logits.append(logits.float().cpu())
         e2.record(cs)
