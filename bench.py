@@ -290,6 +290,13 @@ def run_dali(args, ws, rank, local):
             "policy_virtual_clock_tokens_per_s": float(np.mean([r["tokens_per_second"]
                                                                 for r in rep_v])),
             "pcie_h2d_bytes_per_step": int(np.mean([s.h2d_bytes for s in st_v])),
+            "copies_per_step": {k: float(np.mean([getattr(s, k) for s in st_v])) for k in
+                                ("demand_copies", "prefetch_copies", "replace_copies")},
+            "host_ms_per_step": {k: round(float(np.mean([s.host_ms.get(k, 0.0) for s in st_v])), 2)
+                                 for k in ("launch_pre", "wait_decision", "dispatch_gpu",
+                                           "cpu_experts")},
+            "decode_ms_per_step": float(np.mean([s.decode_ms for s in st_v])),
+            "prefill_ms_per_step": float(np.mean([s.prefill_ms for s in st_v])),
             "cpu_expert_calls_per_step": float(np.mean([s.cpu_expert_calls for s in st_v])),
             "gpu_expert_calls_per_step": float(np.mean([s.gpu_expert_calls for s in st_v])),
             "e2e": {"value": round(dec_e, 4), "unit": "tokens/s",

@@ -80,6 +80,7 @@ class RunStats:
     topk: dict = field(default_factory=dict)        # (step, layer) -> (T, k) experts (capture)
     logits: list = field(default_factory=list)      # per step (B, V) fp32 (capture)
     ffn_events: list = field(default_factory=list)  # (start, end, algorithmic bytes, rows)
+    host_ms: dict = field(default_factory=dict)     # host-side time breakdown of _moe
     steps_meta: list = field(default_factory=list)  # (token_index, tokens, eos)
 
 
@@ -188,6 +189,7 @@ class OffloadEngine:
         N, k, d, f = a.num_experts, a.top_k, a.hidden_dim, a.ffn_dim
         T = h.shape[0]
         cs = torch.cuda.current_stream()
+        tp0 = time.perf_counter()
         idx, wts, wl = route_device(h, self.w.router[l], k, renorm=a.norm_topk_prob)
         gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
         ri = self.policy.layer_step(step, l, token_index, is_eos, wl, h, gate_next)
@@ -210,7 +212,9 @@ class OffloadEngine:
         wl_host.copy_(wl, non_blocking=True)
         ev_dec = torch.cuda.Event()
         ev_dec.record(cs)
+        tp1 = time.perf_counter()
         ev_dec.synchronize()
+        tp2 = time.perf_counter()
         rec = self.policy.record(ri)
         self.stats.workloads[(step, l)] = wl_host.numpy().copy()
         if self.cfg.capture:
@@ -300,6 +304,7 @@ class OffloadEngine:
             self.slot_ready[l] = ev
 
         # ---- CPU experts on the host worker
+        tp3 = time.perf_counter()
         extra_dev = None
         if Cx:
             extra = torch.zeros((T, d), dtype=torch.float32, pin_memory=True)
@@ -318,6 +323,11 @@ class OffloadEngine:
                                  y * torch.from_numpy(w_np[tok, slot])[:, None])
                 self.stats.cpu_expert_calls += 1
             extra_dev = extra.to(self.dev, non_blocking=True)
+        tp4 = time.perf_counter()
+        pr = self.stats.host_ms
+        for key, v in (("launch_pre", tp1 - tp0), ("wait_decision", tp2 - tp1),
+                       ("dispatch_gpu", tp3 - tp2), ("cpu_experts", tp4 - tp3)):
+            pr[key] = pr.get(key, 0.0) + v * 1e3
 
         out = torch.empty_like(x)
         _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), idx.data_ptr(),
