@@ -226,17 +226,36 @@ int dali_expert_ffn_simt(const uint16_t* xp, const int32_t* offsets, int32_t N,
                          const uint64_t* expert_ptr, int32_t d, int32_t f,
                          uint16_t* hbuf, float* yp, void* stream);
 
+/* Tensor-core path (tcgen05 + TMA), same FFN contract as dali_expert_ffn:
+ *   expert_maps [dev] (N,) u64: device address of expert e's 256-byte pair of
+ *       CUtensorMaps (W13 map, W2 map; built by dali_expert_maps), 0 = the
+ *       expert is not on the GPU.
+ *   max_rows_per_expert selects the token tile BN in {16,32,64,128,256};
+ *   n_gpu_experts bounds the grid; yp is `splits` planes of (rows, d) f32
+ *   (split-K of the down projection; splits must divide f/64). */
+int dali_expert_ffn_tc(const uint16_t* xp, const int32_t* offsets, int32_t N,
+                       const uint64_t* expert_maps, int32_t d, int32_t f,
+                       int64_t rows, int32_t max_rows_per_expert,
+                       int32_t n_gpu_experts, uint16_t* hbuf, float* yp,
+                       int32_t splits, void* stream);
+
+/* Host: encode the two weight tensor maps of one expert block at device
+ * address `block` into out[256] (host memory; copy it to device memory). */
+int dali_expert_maps(const void* block, int32_t d, int32_t f, void* out);
+
 /* Eq. (2) combine fused with the residual add and 128-bit scatter:
- *   out[t,:] = x[t,:] + sum_{j: gpu_mask[idx[t,j]]} w[t,j] * yp[pos[t,j],:]
- *              (+ extra[t,:])
- * x, out [dev] (T,d) bf16 (may alias); yp (rows,d) f32; topk_idx/pos/topk_w
- * (T,k); gpu_mask [dev] (N,) int8 (the G vector; NULL = all experts);
- * extra (T,d) f32 partial output of the CPU-assigned experts or NULL. */
+ *   out[t,:] = x[t,:] + sum_{j: gpu_mask[idx[t,j]]} w[t,j] *
+ *              sum_{s<splits} yp[s][pos[t,j],:]  (+ extra[t,:])
+ * x, out [dev] (T,d) bf16 (may alias); yp splits x (rows,d) f32; topk_idx /
+ * pos / topk_w (T,k); gpu_mask [dev] (N,) int8 (the G vector; NULL = all
+ * experts); extra (T,d) f32 partial output of the CPU-assigned experts or
+ * NULL. */
 int dali_unpermute_combine(const uint16_t* x, const float* yp,
                            const int32_t* topk_idx, const int32_t* pos,
                            const float* topk_w, const int8_t* gpu_mask,
                            const float* extra, int64_t T, int32_t k,
-                           int32_t d, uint16_t* out, void* stream);
+                           int32_t d, int32_t splits, int64_t rows,
+                           uint16_t* out, void* stream);
 
 /* Deterministic counter-hash weight init (uniform, given std):
  * out[i] = bf16(std * sqrt(3) * (2*u(seed, offset+i) - 1)). */

@@ -59,6 +59,7 @@ class EngineConfig:
     capture: bool = False                   # keep gate inputs for oracle replay
     max_records: int = 16384
     time_ffn: bool = False                  # CUDA events around every expert-FFN launch
+    ffn_kernel: str = "tc"                  # "tc" (tcgen05 + TMA) | "simt" (weight streaming)
 
 
 @dataclass
@@ -142,15 +143,50 @@ class OffloadEngine:
         self.cpu_threads = cfg.cpu_threads or len(os.sched_getaffinity(0))
         torch.set_num_threads(self.cpu_threads)
         # per-layer pinned scratch for pointer table + G mask
-        self.ptr_host = torch.zeros((L, N * 8 + N), dtype=torch.uint8, pin_memory=True)
-        self.ptr_dev = torch.zeros((L, N * 8 + N), dtype=torch.uint8, device=self.dev)
+        self.ptr_host = torch.zeros((L, N * 16 + N), dtype=torch.uint8, pin_memory=True)
+        self.ptr_dev = torch.zeros((L, N * 16 + N), dtype=torch.uint8, device=self.dev)
         self.rope = Rope(a, max_seq, self.dev)
         self.max_batch, self.max_seq = max_batch, max_seq
         self.kv = None
         self.stats = RunStats()
+        self.use_tc = cfg.ffn_kernel == "tc"
+        self.n_cache_slots = L * slots
+        self._build_maps()
+        self.n_sm = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._load_initial_cache()
 
     # ------------------------------------------------------------------ setup
+    def _build_maps(self):
+        """One (W13, W2) tensor-map pair per physical expert location: cache
+        slots, then staging slots (offload mode) or every expert (resident)."""
+        a = self.arch
+        if self.resident_mode:
+            addrs = [self.w.expert_dev(l, e).data_ptr() for l in range(a.num_layers)
+                     for e in range(a.num_experts)]
+        else:
+            addrs = [self.cache_buf[s].data_ptr() for s in range(self.n_cache_slots)]
+            addrs += [self.staging.ptr(i) for i in range(len(self.staging.free))]
+        buf = np.zeros((max(len(addrs), 1), 256), dtype=np.uint8)
+        if self.use_tc:
+            for i, ad in enumerate(addrs):
+                _lib.call("dali_expert_maps", ad, a.hidden_dim, a.ffn_dim,
+                          buf[i].ctypes.data)
+        self.maps_dev = torch.from_numpy(buf).to(self.dev)
+
+    def _map_addr(self, phys: int) -> int:
+        return self.maps_dev.data_ptr() + phys * 256
+
+    def _splits_for(self, tiles: int) -> int:
+        """Split-K factor of the down projection so decode fills the SMs."""
+        kb = self.arch.ffn_dim // 64
+        best = 1
+        for s in range(1, 17):
+            if kb % s == 0:
+                best = s
+                if tiles * s >= 2 * self.n_sm:
+                    break
+        return best
+
     def _load_initial_cache(self):
         if not self.slots_per_layer:
             return
@@ -223,37 +259,49 @@ class OffloadEngine:
 
         G = [e for e in range(N) if rec.G[e]]
         Cx = [e for e in range(N) if rec.C[e]]
-        # ---- GPU experts: locate or fetch weights
+        # ---- GPU experts: locate or fetch weights (raw block pointer + the
+        # physical slot's tensor-map pair for the tcgen05 path)
         ptrs = np.zeros(N, dtype=np.uint64)
+        maps = np.zeros(N, dtype=np.uint64)
         waits = []
         used_staging = []
         for e in G:
             if self.resident_mode:
                 ptrs[e] = self.w.expert_dev(l, e).data_ptr()
+                maps[e] = self._map_addr(self.w.expert_index(l, e))
                 continue
             s = self.host_slot[l, e]
             if s >= 0:
                 ptrs[e] = self.cache_buf[s].data_ptr()
+                maps[e] = self._map_addr(s)
                 if self.slot_ready[l] is not None:
                     waits.append(self.slot_ready[l])
-            elif (l, e) in self.prefetched:
+                continue
+            if (l, e) in self.prefetched:
                 i, ev = self.prefetched.pop((l, e))
-                ptrs[e] = self.staging.ptr(i)
-                waits.append(ev)
-                used_staging.append(i)
             else:
                 i, ev = self._copy_into_staging(l, e)
                 self.stats.demand_copies += 1
-                ptrs[e] = self.staging.ptr(i)
-                waits.append(ev)
-                used_staging.append(i)
+            ptrs[e] = self.staging.ptr(i)
+            maps[e] = self._map_addr(self.n_cache_slots + i)
+            waits.append(ev)
+            used_staging.append(i)
         ph = self.ptr_host[l]
         ph[:N * 8].view(torch.int64).copy_(torch.from_numpy(ptrs.view(np.int64)))
+        ph[N * 8:N * 16].view(torch.int64).copy_(torch.from_numpy(maps.view(np.int64)))
         gm = np.array(rec.G[:N], dtype=np.int8)
-        ph[N * 8:].copy_(torch.from_numpy(gm.view(np.uint8)))
+        ph[N * 16:].copy_(torch.from_numpy(gm.view(np.uint8)))
         pd = self.ptr_dev[l]
         pd.copy_(ph, non_blocking=True)
-        yp = torch.empty((T * k, d), dtype=torch.float32, device=self.dev)
+        wl_np = self.stats.workloads[(step, l)]
+        splits = 1
+        if G and self.use_tc:
+            max_rows = int(max(wl_np[e] for e in G))
+            bn = 16 if max_rows <= 16 else 32 if max_rows <= 32 else 64 if max_rows <= 64 \
+                else 128 if max_rows <= 128 else 256
+            tiles = sum((int(wl_np[e]) + bn - 1) // bn for e in G) * (d // 128)
+            splits = self._splits_for(tiles)
+        yp = torch.empty((splits, T * k, d), dtype=torch.float32, device=self.dev)
         if G:
             for ev in waits:
                 cs.wait_event(ev)
@@ -261,12 +309,17 @@ class OffloadEngine:
             if self.cfg.time_ffn:
                 t0 = torch.cuda.Event(enable_timing=True)
                 t0.record(cs)
-            _lib.call("dali_expert_ffn", xp.data_ptr(), offsets.data_ptr(), N, pd.data_ptr(), d,
-                      f, T * k, T, hbuf.data_ptr(), yp.data_ptr(), cs.cuda_stream)
+            if self.use_tc:
+                _lib.call("dali_expert_ffn_tc", xp.data_ptr(), offsets.data_ptr(), N,
+                          pd.data_ptr() + N * 8, d, f, T * k, max_rows, len(G),
+                          hbuf.data_ptr(), yp.data_ptr(), splits, cs.cuda_stream)
+            else:
+                _lib.call("dali_expert_ffn", xp.data_ptr(), offsets.data_ptr(), N, pd.data_ptr(),
+                          d, f, T * k, T, hbuf.data_ptr(), yp.data_ptr(), cs.cuda_stream)
             if self.cfg.time_ffn:
                 t1 = torch.cuda.Event(enable_timing=True)
                 t1.record(cs)
-                n_rows = int(sum(int(self.stats.workloads[(step, l)][e]) for e in G))
+                n_rows = int(sum(int(wl_np[e]) for e in G))
                 # algorithmic bytes: each GPU expert's weights once + activations
                 byts = len(G) * self.w.expert_bytes + n_rows * (d * 2 + 2 * f * 2 + d * 4)
                 self.stats.ffn_events.append((t0, t1, byts, n_rows))
@@ -331,9 +384,9 @@ class OffloadEngine:
 
         out = torch.empty_like(x)
         _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), idx.data_ptr(),
-                  pos.data_ptr(), wts.data_ptr(), pd[N * 8:].data_ptr(),
-                  extra_dev.data_ptr() if extra_dev is not None else None, T, k, d,
-                  out.data_ptr(), cs.cuda_stream)
+                  pos.data_ptr(), wts.data_ptr(), pd[N * 16:].data_ptr(),
+                  extra_dev.data_ptr() if extra_dev is not None else None, T, k, d, splits,
+                  T * k, out.data_ptr(), cs.cuda_stream)
         return out
 
     # ------------------------------------------------------------- forward

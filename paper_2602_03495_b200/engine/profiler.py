@@ -40,7 +40,7 @@ def _monotone(samples):
 
 
 def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
-                       non_moe_ms: float | None = None, log=None) -> CostModel:
+                       non_moe_ms: float | None = None, log=None, tc: bool = True) -> CostModel:
     dev = torch.device("cuda", torch.cuda.current_device())
     d, f, N = arch.hidden_dim, arch.ffn_dim, arch.num_experts
     ws = [1 << i for i in range(0, 32) if (1 << i) <= max_w]
@@ -65,17 +65,35 @@ def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
     weights.init_expert(0, 0, block)
     ptrs = torch.zeros((N,), dtype=torch.int64, device=dev)
     ptrs[0] = block.data_ptr()
+    mp = np.zeros(256, dtype=np.uint8)
+    _lib.call("dali_expert_maps", block.data_ptr(), d, f, mp.ctypes.data)
+    maps_dev = torch.from_numpy(mp).to(dev)
+    maps = torch.zeros((N,), dtype=torch.int64, device=dev)
+    maps[0] = maps_dev.data_ptr()
     gpu = []
     cs = torch.cuda.current_stream()
     for w in ws:
         xp = torch.randn(w, d, device=dev).to(torch.bfloat16)
         offs = torch.tensor([0] + [w] * N, dtype=torch.int32, device=dev)
         hbuf = torch.empty((w, f), dtype=torch.bfloat16, device=dev)
-        yp = torch.empty((w, d), dtype=torch.float32, device=dev)
+        tiles = ((w + 15) // 16 if w <= 16 else 1) * (d // 128)
+        splits = 1
+        kb = f // 64
+        for s_ in range(1, 17):
+            if kb % s_ == 0:
+                splits = s_
+                if tiles * s_ >= 2 * torch.cuda.get_device_properties(dev).multi_processor_count:
+                    break
+        yp = torch.empty((splits, w, d), dtype=torch.float32, device=dev)
 
         def run():
-            _lib.call("dali_expert_ffn", xp.data_ptr(), offs.data_ptr(), N, ptrs.data_ptr(), d, f,
-                      w, w, hbuf.data_ptr(), yp.data_ptr(), cs.cuda_stream)
+            if tc:
+                _lib.call("dali_expert_ffn_tc", xp.data_ptr(), offs.data_ptr(), N,
+                          maps.data_ptr(), d, f, w, w, 1, hbuf.data_ptr(), yp.data_ptr(), splits,
+                          cs.cuda_stream)
+            else:
+                _lib.call("dali_expert_ffn", xp.data_ptr(), offs.data_ptr(), N, ptrs.data_ptr(),
+                          d, f, w, w, hbuf.data_ptr(), yp.data_ptr(), cs.cuda_stream)
         run()
         ts = []
         for _ in range(reps):

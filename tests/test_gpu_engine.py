@@ -148,7 +148,8 @@ def test_engine_kernel_pieces_vs_torch():
               T * k, T, hbuf.data_ptr(), yp.data_ptr(), s)
     out = torch.empty_like(x)
     _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), idx.data_ptr(),
-              pos.data_ptr(), wts.data_ptr(), gmask.data_ptr(), None, T, k, d, out.data_ptr(), s)
+              pos.data_ptr(), wts.data_ptr(), gmask.data_ptr(), None, T, k, d, 1, T * k,
+              out.data_ptr(), s)
     ref = x.float().cpu().clone()
     for t in range(T):
         for j in range(k):
@@ -158,3 +159,55 @@ def test_engine_kernel_pieces_vs_torch():
             ref[t] += float(wts[t, j]) * M.expert_forward(x[t:t + 1].float().cpu(),
                                                           blocks[e].cpu(), d, f)[0]
     torch.testing.assert_close(out.float().cpu(), ref, rtol=RTOL, atol=RTOL)
+
+
+@pytest.mark.parametrize("d,f,counts,splits", [
+    (256, 512, [1, 0, 1, 0, 0, 0, 0, 0], 1),
+    (256, 512, [3, 9, 16, 0, 5, 1, 2, 7], 2),
+    (512, 1408, [17, 40, 0, 64, 1, 30, 0, 2], 11),
+    (256, 512, [100, 128, 129, 0, 3, 60, 250, 300], 4),
+    (4096, 1024, [1, 1, 0, 0, 0, 0, 0, 0], 8),
+])
+def test_tc_ffn_matches_simt_and_torch(d, f, counts, splits):
+    """tcgen05/TMA grouped FFN vs the CUDA-core kernel and a torch fp32 reference."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200 import _lib
+    dev = torch.device("cuda")
+    N = len(counts)
+    rows = sum(counts)
+    g = torch.Generator().manual_seed(rows + d)
+    xp = torch.randn(rows, d, generator=g).to(torch.bfloat16).to(dev)
+    blocks = (torch.randn(N, 3 * f * d, generator=g) * 0.04).to(torch.bfloat16).to(dev)
+    offs = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int32, device=dev)
+    on = [c > 0 and e != 2 for e, c in enumerate(counts)]      # expert 2 "on the CPU"
+    mp = np.zeros((N, 256), dtype=np.uint8)
+    for e in range(N):
+        _lib.call("dali_expert_maps", blocks[e].data_ptr(), d, f, mp[e].ctypes.data)
+    maps_dev = torch.from_numpy(mp).to(dev)
+    maps = torch.tensor([maps_dev[e].data_ptr() if on[e] else 0 for e in range(N)],
+                        dtype=torch.int64, device=dev)
+    ptrs = torch.tensor([blocks[e].data_ptr() if on[e] else 0 for e in range(N)],
+                        dtype=torch.int64, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    h_tc = torch.zeros(rows, f, dtype=torch.bfloat16, device=dev)
+    y_tc = torch.zeros(splits, rows, d, dtype=torch.float32, device=dev)
+    _lib.call("dali_expert_ffn_tc", xp.data_ptr(), offs.data_ptr(), N, maps.data_ptr(), d, f,
+              rows, max(counts), sum(on), h_tc.data_ptr(), y_tc.data_ptr(), splits, s)
+    h_s = torch.zeros(rows, f, dtype=torch.bfloat16, device=dev)
+    y_s = torch.zeros(rows, d, dtype=torch.float32, device=dev)
+    _lib.call("dali_expert_ffn", xp.data_ptr(), offs.data_ptr(), N, ptrs.data_ptr(), d, f,
+              rows, max(counts), h_s.data_ptr(), y_s.data_ptr(), s)
+    torch.cuda.synchronize()
+    y_tc = y_tc.sum(0)
+    o = offs.cpu().tolist()
+    for e in range(N):
+        if not on[e]:
+            continue
+        r0, r1 = o[e], o[e + 1]
+        ref = M.expert_forward(xp[r0:r1].float().cpu(), blocks[e].cpu(), d, f)
+        scale = ref.abs().max().item()
+        torch.testing.assert_close(y_tc[r0:r1].cpu(), ref, rtol=RTOL, atol=RTOL * scale)
+        torch.testing.assert_close(y_s[r0:r1].cpu(), ref, rtol=RTOL, atol=RTOL * scale)
+        torch.testing.assert_close(h_tc[r0:r1].float(), h_s[r0:r1].float(), rtol=RTOL,
+                                   atol=RTOL * h_s[r0:r1].float().abs().max().item())
