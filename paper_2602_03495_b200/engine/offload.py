@@ -174,7 +174,7 @@ class OffloadEngine:
         self.maps_dev = torch.from_numpy(buf).to(self.dev)
 
     def _map_addr(self, phys: int) -> int:
-        return self.maps_dev.data_ptr() + phys * 256
+        return self.maps_dev.data_ptr() + int(phys) * 256
 
     def _splits_for(self, tiles: int) -> int:
         """Split-K factor of the down projection so decode fills the SMs."""
