@@ -100,7 +100,9 @@ template <int BN>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGES = BN >= 128 ? 4 : (BN >= 64 ? 6 : 8);
+  // BN <= 64: 4 stages so 2-3 CTAs share an SM (decode weight streaming);
+  // BN 128: one CTA per SM with a deeper ring; BN 256: 4 x 48 KB.
+  static constexpr int STAGES = BN == 128 ? 6 : 4;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr size_t BYTES =
       (size_t)STAGES * (A_BYTES + B_BYTES) + 64 * 17 * 4 + 1024 /*align*/ + 256 /*bars*/;

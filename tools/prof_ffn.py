@@ -1,0 +1,94 @@
+"""Drive the grouped expert FFN kernels at Mixtral-8x7B shapes (for ncu).
+
+    python tools/prof_ffn.py [--mode decode|prefill|both] [--iters N] [--kernel tc|simt]
+
+decode : 2 GPU experts x 1 token (B=1 top-2), weights resident in HBM
+prefill: 8 GPU experts x 128 tokens (512-token prompt, top-2)
+Prints CUDA-event timings and achieved HBM GB/s (algorithmic bytes).
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_03495_b200 import _lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--mode", default="both")
+ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--kernel", default="tc")
+ap.add_argument("--d", type=int, default=4096)
+ap.add_argument("--f", type=int, default=14336)
+args = ap.parse_args()
+d, f, N = args.d, args.f, 8
+dev = torch.device("cuda")
+blocks = torch.empty((N, 3 * f * d), dtype=torch.bfloat16, device=dev)
+for e in range(N):
+    _lib.call("dali_init_uniform_bf16", blocks[e].data_ptr(), blocks[e].numel(), 7 + e, 0,
+              0.02, torch.cuda.current_stream().cuda_stream)
+mp = np.zeros((N, 256), dtype=np.uint8)
+for e in range(N):
+    _lib.call("dali_expert_maps", blocks[e].data_ptr(), d, f, mp[e].ctypes.data)
+maps_dev = torch.from_numpy(mp).to(dev)
+nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+peak = 6552.3
+
+
+def run(counts, label):
+    rows = sum(counts)
+    on = [c > 0 for c in counts]
+    offs = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int32, device=dev)
+    maps = torch.tensor([maps_dev[e].data_ptr() if on[e] else 0 for e in range(N)],
+                        dtype=torch.int64, device=dev)
+    ptrs = torch.tensor([blocks[e].data_ptr() if on[e] else 0 for e in range(N)],
+                        dtype=torch.int64, device=dev)
+    xp = torch.randn(rows, d, device=dev).to(torch.bfloat16)
+    h = torch.empty(rows, f, dtype=torch.bfloat16, device=dev)
+    mr = max(counts)
+    bn = 16 if mr <= 16 else 32 if mr <= 32 else 64 if mr <= 64 else 128 if mr <= 128 else 256
+    tiles = sum((c + bn - 1) // bn for c in counts if c) * (d // 128)
+    splits = 1
+    for s in range(1, 17):
+        if (f // 64) % s == 0:
+            splits = s
+            if tiles * s >= 2 * nsm:
+                break
+    y = torch.empty(splits, rows, d, dtype=torch.float32, device=dev)
+    cs = torch.cuda.current_stream().cuda_stream
+
+    def go():
+        if args.kernel == "tc":
+            _lib.call("dali_expert_ffn_tc", xp.data_ptr(), offs.data_ptr(), N, maps.data_ptr(), d,
+                      f, rows, mr, sum(on), h.data_ptr(), y.data_ptr(), splits, cs)
+        else:
+            _lib.call("dali_expert_ffn", xp.data_ptr(), offs.data_ptr(), N, ptrs.data_ptr(), d, f,
+                      rows, mr, h.data_ptr(), y.data_ptr(), cs)
+    for _ in range(3):
+        go()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        go()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    byts = sum(on) * 3 * f * d * 2 + rows * (d * 2 + 2 * f * 2 + d * 4 * splits)
+    flops = 6.0 * rows * d * f
+    print(f"{label}: {args.kernel} splits={splits} bn={bn} median {ms * 1e3:.1f} us, "
+          f"{byts / ms / 1e6:.0f} GB/s ({byts / ms / 1e6 / peak:.3f} of {peak}), "
+          f"{flops / ms / 1e9:.1f} TFLOP/s, bytes {byts}")
+
+
+if args.mode in ("decode", "both"):
+    run([1, 0, 0, 1, 0, 0, 0, 0], "decode 2x1")
+if args.mode in ("prefill", "both"):
+    run([128] * 8, "prefill 8x128")
+if args.mode == "all":
+    for c in ([1, 1, 0, 0, 0, 0, 0, 0], [4] * 8, [16] * 8, [64] * 8, [256] * 8, [512] * 8):
+        run(c, f"counts {c[0]}x{sum(1 for x in c if x)}")
