@@ -114,11 +114,16 @@ def barrier(ws):
         dist.barrier()
 
 
+def _red_device():
+    import torch.distributed as dist
+    return "cpu" if dist.get_backend() == "gloo" else "cuda"
+
+
 def max_over_ranks(v: float, ws: int) -> float:
     if ws == 1:
         return v
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=_red_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -127,7 +132,7 @@ def sum_over_ranks(v: float, ws: int) -> float:
     if ws == 1:
         return v
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=_red_device())
     dist.all_reduce(t)
     return float(t.item())
 
@@ -195,10 +200,31 @@ def run_dali(args, ws, rank, local):
     from paper_2602_03495_b200.engine import EngineConfig, build_engine
 
     t_setup = time.time()
+    local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", ws))
+    cores = len(os.sched_getaffinity(0))
     cfg = EngineConfig(cache_gb=args.cache_gb, prefetch_size=args.prefetch, w_size=4,
-                       seed=0, time_ffn=True)
+                       seed=0, time_ffn=True, cpu_threads=max(1, cores // local_ws))
+    weights = None
+    if local_ws > 1:
+        # one node-shared host expert store (memfd) filled once by local rank 0
+        import torch.distributed as dist
+        from paper_2602_03495_b200.engine import ModelWeights, preset
+        from paper_2602_03495_b200.engine.weights import HostStore
+        arch = preset(args.model)
+        nbytes = arch.num_layers * arch.num_experts * arch.expert_bytes
+        info = [None]
+        store = None
+        if local == 0:
+            store = HostStore(nbytes, cores, shared="create")
+            info = [(store.fd, store.owner_pid)]
+        dist.broadcast_object_list(info, src=rank - local)
+        if local != 0:
+            store = HostStore(nbytes, 1, shared="open", fd=info[0][0], owner_pid=info[0][1])
+        weights = ModelWeights(arch, seed=0, host_store=store, fill_experts=(local == 0))
+        barrier(ws)
     eng = build_engine(args.model, cfg, seed=0, max_batch=args.batch,
-                       max_seq=args.prefill + args.decode + 8, log=log if rank == 0 else None)
+                       max_seq=args.prefill + args.decode + 8, log=log if rank == 0 else None,
+                       weights=weights)
     log(f"rank {rank}: setup {time.time() - t_setup:.1f}s, slots/layer {eng.slots_per_layer}, "
         f"cost model {eng.cm.to_dict()}")
     V = eng.arch.vocab_size

@@ -109,6 +109,12 @@ int64_t dali_launch_count(void);
  * cudaHostRegister (portable).  Exact size (no power-of-two rounding). */
 int dali_host_alloc(size_t bytes, int32_t nthreads, void** out);
 int dali_host_free(void* p, size_t bytes);
+/* Shared variant for one store per node (data-parallel replicas): with
+ * create != 0 a memfd of `bytes` is created, touched and registered and its
+ * descriptor returned in *fd; with create == 0 the owner's memfd is opened
+ * through /proc/<owner_pid>/fd/<*fd>, mapped MAP_SHARED and registered. */
+int dali_host_alloc_shared(size_t bytes, int32_t nthreads, int32_t create,
+                           int32_t* fd, int32_t owner_pid, void** out);
 
 /* ---- (1) gating: route + softmax + stable top-k + histogram --------------
  * Replaces derive_workloads / gate_scores / topk_indices

@@ -66,3 +66,49 @@ extern "C" int dali_host_free(void* p, size_t bytes) {
   munmap(p, bytes);
   return DALI_OK;
 }
+
+#include <fcntl.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+extern "C" int dali_host_alloc_shared(size_t bytes, int32_t nthreads, int32_t create, int32_t* fd,
+                                      int32_t owner_pid, void** out) {
+  DALI_REQUIRE(out != nullptr && fd != nullptr && bytes > 0, DALI_ECUDA, "bad shared alloc");
+  int f = -1;
+  if (create) {
+    f = (int)syscall(SYS_memfd_create, "dali_expert_store", 0);
+    DALI_REQUIRE(f >= 0, DALI_ECUDA, "memfd_create failed");
+    DALI_REQUIRE(ftruncate(f, (off_t)bytes) == 0, DALI_ECUDA, "ftruncate(%zu) failed", bytes);
+  } else {
+    char path[64];
+    snprintf(path, sizeof(path), "/proc/%d/fd/%d", owner_pid, *fd);
+    f = open(path, O_RDWR);
+    DALI_REQUIRE(f >= 0, DALI_ECUDA, "open(%s) failed", path);
+  }
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, f, 0);
+  DALI_REQUIRE(p != MAP_FAILED, DALI_ECUDA, "mmap of shared store failed");
+  madvise(p, bytes, MADV_HUGEPAGE);
+  if (create) {
+    if (nthreads < 1) nthreads = 1;
+    std::vector<std::thread> th;
+    const size_t chunk = (bytes + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t)
+      th.emplace_back([=] {
+        const size_t a = (size_t)t * chunk;
+        if (a >= bytes) return;
+        const size_t b = a + chunk < bytes ? a + chunk : bytes;
+        char* c = static_cast<char*>(p);
+        for (size_t i = a; i < b; i += 4096) c[i] = 0;
+      });
+    for (auto& x : th) x.join();
+    *fd = f;
+  }
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    munmap(p, bytes);
+    dali::set_error("cudaHostRegister(shared, %zu bytes): %s", bytes, cudaGetErrorString(e));
+    return DALI_ECUDA;
+  }
+  *out = p;
+  return DALI_OK;
+}

@@ -41,10 +41,10 @@ def calibrate_residuals_engine(arch: MoEArch, weights: ModelWeights, cost_model,
 def build_engine(name: str, cfg: EngineConfig, seed: int = 0, cost_model=None,
                  residuals: np.ndarray | None = None, resident: bool = False,
                  max_batch: int = 1, max_seq: int = 1024, calib_prompt_len: int = 64,
-                 log=None) -> OffloadEngine:
+                 log=None, weights: ModelWeights | None = None) -> OffloadEngine:
     from .profiler import profile_cost_model
     arch = preset(name)
-    w = ModelWeights(arch, seed=seed, resident=resident)
+    w = weights if weights is not None else ModelWeights(arch, seed=seed, resident=resident)
     if cost_model is None:
         cost_model = profile_cost_model(arch, w, log=log)
     if residuals is None and cfg.prefetch_size > 0 and not resident:

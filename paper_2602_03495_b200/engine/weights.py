@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import numpy as np
 import torch
@@ -55,10 +56,22 @@ def router_weights(arch: MoEArch, seed: int, layer: int) -> np.ndarray:
 class HostStore:
     """Page-locked expert store (exact size, huge pages, parallel first touch)."""
 
-    def __init__(self, nbytes: int, nthreads: int = 16):
+    def __init__(self, nbytes: int, nthreads: int = 16, shared: str | None = None,
+                 fd: int = -1, owner_pid: int = 0):
+        """shared=None: private store; "create": node-shared memfd store (its
+        fd/pid go to the other local ranks); "open": map the owner's store."""
         self.nbytes = int(nbytes)
         p = C.c_void_p()
-        _lib.call("dali_host_alloc", self.nbytes, int(nthreads), C.byref(p))
+        self.fd, self.owner_pid = fd, owner_pid
+        if shared is None:
+            _lib.call("dali_host_alloc", self.nbytes, int(nthreads), C.byref(p))
+        else:
+            cfd = C.c_int32(fd)
+            _lib.call("dali_host_alloc_shared", self.nbytes, int(nthreads),
+                      int(shared == "create"), C.byref(cfd), int(owner_pid), C.byref(p))
+            self.fd = int(cfd.value)
+            if shared == "create":
+                self.owner_pid = os.getpid()
         self.ptr = int(p.value)
         arr = np.ctypeslib.as_array((C.c_uint8 * self.nbytes).from_address(self.ptr))
         self.bytes = torch.from_numpy(arr)           # uint8 CPU view (pinned)
@@ -77,7 +90,8 @@ class HostStore:
 
 class ModelWeights:
     def __init__(self, arch: MoEArch, seed: int = 0, device="cuda", resident: bool = False,
-                 host_threads: int = 16):
+                 host_threads: int = 16, host_store: "HostStore | None" = None,
+                 fill_experts: bool = True):
         self.arch, self.seed = arch, seed
         a = arch
         dev = torch.device(device)
@@ -109,14 +123,17 @@ class ModelWeights:
             self.host = None
         else:
             self.dev_store = None
-            self.host = HostStore(L * N * a.expert_bytes, host_threads)
-        stage = torch.empty((E,), dtype=bf, device=dev)
-        for l in range(L):
-            for e in range(N):
-                dst = self.expert_dev(l, e) if resident else stage
-                self.init_expert(l, e, dst)
-                if not resident:
-                    self.expert_host(l, e).copy_(stage)   # D2H into the pinned store
+            self.host = host_store or HostStore(L * N * a.expert_bytes, host_threads)
+            if self.host.nbytes != L * N * a.expert_bytes:
+                raise ValueError("host store size does not match the architecture")
+        if resident or fill_experts:
+            stage = torch.empty((E,), dtype=bf, device=dev)
+            for l in range(L):
+                for e in range(N):
+                    dst = self.expert_dev(l, e) if resident else stage
+                    self.init_expert(l, e, dst)
+                    if not resident:
+                        self.expert_host(l, e).copy_(stage)   # D2H into the pinned store
         torch.cuda.synchronize()
 
     def init_expert(self, l: int, e: int, out: torch.Tensor) -> torch.Tensor:
