@@ -252,6 +252,7 @@ def run_dali(args, ws, rank, local):
         l0 = _lib.launch_count()
         stats, reps = [], []
         with ClockSampler(local) as clk:
+            torch.cuda.nvtx.range_push("timed")
             e0.record(cs)
             for p in dev_prompts:
                 toks, st = eng.generate(p, args.decode, host_io=host_io)
@@ -259,6 +260,7 @@ def run_dali(args, ws, rank, local):
                 reps.append(eng.policy_report())
             e1.record(cs)
             torch.cuda.synchronize()
+            torch.cuda.nvtx.range_pop()
         barrier(ws)
         launches = _lib.launch_count() - l0
         ms = max_over_ranks(e0.elapsed_time(e1), ws)
