@@ -91,6 +91,11 @@ def forward(arch, dense, expert_block, tokens, topk_override=None):
                 continue
             out = expert_forward(h[rows], expert_block(l, e), d, a.ffn_dim)
             y.index_add_(0, rows, out * sel[rows, slot].float()[:, None])
+        if a.num_shared_experts > 0:
+            ys = expert_forward(h, dense["shared"][l], d, a.shared_ffn_dim)
+            if a.shared_gate:
+                ys = ys * torch.sigmoid(h @ dense["shared_gate"][l].float().t())
+            y = y + ys
         x = x + y
     xf = _rms(x, a.rms_eps) * dense["final_norm"].float()
     logits = xf @ dense["lm_head"].float().t()
@@ -106,4 +111,6 @@ def dense_from_weights(w):
         "moe_norm": [w.moe_norm[l].cpu() for l in range(L)],
         "wqkv": [w.wqkv[l].cpu() for l in range(L)], "wo": [w.wo[l].cpu() for l in range(L)],
         "router": [w.router[l].cpu() for l in range(L)],
+        "shared": [b.cpu() for b in w.shared],
+        "shared_gate": [g.cpu() for g in w.shared_gate],
     }

@@ -15,10 +15,11 @@
 namespace dali {
 
 constexpr int kRouteThreads = 256;
-constexpr int kRouteTB = 8;      // tokens per CTA (== warps per CTA)
+// tokens per CTA (TB <= warps per CTA) is a template parameter: 8 for long
+// prompts, fewer when T is small so the grid still covers the SMs.
 constexpr int kRouteCH = 256;    // hidden chunk staged per iteration
 
-template <typename TH, typename TW>
+template <typename TH, typename TW, int kRouteTB>
 __global__ void __launch_bounds__(kRouteThreads)
 route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
              const TW* __restrict__ gate, int64_t T, int d, int N, int k,
@@ -147,18 +148,31 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
   DALI_LAUNCH_CHECK("zero_i64");
   if (T == 0) return DALI_OK;
   const int S = kRouteThreads / N;
-  const size_t smem = sizeof(double) * kRouteTB * N * S;
-  const int64_t grid = (T + kRouteTB - 1) / kRouteTB;
-  DALI_REQUIRE(grid < (1ll << 31), DALI_ETRACE, "too many tokens");
-  static bool attr_set = false;   // static smem (34 KB) + dynamic (16 KB) > 48 KB default
+  DALI_REQUIRE((T + 1) / 2 < (1ll << 31), DALI_ETRACE, "too many tokens");
+  static bool attr_set = false;   // static smem (up to 34 KB) + dynamic (16 KB) > 48 KB default
   if (!attr_set) {
-    cudaFuncSetAttribute(route_kernel<TH, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(route_kernel<TH, TW, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         64 * 1024);
+    cudaFuncSetAttribute(route_kernel<TH, TW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         64 * 1024);
+    cudaFuncSetAttribute(route_kernel<TH, TW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          64 * 1024);
     attr_set = true;
   }
-  route_kernel<TH, TW><<<(unsigned)grid, kRouteThreads, smem, st>>>(
-      hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w,
-      reinterpret_cast<unsigned long long*>(workloads));
+  auto* ul = reinterpret_cast<unsigned long long*>(workloads);
+  if (T >= 8 * 148) {
+    route_kernel<TH, TW, 8><<<(unsigned)((T + 7) / 8), kRouteThreads,
+                              sizeof(double) * 8 * N * S, st>>>(
+        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
+  } else if (T >= 4 * 148) {
+    route_kernel<TH, TW, 4><<<(unsigned)((T + 3) / 4), kRouteThreads,
+                              sizeof(double) * 4 * N * S, st>>>(
+        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
+  } else {
+    route_kernel<TH, TW, 2><<<(unsigned)((T + 1) / 2), kRouteThreads,
+                              sizeof(double) * 2 * N * S, st>>>(
+        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
+  }
   DALI_LAUNCH_CHECK("route_kernel");
   return DALI_OK;
 }

@@ -129,7 +129,8 @@ class OffloadEngine:
             L, N, k, cost_model, assignment=cfg.assignment, gpu_capacity=cfg.gpu_capacity,
             prefetch_size=cfg.prefetch_size if not self.resident_mode else 0,
             residuals=res_dev, cache_capacity=slots, w_size=cfg.w_size, u_size=cfg.u_size,
-            seed=cfg.seed, max_records=cfg.max_records, all_resident=self.resident_mode)
+            seed=cfg.seed, max_records=cfg.max_records, all_resident=self.resident_mode,
+            num_shared_experts=a.num_shared_experts)
         self.copy_stream = torch.cuda.Stream()
         # HBM expert cache slots: layer l owns slots [l*slots, (l+1)*slots)
         self.cache_buf = (torch.empty((L * slots, weights.expert_bytes), dtype=torch.uint8,
@@ -152,6 +153,18 @@ class OffloadEngine:
         self.use_tc = cfg.ffn_kernel == "tc"
         self.n_cache_slots = L * slots
         self._build_maps()
+        # shared expert(s): resident dense SwiGLU blocks, one tensor-map pair per layer
+        self.shared_map_ptr = None
+        if a.num_shared_experts > 0:
+            sm = np.zeros((L, 256), dtype=np.uint8)
+            for l in range(L):
+                _lib.call("dali_expert_maps", weights.shared[l].data_ptr(), d, a.shared_ffn_dim,
+                          sm[l].ctypes.data)
+            self.shared_maps_dev = torch.from_numpy(sm).to(self.dev)
+            self.shared_map_ptr = torch.tensor(
+                [self.shared_maps_dev[l].data_ptr() for l in range(L)], dtype=torch.int64,
+                device=self.dev)
+        self._offs_cache: dict = {}
         self.n_sm = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._load_initial_cache()
 
@@ -172,6 +185,34 @@ class OffloadEngine:
                 _lib.call("dali_expert_maps", ad, a.hidden_dim, a.ffn_dim,
                           buf[i].ctypes.data)
         self.maps_dev = torch.from_numpy(buf).to(self.dev)
+
+    def _shared_ffn(self, l: int, h: torch.Tensor) -> torch.Tensor:
+        """Shared expert(s) of layer l over all T tokens -> (T, d) f32."""
+        a = self.arch
+        T, d, fs = h.shape[0], a.hidden_dim, a.shared_ffn_dim
+        offs = self._offs_cache.get(T)
+        if offs is None:
+            offs = torch.tensor([0, T], dtype=torch.int32, device=self.dev)
+            self._offs_cache[T] = offs
+        bn = 16 if T <= 16 else 32 if T <= 32 else 64 if T <= 64 else 128 if T <= 128 else 256
+        kb = fs // 64
+        tiles = ((T + bn - 1) // bn) * (d // 128)
+        sp = 1
+        for s in range(1, 17):
+            if kb % s == 0:
+                sp = s
+                if tiles * s >= 2 * self.n_sm:
+                    break
+        hs = torch.empty((T, fs), dtype=torch.bfloat16, device=self.dev)
+        ys = torch.empty((sp, T, d), dtype=torch.float32, device=self.dev)
+        cs = torch.cuda.current_stream()
+        _lib.call("dali_expert_ffn_tc", h.data_ptr(), offs.data_ptr(), 1,
+                  self.shared_map_ptr.data_ptr() + 8 * l, d, fs, T, T, 1, hs.data_ptr(),
+                  ys.data_ptr(), sp, cs.cuda_stream)
+        y = ys.sum(0) if sp > 1 else ys[0]
+        if a.shared_gate:
+            y = y * torch.sigmoid(h.float() @ self.w.shared_gate[l].float().t())
+        return y
 
     def _map_addr(self, phys: int) -> int:
         return self.maps_dev.data_ptr() + int(phys) * 256
@@ -356,6 +397,12 @@ class OffloadEngine:
                 ev.record(self.copy_stream)
             self.slot_ready[l] = ev
 
+        # ---- shared expert(s): dense SwiGLU over every token on the tensor cores,
+        # queued before the host starts the CPU experts so the two overlap
+        y_shared = None
+        if self.shared_map_ptr is not None:
+            y_shared = self._shared_ffn(l, h)
+
         # ---- CPU experts on the host worker
         tp3 = time.perf_counter()
         extra_dev = None
@@ -376,6 +423,8 @@ class OffloadEngine:
                                  y * torch.from_numpy(w_np[tok, slot])[:, None])
                 self.stats.cpu_expert_calls += 1
             extra_dev = extra.to(self.dev, non_blocking=True)
+        if y_shared is not None:
+            extra_dev = y_shared if extra_dev is None else extra_dev + y_shared
         tp4 = time.perf_counter()
         pr = self.stats.host_ms
         for key, v in (("launch_pre", tp1 - tp0), ("wait_decision", tp2 - tp1),

@@ -122,8 +122,31 @@ def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
     else:
         trans = 0.0
     nm = quantize_ms(non_moe_ms) if non_moe_ms is not None else 0.0
+    shared_ms = 0.0
+    if arch.num_shared_experts > 0:
+        # shared expert(s) at a decode-sized batch: always on the GPU (resident)
+        fs = arch.shared_ffn_dim
+        smp = np.zeros(256, dtype=np.uint8)
+        _lib.call("dali_expert_maps", weights.shared[0].data_ptr(), d, fs, smp.ctypes.data)
+        smd = torch.from_numpy(smp).to(dev)
+        sptr = torch.tensor([smd.data_ptr()], dtype=torch.int64, device=dev)
+        w = 1
+        xs = torch.randn(w, d, device=dev).to(torch.bfloat16)
+        offs = torch.tensor([0, w], dtype=torch.int32, device=dev)
+        hs = torch.empty((w, fs), dtype=torch.bfloat16, device=dev)
+        ys = torch.empty((1, w, d), dtype=torch.float32, device=dev)
+        ts = []
+        for _ in range(reps + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            _lib.call("dali_expert_ffn_tc", xs.data_ptr(), offs.data_ptr(), 1, sptr.data_ptr(),
+                      d, fs, w, w, 1, hs.data_ptr(), ys.data_ptr(), 1, cs.cuda_stream)
+            e1.record(cs)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        shared_ms = quantize_ms(statistics.median(ts[1:]))
     cpu = [(w, max(ms, 2.0 ** -12)) for w, ms in _monotone(cpu)]
     gpu = [(w, max(ms, 2.0 ** -12)) for w, ms in _monotone(gpu)]
     if log:
-        log(f"cost model: cpu {cpu} gpu {gpu} trans {trans} non_moe {nm}")
-    return fit_cost_model(cpu, gpu, trans, 0.0, nm)
+        log(f"cost model: cpu {cpu} gpu {gpu} trans {trans} non_moe {nm} shared {shared_ms}")
+    return fit_cost_model(cpu, gpu, trans, shared_ms, nm)

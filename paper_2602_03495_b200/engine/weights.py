@@ -29,6 +29,7 @@ from .. import _lib
 from .arch import MoEArch
 
 KIND_EMBED, KIND_LMHEAD, KIND_QKV, KIND_O, KIND_W13, KIND_W2 = 1, 2, 3, 4, 5, 6
+KIND_SH13, KIND_SH2, KIND_SHGATE = 7, 8, 9
 
 
 def tensor_seed(seed: int, kind: int, layer: int, index: int) -> int:
@@ -112,6 +113,18 @@ class ModelWeights:
         self.wo = [w((d, H * hd), KIND_O, l, 0, 1.0 / math.sqrt(H * hd))
                    for l in range(a.num_layers)]
         self.router64 = [router_weights(a, seed, l) for l in range(a.num_layers)]
+        # shared expert(s): one dense SwiGLU block per layer, always resident in HBM
+        self.shared = []
+        self.shared_gate = []
+        if a.num_shared_experts > 0:
+            fs = a.shared_ffn_dim
+            for l in range(a.num_layers):
+                blk = torch.empty((3 * fs * d,), dtype=bf, device=dev)
+                init_uniform_(blk[:2 * fs * d], tensor_seed(seed, KIND_SH13, l, 0), 1.0 / math.sqrt(d))
+                init_uniform_(blk[2 * fs * d:], tensor_seed(seed, KIND_SH2, l, 0), 1.0 / math.sqrt(fs))
+                self.shared.append(blk)
+                if a.shared_gate:
+                    self.shared_gate.append(w((1, d), KIND_SHGATE, l, 0, 1.0 / math.sqrt(d)))
         self.router = torch.stack([torch.from_numpy(r).to(bf) for r in self.router64]).to(dev)
 
         # routed experts

@@ -16,15 +16,20 @@ pytestmark = pytest.mark.gpu
 RTOL = 2e-2
 
 
-@pytest.fixture(scope="module")
-def eng():
+SHARED_MS = {"tiny": 0.0, "tiny-shared": 0.5}
+
+
+@pytest.fixture(scope="module", params=["tiny", "tiny-shared"])
+def eng(request):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2602_03495_b200.cost_model import default_cost_model
     from paper_2602_03495_b200.engine import EngineConfig, build_engine
-    cfg = EngineConfig(cache_slots_per_layer=2, prefetch_size=2, capture=True, seed=3)
-    return build_engine("tiny", cfg, seed=5,
-                        cost_model=default_cost_model(non_moe_layer_time=3.0), max_seq=128)
+    name = request.param
+    slots = 2 if name == "tiny" else 6
+    cfg = EngineConfig(cache_slots_per_layer=slots, prefetch_size=2, capture=True, seed=3)
+    cm = default_cost_model(shared_expert_gpu_time=SHARED_MS[name], non_moe_layer_time=3.0)
+    return build_engine(name, cfg, seed=5, cost_model=cm, max_seq=128)
 
 
 def _oracle_replay(eng, st):
@@ -39,11 +44,12 @@ def _oracle_replay(eng, st):
         wl = np.stack([st.workloads[(s, l)] for l in range(L)])
         steps.append(D.StepInput(ti, ntok, wl, hid, eos))
     gates = np.stack([eng.w.router[l].double().cpu().numpy() for l in range(L)])
-    dcfg = D.DriverConfig(tables=P.default_tables(non_moe_layer_time=3.0),
+    dcfg = D.DriverConfig(tables=P.default_tables(SHARED_MS[a.name], non_moe_layer_time=3.0),
                           prefetch_size=eng.cfg.prefetch_size, residuals=eng.residuals_np,
                           cache_capacity=eng.slots_per_layer, w_size=eng.cfg.w_size,
                           u_size=eng.cfg.u_size, seed=eng.cfg.seed,
-                          initial_on_gpu=st.initial_on_gpu)
+                          initial_on_gpu=st.initial_on_gpu,
+                          num_shared_experts=a.num_shared_experts)
     return steps, gates, D.run(steps, gates, dcfg, L, N, k)
 
 
