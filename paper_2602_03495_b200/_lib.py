@@ -83,6 +83,8 @@ SIGNATURES = {
     "dali_init_uniform_bf16": [_P, _I64, C.c_uint64, C.c_uint64, C.c_float, _P],
     "dali_host_alloc": [C.c_size_t, _I32, C.POINTER(C.c_void_p)],
     "dali_host_free": [_P, C.c_size_t],
+    "dali_host_alloc_shared": [C.c_size_t, _I32, _I32, C.POINTER(C.c_int32), _I32,
+                               C.POINTER(C.c_void_p)],
 }
 _RESTYPES = {"dali_last_error": C.c_char_p, "dali_version": C.c_int,
              "dali_launch_count": C.c_int64}
