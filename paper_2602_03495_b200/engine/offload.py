@@ -144,8 +144,9 @@ class OffloadEngine:
         self.cpu_threads = cfg.cpu_threads or len(os.sched_getaffinity(0))
         torch.set_num_threads(self.cpu_threads)
         # per-layer pinned scratch for pointer table + G mask
-        self.ptr_host = torch.zeros((L, N * 16 + N), dtype=torch.uint8, pin_memory=True)
-        self.ptr_dev = torch.zeros((L, N * 16 + N), dtype=torch.uint8, device=self.dev)
+        row = (N * 17 + 63) // 64 * 64        # ptrs | maps | G mask, 64-B aligned rows
+        self.ptr_host = torch.zeros((L, row), dtype=torch.uint8, pin_memory=True)
+        self.ptr_dev = torch.zeros((L, row), dtype=torch.uint8, device=self.dev)
         self.rope = Rope(a, max_seq, self.dev)
         self.max_batch, self.max_seq = max_batch, max_seq
         self.kv = None
@@ -331,7 +332,7 @@ class OffloadEngine:
         ph[:N * 8].view(torch.int64).copy_(torch.from_numpy(ptrs.view(np.int64)))
         ph[N * 8:N * 16].view(torch.int64).copy_(torch.from_numpy(maps.view(np.int64)))
         gm = np.array(rec.G[:N], dtype=np.int8)
-        ph[N * 16:].copy_(torch.from_numpy(gm.view(np.uint8)))
+        ph[N * 16:N * 17].copy_(torch.from_numpy(gm.view(np.uint8)))
         pd = self.ptr_dev[l]
         pd.copy_(ph, non_blocking=True)
         wl_np = self.stats.workloads[(step, l)]
