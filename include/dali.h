@@ -263,6 +263,13 @@ int dali_unpermute_combine(const uint16_t* x, const float* yp,
                            int32_t d, int32_t splits, int64_t rows,
                            uint16_t* out, void* stream);
 
+/* Engine plumbing: fused residual add + RMSNorm over (T, d) bf16 rows:
+ *   x_out = x + a (a may be NULL: x_out untouched, x used as is);
+ *   h = bf16(bf16(x_out * rsqrt(mean(x_out^2) + eps)) * w). */
+int dali_add_rmsnorm(const uint16_t* x, const uint16_t* a, const uint16_t* w,
+                     float eps, int64_t T, int32_t d, uint16_t* x_out,
+                     uint16_t* h, void* stream);
+
 /* Deterministic counter-hash weight init (uniform, given std):
  * out[i] = bf16(std * sqrt(3) * (2*u(seed, offset+i) - 1)). */
 int dali_init_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed,

@@ -83,6 +83,7 @@ SIGNATURES = {
     "dali_init_uniform_bf16": [_P, _I64, C.c_uint64, C.c_uint64, C.c_float, _P],
     "dali_host_alloc": [C.c_size_t, _I32, C.POINTER(C.c_void_p)],
     "dali_host_free": [_P, C.c_size_t],
+    "dali_add_rmsnorm": [_P, _P, _P, C.c_float, _I64, _I32, _P, _P, _P],
     "dali_host_alloc_shared": [C.c_size_t, _I32, _I32, C.POINTER(C.c_int32), _I32,
                                C.POINTER(C.c_void_p)],
 }

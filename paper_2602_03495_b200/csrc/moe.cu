@@ -350,3 +350,93 @@ extern "C" int dali_expert_ffn(const uint16_t* xp, const int32_t* offsets, int32
   (void)max_rows_per_expert;
   return dali_expert_ffn_simt(xp, offsets, N, expert_ptr, d, f, hbuf, yp, stream);
 }
+
+// ---------------------------------------------------------------------------
+// Fused residual add + RMSNorm (engine plumbing around the MoE layer):
+//   x_out = x (+ a);  h = bf16(x_out * rsqrt(mean(x_out^2) + eps)) * w
+// one CTA per row, 8 bf16 per thread step, fp32 statistics.
+// ---------------------------------------------------------------------------
+namespace dali {
+__global__ void add_rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ a,
+                                   const uint16_t* __restrict__ w, float eps, int d,
+                                   uint16_t* __restrict__ x_out, uint16_t* __restrict__ h) {
+  const int64_t row = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * d);
+  const uint4* ar = a ? reinterpret_cast<const uint4*>(a + row * d) : nullptr;
+  const int d8 = d >> 3;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < d8; c += blockDim.x) {
+    uint4 xv = xr[c];
+    uint32_t* xw = reinterpret_cast<uint32_t*>(&xv);
+    if (ar) {
+      const uint4 av = ar[c];
+      const uint32_t* aw = reinterpret_cast<const uint32_t*>(&av);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float lo = __uint_as_float(xw[q] << 16) + __uint_as_float(aw[q] << 16);
+        const float hi = __uint_as_float(xw[q] & 0xffff0000u) + __uint_as_float(aw[q] & 0xffff0000u);
+        xw[q] = (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
+      }
+      if (x_out) reinterpret_cast<uint4*>(x_out + row * d)[c] = xv;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float lo = __uint_as_float(xw[q] << 16), hi = __uint_as_float(xw[q] & 0xffff0000u);
+      ss += lo * lo + hi * hi;
+    }
+  }
+  __shared__ float red[32];
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / (float)d + eps);
+  const uint4* src = (ar && x_out) ? reinterpret_cast<const uint4*>(x_out + row * d) : xr;
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  for (int c = threadIdx.x; c < d8; c += blockDim.x) {
+    uint4 xv = src[c];
+    if (ar && !x_out) {
+      const uint4 av = ar[c];
+      uint32_t* xw = reinterpret_cast<uint32_t*>(&xv);
+      const uint32_t* aw = reinterpret_cast<const uint32_t*>(&av);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float lo = __uint_as_float(xw[q] << 16) + __uint_as_float(aw[q] << 16);
+        const float hi = __uint_as_float(xw[q] & 0xffff0000u) + __uint_as_float(aw[q] & 0xffff0000u);
+        xw[q] = (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
+      }
+    }
+    const uint4 wv = wr[c];
+    const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xv);
+    const uint32_t* ww = reinterpret_cast<const uint32_t*>(&wv);
+    uint4 ov;
+    uint32_t* ow = reinterpret_cast<uint32_t*>(&ov);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      // torch order: bf16(x * r) then * w (bf16 product rounded)
+      const float lo = __uint_as_float((uint32_t)f32_to_bf16_bits(__uint_as_float(xw[q] << 16) * r) << 16) *
+                       __uint_as_float(ww[q] << 16);
+      const float hi = __uint_as_float((uint32_t)f32_to_bf16_bits(__uint_as_float(xw[q] & 0xffff0000u) * r) << 16) *
+                       __uint_as_float(ww[q] & 0xffff0000u);
+      ow[q] = (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
+    }
+    reinterpret_cast<uint4*>(h + row * d)[c] = ov;
+  }
+}
+}  // namespace dali
+
+extern "C" int dali_add_rmsnorm(const uint16_t* x, const uint16_t* a, const uint16_t* w, float eps,
+                                int64_t T, int32_t d, uint16_t* x_out, uint16_t* h,
+                                void* stream) {
+  DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
+  if (T <= 0) return DALI_OK;
+  dali::add_rmsnorm_kernel<<<(unsigned)T, 256, 0, dali::as_stream(stream)>>>(x, a, w, eps, d, x_out,
+                                                                             h);
+  DALI_LAUNCH_CHECK("add_rmsnorm_kernel");
+  return DALI_OK;
+}

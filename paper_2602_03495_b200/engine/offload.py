@@ -166,6 +166,7 @@ class OffloadEngine:
                 [self.shared_maps_dev[l].data_ptr() for l in range(L)], dtype=torch.int64,
                 device=self.dev)
         self._offs_cache: dict = {}
+        self._wsd: dict = {}
         self.n_sm = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._load_initial_cache()
 
@@ -204,8 +205,8 @@ class OffloadEngine:
                 sp = s
                 if tiles * s >= 2 * self.n_sm:
                     break
-        hs = torch.empty((T, fs), dtype=torch.bfloat16, device=self.dev)
-        ys = torch.empty((sp, T, d), dtype=torch.float32, device=self.dev)
+        hs = self._ws("sh_h", (T, fs), torch.bfloat16)
+        ys = self._ws("sh_y", (sp, T, d), torch.float32)
         cs = torch.cuda.current_stream()
         _lib.call("dali_expert_ffn_tc", h.data_ptr(), offs.data_ptr(), 1,
                   self.shared_map_ptr.data_ptr() + 8 * l, d, fs, T, T, 1, hs.data_ptr(),
@@ -214,6 +215,18 @@ class OffloadEngine:
         if a.shared_gate:
             y = y * torch.sigmoid(h.float() @ self.w.shared_gate[l].float().t())
         return y
+
+    def _ws(self, name: str, shape: tuple, dtype, pinned: bool = False) -> torch.Tensor:
+        """Per-engine workspace reused across layers/steps (stream-ordered on
+        the compute stream; pinned ones are rewritten only after the event
+        wait that follows their previous consumer)."""
+        key = (name, shape, dtype)
+        t = self._wsd.get(key)
+        if t is None:
+            t = (torch.empty(shape, dtype=dtype, pin_memory=True) if pinned
+                 else torch.empty(shape, dtype=dtype, device=self.dev))
+            self._wsd[key] = t
+        return t
 
     def _map_addr(self, phys: int) -> int:
         return self.maps_dev.data_ptr() + int(phys) * 256
@@ -268,26 +281,32 @@ class OffloadEngine:
         T = h.shape[0]
         cs = torch.cuda.current_stream()
         tp0 = time.perf_counter()
-        idx, wts, wl = route_device(h, self.w.router[l], k, renorm=a.norm_topk_prob)
+        # routing outputs live in one device block [wl | idx | wts] so a single
+        # D2H moves them to the host worker's pinned mirror
+        nb = N * 8 + T * k * 8
+        rblk = self._ws("route", (nb,), torch.uint8)
+        wl = rblk[:N * 8].view(torch.int64)
+        idx = rblk[N * 8:N * 8 + T * k * 4].view(torch.int32).view(T, k)
+        wts = rblk[N * 8 + T * k * 4:].view(torch.float32).view(T, k)
+        route_device(h, self.w.router[l], k, renorm=a.norm_topk_prob, out=(idx, wts, wl))
         gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
         ri = self.policy.layer_step(step, l, token_index, is_eos, wl, h, gate_next)
-        offsets = torch.empty((N + 1,), dtype=torch.int32, device=self.dev)
-        perm = torch.empty((T * k,), dtype=torch.int32, device=self.dev)
-        pos = torch.empty((T, k), dtype=torch.int32, device=self.dev)
+        offsets = self._ws("offsets", (N + 1,), torch.int32)
+        perm = self._ws("perm", (T * k,), torch.int32)
+        pos = self._ws("pos", (T, k), torch.int32)
         _lib.call("dali_moe_plan", idx.data_ptr(), T, k, N, offsets.data_ptr(), perm.data_ptr(),
                   pos.data_ptr(), cs.cuda_stream)
-        xp = torch.empty((T * k, d), dtype=torch.bfloat16, device=self.dev)
+        xp = self._ws("xp", (T * k, d), torch.bfloat16)
         _lib.call("dali_permute", h.data_ptr(), perm.data_ptr(), T * k, d, xp.data_ptr(),
                   cs.cuda_stream)
         # host copies for the CPU worker (small; needed before the decision is known)
-        h_host = torch.empty((T, d), dtype=torch.bfloat16, pin_memory=True)
-        idx_host = torch.empty((T, k), dtype=torch.int32, pin_memory=True)
-        w_host = torch.empty((T, k), dtype=torch.float32, pin_memory=True)
+        rblk_host = self._ws("route_h", (nb,), torch.uint8, pinned=True)
+        h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
+        rblk_host.copy_(rblk, non_blocking=True)
         h_host.copy_(h, non_blocking=True)
-        idx_host.copy_(idx, non_blocking=True)
-        w_host.copy_(wts, non_blocking=True)
-        wl_host = torch.empty((N,), dtype=torch.int64, pin_memory=True)
-        wl_host.copy_(wl, non_blocking=True)
+        wl_host = rblk_host[:N * 8].view(torch.int64)
+        idx_host = rblk_host[N * 8:N * 8 + T * k * 4].view(torch.int32).view(T, k)
+        w_host = rblk_host[N * 8 + T * k * 4:].view(torch.float32).view(T, k)
         ev_dec = torch.cuda.Event()
         ev_dec.record(cs)
         tp1 = time.perf_counter()
@@ -343,11 +362,11 @@ class OffloadEngine:
                 else 128 if max_rows <= 128 else 256
             tiles = sum((int(wl_np[e]) + bn - 1) // bn for e in G) * (d // 128)
             splits = self._splits_for(tiles)
-        yp = torch.empty((splits, T * k, d), dtype=torch.float32, device=self.dev)
+        yp = self._ws("yp", (splits, T * k, d), torch.float32)
         if G:
             for ev in waits:
                 cs.wait_event(ev)
-            hbuf = torch.empty((T * k, f), dtype=torch.bfloat16, device=self.dev)
+            hbuf = self._ws("hbuf", (T * k, f), torch.bfloat16)
             if self.cfg.time_ffn:
                 t0 = torch.cuda.Event(enable_timing=True)
                 t0.record(cs)
@@ -408,7 +427,8 @@ class OffloadEngine:
         tp3 = time.perf_counter()
         extra_dev = None
         if Cx:
-            extra = torch.zeros((T, d), dtype=torch.float32, pin_memory=True)
+            extra = self._ws("extra_h", (T, d), torch.float32, pinned=True)
+            extra.zero_()
             idx_np = idx_host.numpy()
             w_np = w_host.numpy()
             for e in Cx:
@@ -444,11 +464,18 @@ class OffloadEngine:
                  token_index: int, is_eos: bool) -> torch.Tensor:
         a, W = self.arch, self.w
         x = W.embed[tokens_dev.reshape(-1)]
+        T, d = x.shape
+        sp = torch.cuda.current_stream().cuda_stream
+        hn = self._ws("hn", (T, d), torch.bfloat16)
+        h = self._ws("h", (T, d), torch.bfloat16)
         for l in range(a.num_layers):
-            hn = rms_norm(x, W.attn_norm[l], a.rms_eps)
-            x = x + attention(a, hn, W.wqkv[l], W.wo[l], self.rope, self.kv, l, B, S, pos0)
-            h = rms_norm(x, W.moe_norm[l], a.rms_eps).contiguous()
-            x = self._moe(l, x, h, step, token_index, is_eos)
+            _lib.call("dali_add_rmsnorm", x.data_ptr(), None, W.attn_norm[l].data_ptr(),
+                      a.rms_eps, T, d, None, hn.data_ptr(), sp)
+            att = attention(a, hn, W.wqkv[l], W.wo[l], self.rope, self.kv, l, B, S, pos0)
+            x2 = torch.empty_like(x)
+            _lib.call("dali_add_rmsnorm", x.data_ptr(), att.data_ptr(), W.moe_norm[l].data_ptr(),
+                      a.rms_eps, T, d, x2.data_ptr(), h.data_ptr(), sp)
+            x = self._moe(l, x2, h, step, token_index, is_eos)
         last = x.view(B, S, -1)[:, -1]
         return rms_norm(last, W.final_norm, a.rms_eps) @ W.lm_head.t()
 

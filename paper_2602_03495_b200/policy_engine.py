@@ -138,7 +138,8 @@ class PolicyEngine:
             if hidden is None or gate_next is None:
                 raise SimulationError("prefetching requires the layer's gate inputs")
             _, _, wl = route_device(hidden, gate_next, self.k, residual=self.residuals[layer],
-                                    want_idx=False, want_weights=False, stream=stream)
+                                    want_idx=False, want_weights=False, stream=stream,
+                                    out=(None, None, self.predicted))
             self.predicted = wl
             pred_p = wl.data_ptr()
         i = self.n_records

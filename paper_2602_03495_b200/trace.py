@@ -205,7 +205,7 @@ def topk_indices(scores, k: int) -> np.ndarray:
 
 def route_device(hidden: torch.Tensor, gate: torch.Tensor, k: int,
                  residual: torch.Tensor | None = None, renorm: bool = False,
-                 want_idx: bool = True, want_weights: bool = True, stream=None):
+                 want_idx: bool = True, want_weights: bool = True, stream=None, out=None):
     """Launch the fused routing kernel on device tensors.
 
     hidden (T, d) float64 or bfloat16; gate (d, N) same dtype family;
@@ -219,9 +219,12 @@ def route_device(hidden: torch.Tensor, gate: torch.Tensor, k: int,
     if not (1 <= k <= N):
         raise TraceError(f"top_k {k} out of range for {N} experts")
     dev = hidden.device
-    idx = torch.empty((T, k), dtype=torch.int32, device=dev) if want_idx else None
-    wts = torch.empty((T, k), dtype=torch.float32, device=dev) if want_weights else None
-    wl = torch.empty((N,), dtype=torch.int64, device=dev)
+    if out is not None:            # caller-owned (idx, wts, wl) workspaces
+        idx, wts, wl = out
+    else:
+        idx = torch.empty((T, k), dtype=torch.int32, device=dev) if want_idx else None
+        wts = torch.empty((T, k), dtype=torch.float32, device=dev) if want_weights else None
+        wl = torch.empty((N,), dtype=torch.int64, device=dev)
     res_p = _dev.ptr(residual)
     if hidden.dtype == torch.float64:
         fn = "dali_route_f64"
