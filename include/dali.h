@@ -250,17 +250,20 @@ int dali_expert_ffn_tc(const uint16_t* xp, const int32_t* offsets, int32_t N,
 int dali_expert_maps(const void* block, int32_t d, int32_t f, void* out);
 
 /* Eq. (2) combine fused with the residual add and 128-bit scatter:
- *   out[t,:] = x[t,:] + sum_{j: gpu_mask[idx[t,j]]} w[t,j] *
- *              sum_{s<splits} yp[s][pos[t,j],:]  (+ extra[t,:])
- * x, out [dev] (T,d) bf16 (may alias); yp splits x (rows,d) f32; topk_idx /
- * pos / topk_w (T,k); gpu_mask [dev] (N,) int8 (the G vector; NULL = all
- * experts); extra (T,d) f32 partial output of the CPU-assigned experts or
- * NULL. */
+ *   out[t,:] = x[t,:] + sum_j w[t,j] * row(t,j) (+ extra[t,:]),
+ *   row(t,j) = sum_{s<splits} yp[s][pos[t,j],:]   if gpu_mask == NULL or
+ *                                                 gpu_mask[idx[t,j]] (GPU expert)
+ *            = cpu_rows[pos[t,j],:]               otherwise, if cpu_rows != NULL
+ *              (rows the host worker computed for CPU-assigned experts)
+ * x, out [dev] (T,d) bf16 (may alias); yp splits x (rows,d) f32; cpu_rows
+ * (rows,d) f32 or NULL; topk_idx / pos / topk_w (T,k); gpu_mask [dev] (N,)
+ * int8 (the G vector); extra (T,d) f32 token-level addend (shared experts)
+ * or NULL. */
 int dali_unpermute_combine(const uint16_t* x, const float* yp,
                            const int32_t* topk_idx, const int32_t* pos,
                            const float* topk_w, const int8_t* gpu_mask,
-                           const float* extra, int64_t T, int32_t k,
-                           int32_t d, int32_t splits, int64_t rows,
+                           const float* cpu_rows, const float* extra, int64_t T,
+                           int32_t k, int32_t d, int32_t splits, int64_t rows,
                            uint16_t* out, void* stream);
 
 /* Engine plumbing: fused residual add + RMSNorm over (T, d) bf16 rows:

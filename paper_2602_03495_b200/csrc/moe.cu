@@ -199,6 +199,7 @@ ffn_down_simt(const uint16_t* __restrict__ h, const int32_t* __restrict__ offset
 __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __restrict__ yp,
                                const int32_t* __restrict__ idx, const int32_t* __restrict__ pos,
                                const float* __restrict__ wts, const int8_t* __restrict__ mask,
+                               const float* __restrict__ cpu_rows,
                                const float* __restrict__ extra, int64_t T, int k, int d,
                                int splits, int64_t plane, uint16_t* __restrict__ out) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -211,16 +212,25 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.f;
       for (int j = 0; j < k; ++j) {
-        if (mask && !mask[idx[t * k + j]]) continue;
+        const bool on_gpu = !mask || mask[idx[t * k + j]];
+        if (!on_gpu && !cpu_rows) continue;
         const float g = wts[t * k + j];
-        const float4* src = reinterpret_cast<const float4*>(yp + (int64_t)pos[t * k + j] * d) + 2 * c;
-        float4 a = src[0], b = src[1];
-        for (int s = 1; s < splits; ++s) {           // split-K planes, fixed order
-          const float4* q = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src) +
-                                                            s * plane);
-          const float4 a2 = q[0], b2 = q[1];
-          a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
-          b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
+        const int64_t r = (int64_t)pos[t * k + j] * d;
+        float4 a, b;
+        if (on_gpu) {
+          const float4* src = reinterpret_cast<const float4*>(yp + r) + 2 * c;
+          a = src[0];
+          b = src[1];
+          for (int s = 1; s < splits; ++s) {           // split-K planes, fixed order
+            const float4* q = reinterpret_cast<const float4*>(yp + s * plane + r) + 2 * c;
+            const float4 a2 = q[0], b2 = q[1];
+            a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
+            b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
+          }
+        } else {                                       // row computed by the CPU worker
+          const float4* src = reinterpret_cast<const float4*>(cpu_rows + r) + 2 * c;
+          a = src[0];
+          b = src[1];
         }
         acc[0] = fmaf(g, a.x, acc[0]); acc[1] = fmaf(g, a.y, acc[1]);
         acc[2] = fmaf(g, a.z, acc[2]); acc[3] = fmaf(g, a.w, acc[3]);
@@ -318,14 +328,16 @@ extern "C" int dali_expert_ffn_simt(const uint16_t* xp, const int32_t* offsets, 
 
 extern "C" int dali_unpermute_combine(const uint16_t* x, const float* yp, const int32_t* topk_idx,
                                       const int32_t* pos, const float* topk_w,
-                                      const int8_t* gpu_mask, const float* extra, int64_t T,
-                                      int32_t k, int32_t d, int32_t splits, int64_t rows,
-                                      uint16_t* out, void* stream) {
+                                      const int8_t* gpu_mask, const float* cpu_rows,
+                                      const float* extra, int64_t T, int32_t k, int32_t d,
+                                      int32_t splits, int64_t rows, uint16_t* out,
+                                      void* stream) {
   DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
   if (T <= 0) return DALI_OK;
   const int64_t blocks = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 8);
   combine_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(x, yp, topk_idx, pos, topk_w,
-                                                                  gpu_mask, extra, T, k, d,
+                                                                  gpu_mask, cpu_rows, extra, T, k,
+                                                                  d,
                                                                   splits < 1 ? 1 : splits,
                                                                   rows * (int64_t)d, out);
   DALI_LAUNCH_CHECK("combine_kernel");

@@ -109,11 +109,18 @@ class _Staging:
 class OffloadEngine:
     def __init__(self, arch: MoEArch, weights: ModelWeights, cost_model: CostModel,
                  cfg: EngineConfig, residuals: np.ndarray | None = None,
-                 max_batch: int = 1, max_seq: int = 1024):
+                 max_batch: int = 1, max_seq: int = 1024, ep=None):
         self.arch, self.w, self.cm, self.cfg = arch, weights, cost_model, cfg
+        self.ep = ep                        # EPGroup or None (see ep.py)
+        self.NL = weights.n_local           # routed experts held by this rank
         self.dev = torch.device("cuda", torch.cuda.current_device())
         a = arch
-        L, N, k, d, f = a.num_layers, a.num_experts, a.top_k, a.hidden_dim, a.ffn_dim
+        L, k, d, f = a.num_layers, a.top_k, a.hidden_dim, a.ffn_dim
+        N = self.NL
+        if ep is not None and weights.experts != ep.local_experts:
+            raise SimulationError("weights must hold this rank's expert shard")
+        if ep is None and self.NL != a.num_experts:
+            raise SimulationError("an expert shard needs an EPGroup")
         self.resident_mode = weights.resident
         slots = cfg.cache_slots_per_layer
         if cfg.cache_gb is not None:
@@ -177,7 +184,7 @@ class OffloadEngine:
         a = self.arch
         if self.resident_mode:
             addrs = [self.w.expert_dev(l, e).data_ptr() for l in range(a.num_layers)
-                     for e in range(a.num_experts)]
+                     for e in range(self.NL)]
         else:
             addrs = [self.cache_buf[s].data_ptr() for s in range(self.n_cache_slots)]
             addrs += [self.staging.ptr(i) for i in range(len(self.staging.free))]
@@ -247,7 +254,7 @@ class OffloadEngine:
             return
         with torch.cuda.stream(self.copy_stream):
             for l in range(self.arch.num_layers):
-                for e in range(self.arch.num_experts):
+                for e in range(self.NL):
                     s = self.host_slot[l, e]
                     if s >= 0:
                         self.cache_buf[s].copy_(self.w.host.bytes[
@@ -274,56 +281,63 @@ class OffloadEngine:
         return i, ev
 
     # ------------------------------------------------------------- MoE layer
-    def _moe(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, token_index: int,
-             is_eos: bool) -> torch.Tensor:
+    def _route(self, l: int, h: torch.Tensor):
+        """Route kernel + plan + permute for this rank's T tokens.  Outputs live
+        in one device block [wl (N i64) | offsets (N+1 i32, padded) | idx | wts]
+        mirrored to pinned host memory by one D2H after the decision."""
         a = self.arch
-        N, k, d, f = a.num_experts, a.top_k, a.hidden_dim, a.ffn_dim
+        N, k, d = a.num_experts, a.top_k, a.hidden_dim
         T = h.shape[0]
         cs = torch.cuda.current_stream()
-        tp0 = time.perf_counter()
-        # routing outputs live in one device block [wl | idx | wts] so a single
-        # D2H moves them to the host worker's pinned mirror
-        nb = N * 8 + T * k * 8
+        o_off = N * 8
+        o_idx = o_off + ((N + 1) * 4 + 7) // 8 * 8
+        o_w = o_idx + T * k * 4
+        nb = o_w + T * k * 4
         rblk = self._ws("route", (nb,), torch.uint8)
-        wl = rblk[:N * 8].view(torch.int64)
-        idx = rblk[N * 8:N * 8 + T * k * 4].view(torch.int32).view(T, k)
-        wts = rblk[N * 8 + T * k * 4:].view(torch.float32).view(T, k)
-        route_device(h, self.w.router[l], k, renorm=a.norm_topk_prob, out=(idx, wts, wl))
-        gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
-        ri = self.policy.layer_step(step, l, token_index, is_eos, wl, h, gate_next)
-        offsets = self._ws("offsets", (N + 1,), torch.int32)
+        v = {
+            "wl": rblk[:o_off].view(torch.int64),
+            "offsets": rblk[o_off:o_off + (N + 1) * 4].view(torch.int32),
+            "idx": rblk[o_idx:o_w].view(torch.int32).view(T, k),
+            "wts": rblk[o_w:nb].view(torch.float32).view(T, k),
+        }
+        route_device(h, self.w.router[l], k, renorm=a.norm_topk_prob,
+                     out=(v["idx"], v["wts"], v["wl"]))
         perm = self._ws("perm", (T * k,), torch.int32)
-        pos = self._ws("pos", (T, k), torch.int32)
-        _lib.call("dali_moe_plan", idx.data_ptr(), T, k, N, offsets.data_ptr(), perm.data_ptr(),
-                  pos.data_ptr(), cs.cuda_stream)
-        xp = self._ws("xp", (T * k, d), torch.bfloat16)
-        _lib.call("dali_permute", h.data_ptr(), perm.data_ptr(), T * k, d, xp.data_ptr(),
+        v["pos"] = self._ws("pos", (T, k), torch.int32)
+        _lib.call("dali_moe_plan", v["idx"].data_ptr(), T, k, N, v["offsets"].data_ptr(),
+                  perm.data_ptr(), v["pos"].data_ptr(), cs.cuda_stream)
+        v["xp"] = self._ws("xp", (T * k, d), torch.bfloat16)
+        _lib.call("dali_permute", h.data_ptr(), perm.data_ptr(), T * k, d, v["xp"].data_ptr(),
                   cs.cuda_stream)
-        # host copies for the CPU worker (small; needed before the decision is known)
-        rblk_host = self._ws("route_h", (nb,), torch.uint8, pinned=True)
-        h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
-        rblk_host.copy_(rblk, non_blocking=True)
-        h_host.copy_(h, non_blocking=True)
-        wl_host = rblk_host[:N * 8].view(torch.int64)
-        idx_host = rblk_host[N * 8:N * 8 + T * k * 4].view(torch.int32).view(T, k)
-        w_host = rblk_host[N * 8 + T * k * 4:].view(torch.float32).view(T, k)
-        ev_dec = torch.cuda.Event()
-        ev_dec.record(cs)
-        tp1 = time.perf_counter()
-        ev_dec.synchronize()
-        tp2 = time.perf_counter()
-        rec = self.policy.record(ri)
-        self.stats.workloads[(step, l)] = wl_host.numpy().copy()
-        if self.cfg.capture:
-            self.stats.captured.append((step, l, h_host.clone()))
-            self.stats.topk[(step, l)] = idx_host.numpy().astype(np.int64).copy()
+        v["blk"], v["layout"] = rblk, (o_off, o_idx, o_w, nb)
+        return v
 
-        G = [e for e in range(N) if rec.G[e]]
-        Cx = [e for e in range(N) if rec.C[e]]
-        # ---- GPU experts: locate or fetch weights (raw block pointer + the
-        # physical slot's tensor-map pair for the tcgen05 path)
-        ptrs = np.zeros(N, dtype=np.uint64)
-        maps = np.zeros(N, dtype=np.uint64)
+    def _host_view(self, v, T: int):
+        """Pinned host mirror of the routing block (valid after the event wait)."""
+        N, k = self.arch.num_experts, self.arch.top_k
+        o_off, o_idx, o_w, nb = v["layout"]
+        hb = self._ws("route_h", (nb,), torch.uint8, pinned=True)
+        hb.copy_(v["blk"], non_blocking=True)
+        return {
+            "wl": hb[:o_off].view(torch.int64),
+            "offsets": hb[o_off:o_off + (N + 1) * 4].view(torch.int32),
+            "idx": hb[o_idx:o_w].view(torch.int32).view(T, k),
+            "wts": hb[o_w:nb].view(torch.float32).view(T, k),
+        }
+
+    def _exec_local(self, l: int, xrows: torch.Tensor, offsets: torch.Tensor,
+                    wl_np: np.ndarray, rec, R: int):
+        """GPU side of the local experts' decision: locate (cache slot /
+        prefetch staging) or demand-fetch each GPU expert's weights, run the
+        grouped FFN over ``xrows`` grouped by ``offsets``; issue the layer+1
+        prefetch copies and the cache replacement copies.  Returns
+        (yp planes, splits, G mask device pointer)."""
+        a = self.arch
+        NL, d, f = self.NL, a.hidden_dim, a.ffn_dim
+        cs = torch.cuda.current_stream()
+        G = [e for e in range(NL) if rec.G[e]]
+        ptrs = np.zeros(NL, dtype=np.uint64)
+        maps = np.zeros(NL, dtype=np.uint64)
         waits = []
         used_staging = []
         for e in G:
@@ -348,35 +362,36 @@ class OffloadEngine:
             waits.append(ev)
             used_staging.append(i)
         ph = self.ptr_host[l]
-        ph[:N * 8].view(torch.int64).copy_(torch.from_numpy(ptrs.view(np.int64)))
-        ph[N * 8:N * 16].view(torch.int64).copy_(torch.from_numpy(maps.view(np.int64)))
-        gm = np.array(rec.G[:N], dtype=np.int8)
-        ph[N * 16:N * 17].copy_(torch.from_numpy(gm.view(np.uint8)))
+        ph[:NL * 8].view(torch.int64).copy_(torch.from_numpy(ptrs.view(np.int64)))
+        ph[NL * 8:NL * 16].view(torch.int64).copy_(torch.from_numpy(maps.view(np.int64)))
+        gm = np.array(rec.G[:NL], dtype=np.int8)
+        ph[NL * 16:NL * 17].copy_(torch.from_numpy(gm.view(np.uint8)))
         pd = self.ptr_dev[l]
         pd.copy_(ph, non_blocking=True)
-        wl_np = self.stats.workloads[(step, l)]
         splits = 1
+        max_rows = 0
         if G and self.use_tc:
             max_rows = int(max(wl_np[e] for e in G))
             bn = 16 if max_rows <= 16 else 32 if max_rows <= 32 else 64 if max_rows <= 64 \
                 else 128 if max_rows <= 128 else 256
             tiles = sum((int(wl_np[e]) + bn - 1) // bn for e in G) * (d // 128)
             splits = self._splits_for(tiles)
-        yp = self._ws("yp", (splits, T * k, d), torch.float32)
-        if G:
+        yp = self._ws("yp", (splits, max(R, 1), d), torch.float32)
+        if G and R > 0:
             for ev in waits:
                 cs.wait_event(ev)
-            hbuf = self._ws("hbuf", (T * k, f), torch.bfloat16)
+            hbuf = self._ws("hbuf", (R, f), torch.bfloat16)
             if self.cfg.time_ffn:
                 t0 = torch.cuda.Event(enable_timing=True)
                 t0.record(cs)
             if self.use_tc:
-                _lib.call("dali_expert_ffn_tc", xp.data_ptr(), offsets.data_ptr(), N,
-                          pd.data_ptr() + N * 8, d, f, T * k, max_rows, len(G),
+                _lib.call("dali_expert_ffn_tc", xrows.data_ptr(), offsets.data_ptr(), NL,
+                          pd.data_ptr() + NL * 8, d, f, R, max_rows, len(G),
                           hbuf.data_ptr(), yp.data_ptr(), splits, cs.cuda_stream)
             else:
-                _lib.call("dali_expert_ffn", xp.data_ptr(), offsets.data_ptr(), N, pd.data_ptr(),
-                          d, f, T * k, T, hbuf.data_ptr(), yp.data_ptr(), cs.cuda_stream)
+                _lib.call("dali_expert_ffn", xrows.data_ptr(), offsets.data_ptr(), NL,
+                          pd.data_ptr(), d, f, R, R, hbuf.data_ptr(), yp.data_ptr(),
+                          cs.cuda_stream)
             if self.cfg.time_ffn:
                 t1 = torch.cuda.Event(enable_timing=True)
                 t1.record(cs)
@@ -389,74 +404,177 @@ class OffloadEngine:
         ffn_done.record(cs)
         for i in used_staging:
             self.staging.release(i, ffn_done)
-        # prefetched-but-unused entries for this layer are dropped
-        for key in [kk for kk in self.prefetched if kk[0] == l]:
+        for key in [kk for kk in self.prefetched if kk[0] == l]:   # granted but unused
             i, ev = self.prefetched.pop(key)
             self.staging.release(i, ev)
-
-        # ---- prefetch for layer+1: the arrivals the virtual clock granted
         if not self.resident_mode:
+            # prefetch for layer+1: the arrivals the virtual clock granted
             for j in range(rec.n_done):
                 e = int(rec.cand[j])
                 i, ev = self._copy_into_staging(l + 1, e)
                 self.prefetched[(l + 1, e)] = (i, ev)
                 self.stats.prefetch_copies += 1
+            # replacement: admitted experts into the victims' slots once read
+            if rec.ev_valid and rec.ev_n:
+                with torch.cuda.stream(self.copy_stream):
+                    self.copy_stream.wait_event(ffn_done)
+                    for j in range(rec.ev_n):
+                        v_, c_ = int(rec.evicted[j]), int(rec.admitted[j])
+                        s = self.host_slot[l, v_]
+                        self.cache_buf[s].copy_(self._host_block(l, c_), non_blocking=True)
+                        self.host_slot[l, c_], self.host_slot[l, v_] = s, -1
+                        self.stats.h2d_bytes += self.w.expert_bytes
+                        self.stats.replace_copies += 1
+                    ev = torch.cuda.Event()
+                    ev.record(self.copy_stream)
+                self.slot_ready[l] = ev
+        return yp, splits, pd.data_ptr() + NL * 16
 
-        # ---- replacement: admitted experts into the victims' slots
-        if rec.ev_valid and rec.ev_n and not self.resident_mode:
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_event(ffn_done)
-                for j in range(rec.ev_n):
-                    v, c = int(rec.evicted[j]), int(rec.admitted[j])
-                    s = self.host_slot[l, v]
-                    self.cache_buf[s].copy_(self._host_block(l, c), non_blocking=True)
-                    self.host_slot[l, c], self.host_slot[l, v] = s, -1
-                    self.stats.h2d_bytes += self.w.expert_bytes
-                    self.stats.replace_copies += 1
-                ev = torch.cuda.Event()
-                ev.record(self.copy_stream)
-            self.slot_ready[l] = ev
+    def _cpu_rows(self, l: int, rows_host: torch.Tensor, offs_np: np.ndarray, rec,
+                  R: int) -> torch.Tensor | None:
+        """CPU-assigned experts on the host worker: SwiGLU of each expert's
+        contiguous rows over the pinned store -> (R, d) f32 on the device
+        (rows of GPU experts are left unused)."""
+        a = self.arch
+        d, f = a.hidden_dim, a.ffn_dim
+        Cx = [e for e in range(self.NL) if rec.C[e]]
+        if not Cx or R == 0:
+            return None
+        out = self._ws("cpu_rows_h", (R, d), torch.float32, pinned=True)
+        for e in Cx:
+            r0, r1 = int(offs_np[e]), int(offs_np[e + 1])
+            if r1 <= r0:
+                continue
+            W13, W2 = self.w.split_expert(self._host_block(l, e).view(torch.bfloat16))
+            xr = rows_host[r0:r1]
+            n = r1 - r0
+            gu = (xr @ W13.t()).view(n, f // 64, 2, 64)
+            g = gu[:, :, 0, :].reshape(n, f).float()
+            u = gu[:, :, 1, :].reshape(n, f).float()
+            act = (torch.nn.functional.silu(g) * u).to(torch.bfloat16)
+            out[r0:r1].copy_((act @ W2.t()).float())
+            self.stats.cpu_expert_calls += 1
+        return out.to(self.dev, non_blocking=True)
 
-        # ---- shared expert(s): dense SwiGLU over every token on the tensor cores,
-        # queued before the host starts the CPU experts so the two overlap
-        y_shared = None
-        if self.shared_map_ptr is not None:
-            y_shared = self._shared_ffn(l, h)
-
-        # ---- CPU experts on the host worker
+    def _moe(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, token_index: int,
+             is_eos: bool) -> torch.Tensor:
+        if self.ep is not None:
+            return self._moe_ep(l, x, h, step, token_index, is_eos)
+        a = self.arch
+        N, k, d = a.num_experts, a.top_k, a.hidden_dim
+        T = h.shape[0]
+        R = T * k
+        cs = torch.cuda.current_stream()
+        tp0 = time.perf_counter()
+        v = self._route(l, h)
+        gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
+        ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], h, gate_next)
+        hv = self._host_view(v, T)
+        xp_host = self._ws("xp_h", (R, d), torch.bfloat16, pinned=True)
+        xp_host.copy_(v["xp"], non_blocking=True)
+        if self.cfg.capture:
+            h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
+            h_host.copy_(h, non_blocking=True)
+        ev_dec = torch.cuda.Event()
+        ev_dec.record(cs)
+        tp1 = time.perf_counter()
+        ev_dec.synchronize()
+        tp2 = time.perf_counter()
+        rec = self.policy.record(ri)
+        wl_np = hv["wl"].numpy().copy()
+        self.stats.workloads[(step, l)] = wl_np
+        if self.cfg.capture:
+            self.stats.captured.append((step, l, h_host.clone()))
+            self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
+        yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
+        # shared expert(s): queued before the host starts the CPU experts
+        y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
         tp3 = time.perf_counter()
-        extra_dev = None
-        if Cx:
-            extra = self._ws("extra_h", (T, d), torch.float32, pinned=True)
-            extra.zero_()
-            idx_np = idx_host.numpy()
-            w_np = w_host.numpy()
-            for e in Cx:
-                tok, slot = np.nonzero(idx_np == e)
-                W13, W2 = self.w.split_expert(self._host_block(l, e).view(torch.bfloat16))
-                xr = h_host[torch.from_numpy(tok)]
-                gu = (xr @ W13.t()).view(len(tok), f // 64, 2, 64)
-                g = gu[:, :, 0, :].reshape(len(tok), f).float()
-                u = gu[:, :, 1, :].reshape(len(tok), f).float()
-                act = (torch.nn.functional.silu(g) * u).to(torch.bfloat16)
-                y = (act @ W2.t()).float()
-                extra.index_add_(0, torch.from_numpy(tok),
-                                 y * torch.from_numpy(w_np[tok, slot])[:, None])
-                self.stats.cpu_expert_calls += 1
-            extra_dev = extra.to(self.dev, non_blocking=True)
-        if y_shared is not None:
-            extra_dev = y_shared if extra_dev is None else extra_dev + y_shared
+        cpu_rows = self._cpu_rows(l, xp_host, hv["offsets"].numpy(), rec, R)
         tp4 = time.perf_counter()
-        pr = self.stats.host_ms
-        for key, v in (("launch_pre", tp1 - tp0), ("wait_decision", tp2 - tp1),
-                       ("dispatch_gpu", tp3 - tp2), ("cpu_experts", tp4 - tp3)):
-            pr[key] = pr.get(key, 0.0) + v * 1e3
-
+        self._acct(tp0, tp1, tp2, tp3, tp4)
         out = torch.empty_like(x)
-        _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), idx.data_ptr(),
-                  pos.data_ptr(), wts.data_ptr(), pd[N * 16:].data_ptr(),
-                  extra_dev.data_ptr() if extra_dev is not None else None, T, k, d, splits,
-                  T * k, out.data_ptr(), cs.cuda_stream)
+        _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
+                  v["pos"].data_ptr(), v["wts"].data_ptr(), gmask_p,
+                  cpu_rows.data_ptr() if cpu_rows is not None else None,
+                  y_shared.data_ptr() if y_shared is not None else None, T, k, d, splits,
+                  R, out.data_ptr(), cs.cuda_stream)
+        return out
+
+    def _acct(self, tp0, tp1, tp2, tp3, tp4):
+        pr = self.stats.host_ms
+        for key, val in (("launch_pre", tp1 - tp0), ("wait_decision", tp2 - tp1),
+                         ("dispatch_gpu", tp3 - tp2), ("cpu_experts", tp4 - tp3)):
+            pr[key] = pr.get(key, 0.0) + val * 1e3
+
+    def _moe_ep(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, token_index: int,
+                is_eos: bool) -> torch.Tensor:
+        """Expert-parallel MoE layer (see ep.py): dispatch all-to-all, DALI
+        policy + execution on this rank's NL experts with global workloads,
+        return all-to-all, Eq. (2) combine on the source rank."""
+        from .ep import plan_regroup, send_sizes
+        a, ep = self.arch, self.ep
+        N, k, d, NL = a.num_experts, a.top_k, a.hidden_dim, self.NL
+        T = h.shape[0]
+        cs = torch.cuda.current_stream()
+        tp0 = time.perf_counter()
+        v = self._route(l, h)
+        recv_counts = ep.exchange_counts(v["wl"])                  # (G*NL,) int64
+        wl_glob = recv_counts.view(ep.world, NL).sum(0)
+        pred = None
+        if self.policy.prefetch_size > 0 and l + 1 < a.num_layers:
+            _, _, pw = route_device(h, self.w.router[l + 1], k, residual=self.policy.residuals[l],
+                                    want_idx=False, want_weights=False)
+            pred = ep.all_reduce_sum_(pw)[ep.rank * NL:(ep.rank + 1) * NL].contiguous()
+        ri = self.policy.layer_step(step, l, token_index, is_eos, wl_glob, None, None,
+                                    predicted=pred)
+        hv = self._host_view(v, T)
+        rc_host = self._ws("rc_h", (ep.world * NL,), torch.int64, pinned=True)
+        rc_host.copy_(recv_counts, non_blocking=True)
+        ev_dec = torch.cuda.Event()
+        ev_dec.record(cs)
+        tp1 = time.perf_counter()
+        ev_dec.synchronize()
+        tp2 = time.perf_counter()
+        rec = self.policy.record(ri)
+        rc = rc_host.numpy().reshape(ep.world, NL).copy()
+        wl_np = rc.sum(axis=0)
+        self.stats.workloads[(step, l)] = wl_np
+        perm2, offs_l, recv_sz = plan_regroup(rc)
+        snd_sz = send_sizes(hv["wl"].numpy(), ep.world)
+        recv_x = ep.exchange_rows(v["xp"], snd_sz, recv_sz)        # (R, d) bf16
+        R = int(recv_x.shape[0])
+        perm2_d = torch.from_numpy(perm2).to(self.dev, non_blocking=True)
+        offs_d = torch.from_numpy(offs_l).to(self.dev, non_blocking=True)
+        xl = self._ws("xl", (max(R, 1), d), torch.bfloat16)
+        if R:
+            _lib.call("dali_permute", recv_x.data_ptr(), perm2_d.data_ptr(), R, d, xl.data_ptr(),
+                      cs.cuda_stream)
+        yp, splits, _ = self._exec_local(l, xl, offs_d, wl_np, rec, R)
+        y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+        tp3 = time.perf_counter()
+        cpu_rows = None
+        if any(rec.C[e] for e in range(NL)) and R:
+            xl_host = self._ws("xl_h", (R, d), torch.bfloat16, pinned=True)
+            xl_host.copy_(xl[:R])
+            cpu_rows = self._cpu_rows(l, xl_host, offs_l, rec, R)
+        tp4 = time.perf_counter()
+        self._acct(tp0, tp1, tp2, tp3, tp4)
+        # per-row expert outputs in grouped order -> received order -> sources
+        y_l = yp[:, :R].sum(0) if splits > 1 else yp[0, :R].clone()
+        if cpu_rows is not None:
+            for e in range(NL):
+                if rec.C[e] and offs_l[e + 1] > offs_l[e]:
+                    y_l[offs_l[e]:offs_l[e + 1]] = cpu_rows[offs_l[e]:offs_l[e + 1]]
+        y_recv = torch.empty_like(y_l)
+        if R:
+            y_recv.index_copy_(0, perm2_d.long(), y_l)
+        y_back = ep.exchange_rows(y_recv, recv_sz, snd_sz)          # (T*k, d) f32
+        out = torch.empty_like(x)
+        _lib.call("dali_unpermute_combine", x.data_ptr(), y_back.data_ptr(), v["idx"].data_ptr(),
+                  v["pos"].data_ptr(), v["wts"].data_ptr(), None, None,
+                  y_shared.data_ptr() if y_shared is not None else None, T, k, d, 1, T * k,
+                  out.data_ptr(), cs.cuda_stream)
         return out
 
     # ------------------------------------------------------------- forward

@@ -92,7 +92,10 @@ class HostStore:
 class ModelWeights:
     def __init__(self, arch: MoEArch, seed: int = 0, device="cuda", resident: bool = False,
                  host_threads: int = 16, host_store: "HostStore | None" = None,
-                 fill_experts: bool = True):
+                 fill_experts: bool = True, experts: list | None = None):
+        """experts: the routed experts this process holds (expert-parallel
+        shard); default all.  Block (l, j) of the store is expert experts[j];
+        values depend only on (seed, layer, global expert id)."""
         self.arch, self.seed = arch, seed
         a = arch
         dev = torch.device(device)
@@ -129,7 +132,9 @@ class ModelWeights:
 
         # routed experts
         self.resident = resident
-        L, N, E = a.num_layers, a.num_experts, a.expert_elems
+        self.experts = list(range(a.num_experts)) if experts is None else list(experts)
+        self.n_local = len(self.experts)
+        L, N, E = a.num_layers, self.n_local, a.expert_elems
         self.expert_bytes = a.expert_bytes
         if resident:
             self.dev_store = torch.empty((L * N * E,), dtype=bf, device=dev)
@@ -152,12 +157,13 @@ class ModelWeights:
     def init_expert(self, l: int, e: int, out: torch.Tensor) -> torch.Tensor:
         a = self.arch
         n13 = 2 * a.ffn_dim * a.hidden_dim
-        init_uniform_(out[:n13], tensor_seed(self.seed, KIND_W13, l, e), 1.0 / math.sqrt(a.hidden_dim))
-        init_uniform_(out[n13:], tensor_seed(self.seed, KIND_W2, l, e), 1.0 / math.sqrt(a.ffn_dim))
+        ge = self.experts[e]              # global expert id -> seed
+        init_uniform_(out[:n13], tensor_seed(self.seed, KIND_W13, l, ge), 1.0 / math.sqrt(a.hidden_dim))
+        init_uniform_(out[n13:], tensor_seed(self.seed, KIND_W2, l, ge), 1.0 / math.sqrt(a.ffn_dim))
         return out
 
     def expert_index(self, l: int, e: int) -> int:
-        return l * self.arch.num_experts + e
+        return l * self.n_local + e
 
     def expert_host(self, l: int, e: int) -> torch.Tensor:
         """bf16 CPU view of block (l, e) in the pinned store."""

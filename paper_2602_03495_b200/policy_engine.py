@@ -127,14 +127,19 @@ class PolicyEngine:
 
     def layer_step(self, step: int, layer: int, token_index: int, is_eos: bool,
                    workloads: torch.Tensor, hidden: torch.Tensor | None,
-                   gate_next: torch.Tensor | None, stream=None) -> int:
+                   gate_next: torch.Tensor | None, stream=None,
+                   predicted: torch.Tensor | None = None) -> int:
         """Queue the decision of (step, layer) on ``stream``; returns the
-        record index (valid on the host once the stream reaches it)."""
+        record index (valid on the host once the stream reaches it).
+        ``predicted`` supplies layer+1's predicted workloads directly (the
+        expert-parallel path all-reduces them across ranks first)."""
         if self.n_records >= self.max_records:
             raise SimulationError("decision log full")
         sp = _dev.stream_ptr(stream)
         pred_p = None
-        if self.prefetch_size > 0 and layer < self.L - 1:
+        if predicted is not None and self.prefetch_size > 0 and layer < self.L - 1:
+            pred_p = predicted.data_ptr()
+        elif self.prefetch_size > 0 and layer < self.L - 1:
             if hidden is None or gate_next is None:
                 raise SimulationError("prefetching requires the layer's gate inputs")
             _, _, wl = route_device(hidden, gate_next, self.k, residual=self.residuals[layer],

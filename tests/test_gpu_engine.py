@@ -154,7 +154,7 @@ def test_engine_kernel_pieces_vs_torch():
               T * k, T, hbuf.data_ptr(), yp.data_ptr(), s)
     out = torch.empty_like(x)
     _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), idx.data_ptr(),
-              pos.data_ptr(), wts.data_ptr(), gmask.data_ptr(), None, T, k, d, 1, T * k,
+              pos.data_ptr(), wts.data_ptr(), gmask.data_ptr(), None, None, T, k, d, 1, T * k,
               out.data_ptr(), s)
     ref = x.float().cpu().clone()
     for t in range(T):
@@ -217,3 +217,45 @@ def test_tc_ffn_matches_simt_and_torch(d, f, counts, splits):
         torch.testing.assert_close(y_s[r0:r1].cpu(), ref, rtol=RTOL, atol=RTOL * scale)
         torch.testing.assert_close(h_tc[r0:r1].float(), h_s[r0:r1].float(), rtol=RTOL,
                                    atol=RTOL * h_s[r0:r1].float().abs().max().item())
+
+
+def test_engine_expert_parallel_path_world1():
+    """The EP code path (count/row all-to-alls over NCCL, receive-side regroup,
+    return exchange) at world_size 1 must reproduce the 1-GPU engine: same
+    decisions, same logits."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import socket
+
+    import torch.distributed as dist
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    from paper_2602_03495_b200.engine import calibrate_residuals_engine
+    from paper_2602_03495_b200.engine.ep import EPGroup
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                world_size=1, device_id=torch.device("cuda", 0))
+    arch = preset("tiny")
+    cm = default_cost_model(non_moe_layer_time=3.0)
+    w = ModelWeights(arch, seed=11)
+    prompts = torch.randint(0, arch.vocab_size, (1, 16), generator=torch.Generator().manual_seed(5))
+    res = calibrate_residuals_engine(arch, w, cm, prompts)
+    cfg = EngineConfig(cache_slots_per_layer=2, prefetch_size=1, capture=True, seed=3)
+    base = OffloadEngine(arch, w, cm, cfg, residuals=res, max_seq=128)
+    ep_eng = OffloadEngine(arch, w, cm, cfg, residuals=res, max_seq=128, ep=EPGroup(8))
+    p = torch.randint(0, arch.vocab_size, (2, 12), generator=torch.Generator().manual_seed(9))
+    t1, s1 = base.generate(p, 6)
+    d1 = base.policy.decision_log()
+    t2, s2 = ep_eng.generate(p, 6)
+    d2 = ep_eng.policy.decision_log()
+    assert len(d1) == len(d2)
+    for a_, b_ in zip(d1, d2):
+        assert np.array_equal(a_["C"], b_["C"]) and np.array_equal(a_["G"], b_["G"])
+        assert a_["event"] == b_["event"] and a_["done"] == b_["done"]
+    for l1, l2 in zip(s1.logits, s2.logits):
+        torch.testing.assert_close(l1, l2, rtol=1e-3, atol=1e-3 * l1.abs().max().item())
+    dist.destroy_process_group()
