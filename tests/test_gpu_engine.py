@@ -257,5 +257,6 @@ def test_engine_expert_parallel_path_world1():
         assert np.array_equal(a_["C"], b_["C"]) and np.array_equal(a_["G"], b_["G"])
         assert a_["event"] == b_["event"] and a_["done"] == b_["done"]
     for l1, l2 in zip(s1.logits, s2.logits):
-        torch.testing.assert_close(l1, l2, rtol=1e-3, atol=1e-3 * l1.abs().max().item())
+        # split-K planes are summed in a different place (bf16 residual rounding may flip)
+        torch.testing.assert_close(l1, l2, rtol=RTOL, atol=RTOL * l1.abs().max().item())
     dist.destroy_process_group()
