@@ -95,7 +95,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def dist_setup():
+def dist_setup(need_group: bool = False):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -105,6 +105,16 @@ def dist_setup():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
+        if need_group:                       # EP at one GPU: a world-1 NCCL group
+            import socket
+
+            import torch.distributed as dist
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                    world_size=1, device_id=torch.device("cuda", 0))
     return ws, rank, local
 
 
@@ -191,7 +201,9 @@ def config_dict(args, ws):
                         f"per request, B={args.batch}, expert cache {args.cache_gb} GB HBM, "
                         f"prefetch {args.prefetch}, w_size 4",
             "global_batch": args.batch * ws, "prefill": args.prefill, "decode": args.decode,
-            "cache_gb": args.cache_gb, "parallelism": f"replicas{ws}",
+            "cache_gb": args.cache_gb,
+            "parallelism": (f"ep{ws}" if args.ep else f"replicas{ws}") +
+                           ("-resident" if args.resident else ""),
             "l2": "working set (352 MB expert blocks streamed per layer) >> 126 MB L2; no flush"}
 
 
@@ -205,7 +217,12 @@ def run_dali(args, ws, rank, local):
     cfg = EngineConfig(cache_gb=args.cache_gb, prefetch_size=args.prefetch, w_size=4,
                        seed=0, time_ffn=True, cpu_threads=max(1, cores // local_ws))
     weights = None
-    if local_ws > 1:
+    ep = None
+    if args.ep:
+        from paper_2602_03495_b200.engine import preset
+        from paper_2602_03495_b200.engine.ep import EPGroup
+        ep = EPGroup(preset(args.model).num_experts)
+    if local_ws > 1 and ep is None and not args.resident:
         # one node-shared host expert store (memfd) filled once by local rank 0
         import torch.distributed as dist
         from paper_2602_03495_b200.engine import ModelWeights, preset
@@ -224,7 +241,7 @@ def run_dali(args, ws, rank, local):
         barrier(ws)
     eng = build_engine(args.model, cfg, seed=0, max_batch=args.batch,
                        max_seq=args.prefill + args.decode + 8, log=log if rank == 0 else None,
-                       weights=weights)
+                       weights=weights, ep=ep, resident=args.resident)
     log(f"rank {rank}: setup {time.time() - t_setup:.1f}s, slots/layer {eng.slots_per_layer}, "
         f"cost model {eng.cm.to_dict()}")
     V = eng.arch.vocab_size
@@ -358,8 +375,13 @@ def main():
     ap.add_argument("--cache-gb", type=float, default=24.0)
     ap.add_argument("--prefetch", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ep", action="store_true",
+                    help="expert parallelism: experts sharded over the ranks, tokens exchanged "
+                         "by NCCL all-to-all (each rank keeps its own request stream)")
+    ap.add_argument("--resident", action="store_true",
+                    help="all-resident mode: every (local) expert in HBM (roofline reference)")
     args = ap.parse_args()
-    ws, rank, local = dist_setup()
+    ws, rank, local = dist_setup(need_group=args.ep)
     if args.impl == "reference":
         run_reference(args, ws, rank)
     else:

@@ -14,14 +14,14 @@ from .weights import ModelWeights
 
 
 def calibrate_residuals_engine(arch: MoEArch, weights: ModelWeights, cost_model, prompts,
-                               max_seq: int = 1024) -> np.ndarray:
+                               max_seq: int = 1024, ep=None) -> np.ndarray:
     """On-GPU residual calibration (Eq. 11, prefetch.py:88-104 semantics):
     run calibration prompts through an all-GPU engine pass, capture every
     layer's gate input and average h_{l+1} - h_l over tokens in fp64."""
     eng = OffloadEngine(arch, weights, cost_model,
                         EngineConfig(capture=True, cache_slots_per_layer=0,
                                      assignment="greedy"),
-                        max_batch=prompts.shape[0], max_seq=max_seq)
+                        max_batch=prompts.shape[0], max_seq=max_seq, ep=ep)
     eng.generate(prompts, 1)
     L = arch.num_layers
     per_layer = {}
@@ -41,18 +41,22 @@ def calibrate_residuals_engine(arch: MoEArch, weights: ModelWeights, cost_model,
 def build_engine(name: str, cfg: EngineConfig, seed: int = 0, cost_model=None,
                  residuals: np.ndarray | None = None, resident: bool = False,
                  max_batch: int = 1, max_seq: int = 1024, calib_prompt_len: int = 64,
-                 log=None, weights: ModelWeights | None = None) -> OffloadEngine:
+                 log=None, weights: ModelWeights | None = None, ep=None) -> OffloadEngine:
+    """``ep``: an ``ep.EPGroup`` for expert parallelism (this rank then holds
+    only its expert shard); None = every expert on this GPU's engine."""
     from .profiler import profile_cost_model
     arch = preset(name)
-    w = weights if weights is not None else ModelWeights(arch, seed=seed, resident=resident)
+    experts = ep.local_experts if ep is not None else None
+    w = weights if weights is not None else ModelWeights(arch, seed=seed, resident=resident,
+                                                         experts=experts)
     if cost_model is None:
         cost_model = profile_cost_model(arch, w, log=log)
     if residuals is None and cfg.prefetch_size > 0 and not resident:
         g = torch.Generator().manual_seed(seed + 99)
         prompts = torch.randint(0, arch.vocab_size, (1, calib_prompt_len), generator=g)
-        residuals = calibrate_residuals_engine(arch, w, cost_model, prompts, max_seq)
+        residuals = calibrate_residuals_engine(arch, w, cost_model, prompts, max_seq, ep=ep)
     return OffloadEngine(arch, w, cost_model, cfg, residuals=residuals, max_batch=max_batch,
-                         max_seq=max_seq)
+                         max_seq=max_seq, ep=ep)
 
 
 def smoke_engine() -> None:
