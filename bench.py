@@ -301,7 +301,8 @@ def run_dali(args, ws, rank, local):
     hits = [(r["cache_hit_rate"], len(r["cache_hit_rate_per_group"])) for r in rep_v]
     lookups_hit = 0.0
     # overall hit rate across requests = mean of per-request rates weighted equally
-    hit = float(np.mean([h for h, _ in hits if h is not None])) if hits else None
+    hit_vals = [h for h, _ in hits if h is not None]
+    hit = float(np.mean(hit_vals)) if hit_vals else None
     acc1 = [np.mean(list(r["prefetch_accuracy_top1"].values())) for r in rep_v
             if r["prefetch_accuracy_top1"]]
     # roofline: dominant kernel = grouped expert FFN (weight streaming, HBM-bound)

@@ -531,6 +531,9 @@ class OffloadEngine:
         hv = self._host_view(v, T)
         rc_host = self._ws("rc_h", (ep.world * NL,), torch.int64, pinned=True)
         rc_host.copy_(recv_counts, non_blocking=True)
+        if self.cfg.capture:
+            h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
+            h_host.copy_(h, non_blocking=True)
         ev_dec = torch.cuda.Event()
         ev_dec.record(cs)
         tp1 = time.perf_counter()
@@ -540,6 +543,9 @@ class OffloadEngine:
         rc = rc_host.numpy().reshape(ep.world, NL).copy()
         wl_np = rc.sum(axis=0)
         self.stats.workloads[(step, l)] = wl_np
+        if self.cfg.capture:
+            self.stats.captured.append((step, l, h_host.clone()))
+            self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
         perm2, offs_l, recv_sz = plan_regroup(rc)
         snd_sz = send_sizes(hv["wl"].numpy(), ep.world)
         recv_x = ep.exchange_rows(v["xp"], snd_sz, recv_sz)        # (R, d) bf16
