@@ -29,6 +29,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# stdout carries exactly one JSON line: keep NCCL's version banner off it
+if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -179,7 +182,7 @@ def run_reference(args, ws, rank):
     wall = time.time() - t0
     v = r["decode_tokens_per_s"]
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",
+        "impl": "reference", "metric": metric_name(args), "value": round(v, 4), "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(wall * 1e3 / max(args.steps + args.warmup, 1), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -194,6 +197,13 @@ def run_reference(args, ws, rank):
 
 
 METRIC = "decode tokens/s, Mixtral-8x7B shape, 24 GB HBM expert cache (prefill tokens/s + hit rate reported)"
+
+
+def metric_name(args):
+    if args.model == "mixtral-8x7b" and args.cache_gb == 24.0 and not args.resident:
+        return METRIC
+    mode = "all-resident" if args.resident else f"{args.cache_gb:g} GB HBM expert cache"
+    return f"decode tokens/s, {args.model} shape, {mode} (prefill tokens/s + hit rate reported)"
 
 
 def config_dict(args, ws):
@@ -325,7 +335,7 @@ def run_dali(args, ws, rank, local):
                     "prefill_tokens_per_s": round(r["prefill_tokens_per_s"], 3)}
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(dec_v, 4), "unit": "tokens/s", "n_gpus": ws,
+            "metric": metric_name(args), "value": round(dec_v, 4), "unit": "tokens/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_v / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
