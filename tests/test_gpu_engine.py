@@ -260,3 +260,54 @@ def test_engine_expert_parallel_path_world1():
         # split-K planes are summed in a different place (bf16 residual rounding may flip)
         torch.testing.assert_close(l1, l2, rtol=RTOL, atol=RTOL * l1.abs().max().item())
     dist.destroy_process_group()
+
+
+def test_engine_wide_pool_replay_qwen_shape():
+    """Qwen1.5-MoE-shaped layers (60 experts top-4, d 2048, f 1408, gated shared
+    expert), 2 layers, cache 38/60 (u=8), prefetch 4: every decision of a B=4
+    request replays bit-exactly through the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import dataclasses
+
+    from paper_2602_03495_b200.cost_model import fit_cost_model
+    from paper_2602_03495_b200.engine import (EngineConfig, ModelWeights, OffloadEngine,
+                                              calibrate_residuals_engine, preset)
+    arch = dataclasses.replace(preset("qwen1.5-moe-a2.7b"), num_layers=2, vocab_size=4096)
+    # dyadic profile (2^-12 ms grid, power-of-two workloads): exact lane sums
+    cm = fit_cost_model([(1, 0.25), (2, 0.25), (4, 0.3125), (8, 0.5), (16, 0.75)],
+                        [(1, 0.03125), (4, 0.03125), (16, 0.0625)], trans_time=0.375,
+                        shared_expert_gpu_time=0.046875, non_moe_layer_time=0.125)
+    w = ModelWeights(arch, seed=2)
+    g = torch.Generator().manual_seed(3)
+    res = calibrate_residuals_engine(arch, w, cm, torch.randint(0, 4096, (1, 32), generator=g))
+    cfg = EngineConfig(cache_slots_per_layer=38, prefetch_size=4, capture=True, seed=1)
+    eng = OffloadEngine(arch, w, cm, cfg, residuals=res, max_batch=4, max_seq=96)
+    toks, st = eng.generate(torch.randint(0, 4096, (4, 24), generator=g), 10)
+    L, N, k = arch.num_layers, arch.num_experts, arch.top_k
+    by_step = {}
+    for (s, l, h) in st.captured:
+        by_step.setdefault(s, {})[l] = h.double().numpy()
+    steps = [D.StepInput(ti, n, np.stack([st.workloads[(s, l)] for l in range(L)]),
+                         np.stack([by_step[s][l] for l in range(L)]), eos)
+             for s, (ti, n, eos) in enumerate(st.steps_meta)]
+    gates = np.stack([w.router[l].double().cpu().numpy() for l in range(L)])
+    tables = P.tables_from_samples([(1, 0.25), (2, 0.25), (4, 0.3125), (8, 0.5), (16, 0.75)],
+                                   [(1, 0.03125), (4, 0.03125), (16, 0.0625)], 0.375,
+                                   0.046875, 0.125)
+    dcfg = D.DriverConfig(tables=tables, prefetch_size=4, residuals=res, cache_capacity=38,
+                          w_size=4, seed=1, initial_on_gpu=st.initial_on_gpu,
+                          num_shared_experts=1)
+    orep, recs = D.run(steps, gates, dcfg, L, N, k)
+    got = eng.policy.decision_log()
+    assert len(got) == len(recs)
+    for gg, o in zip(got, recs):
+        assert np.array_equal(gg["C"], o.C) and np.array_equal(gg["G"], o.G)
+        assert gg["hits"] == o.lookups and gg["event"] == o.event
+        if o.prefetch_set is not None:
+            assert gg["pset"] == o.prefetch_set.tolist() and gg["done"] == o.completed
+    rep = eng.policy_report()
+    for key in ("cache_hit_rate", "prefetch_accuracy_topk", "replacement_events",
+                "total_time_ms"):
+        assert rep[key] == orep[key], key
+    assert any(r.event for r in recs if r.event) and st.cpu_expert_calls > 0
