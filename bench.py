@@ -234,19 +234,11 @@ def run_dali(args, ws, rank, local):
         ep = EPGroup(preset(args.model).num_experts)
     if local_ws > 1 and ep is None and not args.resident:
         # one node-shared host expert store (memfd) filled once by local rank 0
-        import torch.distributed as dist
         from paper_2602_03495_b200.engine import ModelWeights, preset
-        from paper_2602_03495_b200.engine.weights import HostStore
+        from paper_2602_03495_b200.engine.sharing import shared_host_store
         arch = preset(args.model)
         nbytes = arch.num_layers * arch.num_experts * arch.expert_bytes
-        info = [None]
-        store = None
-        if local == 0:
-            store = HostStore(nbytes, cores, shared="create")
-            info = [(store.fd, store.owner_pid)]
-        dist.broadcast_object_list(info, src=rank - local)
-        if local != 0:
-            store = HostStore(nbytes, 1, shared="open", fd=info[0][0], owner_pid=info[0][1])
+        store = shared_host_store(nbytes, local, local_ws, rank - local, cores)
         weights = ModelWeights(arch, seed=0, host_store=store, fill_experts=(local == 0))
         barrier(ws)
     eng = build_engine(args.model, cfg, seed=0, max_batch=args.batch,

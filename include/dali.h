@@ -112,7 +112,9 @@ int dali_host_free(void* p, size_t bytes);
 /* Shared variant for one store per node (data-parallel replicas): with
  * create != 0 a memfd of `bytes` is created, touched and registered and its
  * descriptor returned in *fd; with create == 0 the owner's memfd is opened
- * through /proc/<owner_pid>/fd/<*fd>, mapped MAP_SHARED and registered. */
+ * through /proc/<owner_pid>/fd/<*fd> (or, with owner_pid < 0, *fd is a
+ * descriptor this process already holds, e.g. received with SCM_RIGHTS),
+ * mapped MAP_SHARED and registered. */
 int dali_host_alloc_shared(size_t bytes, int32_t nthreads, int32_t create,
                            int32_t* fd, int32_t owner_pid, void** out);
 

@@ -79,6 +79,8 @@ extern "C" int dali_host_alloc_shared(size_t bytes, int32_t nthreads, int32_t cr
     f = (int)syscall(SYS_memfd_create, "dali_expert_store", 0);
     DALI_REQUIRE(f >= 0, DALI_ECUDA, "memfd_create failed");
     DALI_REQUIRE(ftruncate(f, (off_t)bytes) == 0, DALI_ECUDA, "ftruncate(%zu) failed", bytes);
+  } else if (owner_pid < 0) {
+    f = *fd;                     // descriptor received over a Unix socket (SCM_RIGHTS)
   } else {
     char path[64];
     snprintf(path, sizeof(path), "/proc/%d/fd/%d", owner_pid, *fd);

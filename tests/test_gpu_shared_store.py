@@ -26,17 +26,13 @@ def _worker(rank, port, out):
                       WORLD_SIZE="2")
     dist.init_process_group("gloo", rank=rank, world_size=2)
     torch.cuda.set_device(0)
-    from paper_2602_03495_b200.engine.weights import HostStore
+    from paper_2602_03495_b200.engine.sharing import shared_host_store
     n = 64 << 20
-    info = [None]
+    st = shared_host_store(n, rank, 2, 0, 4)
     if rank == 0:
-        st = HostStore(n, 4, shared="create")
         st.bytes[:] = torch.arange(n, dtype=torch.int64).remainder(251).to(torch.uint8)
-        info = [(st.fd, st.owner_pid)]
-    dist.broadcast_object_list(info, src=0)
     dist.barrier()
     if rank == 1:
-        st = HostStore(n, 1, shared="open", fd=info[0][0], owner_pid=info[0][1])
         dev = st.bytes[(n // 2):(n // 2) + 4096].to("cuda", non_blocking=True)
         torch.cuda.synchronize()
         want = torch.arange(n // 2, n // 2 + 4096, dtype=torch.int64).remainder(251)
