@@ -116,8 +116,7 @@ struct Tile {
 // offsets; experts whose map is 0 (not on the GPU) contribute no tiles.
 template <int BN>
 __device__ bool find_tile(const int32_t* offs, const uint64_t* maps, int N, int m_tiles,
-                          int splits, Tile& t) {
-  int idx = blockIdx.x;
+                          int splits, Tile& t, int idx) {
   for (int e = 0; e < N; ++e) {
     if (!maps[e]) continue;
     const int ne = offs[e + 1] - offs[e];
@@ -146,7 +145,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap b_map, const int32_t* __restri
               int out_ld, uint16_t* __restrict__ H, float* __restrict__ Y, int64_t y_plane) {
   using S = Smem<BN>;
   Tile t;
-  if (!find_tile<BN>(offs, a_maps, N, m_tiles, splits, t)) return;
+  if (!find_tile<BN>(offs, a_maps, N, m_tiles, splits, t, blockIdx.x)) return;
   const void* a_map = reinterpret_cast<const void*>(a_maps[t.e] + (MODE == 0 ? 0 : 128));
 
   extern __shared__ uint8_t smem_raw[];
@@ -262,6 +261,188 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap b_map, const int32_t* __restri
 }
 
 // ---------------------------------------------------------------------------
+// Persistent warp-specialized variant for wide token tiles (prefill): one CTA
+// per SM loops over tiles; warp 0 = TMA producer, warp 1 = MMA issuer (owns
+// TMEM), warps 2-5 = epilogue.  Two TMEM accumulator stages (tfull/tempty
+// mbarriers) let the epilogue of tile i drain while tile i+1 accumulates.
+// ---------------------------------------------------------------------------
+constexpr int kPThreads = 192;
+
+template <int BN>
+struct PSmem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGES = BN >= 256 ? 4 : 6;
+  static constexpr int ACC_COLS = BN < 32 ? 32 : BN;      // one accumulator stage
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;          // <= 512
+  static constexpr size_t BYTES =
+      (size_t)STAGES * (A_BYTES + B_BYTES) + 64 * 17 * 4 + 1024 + 512;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+
+template <int BN>
+__device__ int count_tiles(const int32_t* offs, const uint64_t* maps, int N, int m_tiles,
+                           int splits) {
+  int n = 0;
+  for (int e = 0; e < N; ++e) {
+    if (!maps[e]) continue;
+    const int ne = offs[e + 1] - offs[e];
+    if (ne > 0) n += ((ne + BN - 1) / BN) * m_tiles * splits;
+  }
+  return n;
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kPThreads, 1)
+ffn_tc_persistent(const __grid_constant__ CUtensorMap b_map, const int32_t* __restrict__ offs,
+                  const uint64_t* __restrict__ a_maps, int N, int K, int m_tiles, int splits,
+                  int out_ld, uint16_t* __restrict__ H, float* __restrict__ Y, int64_t y_plane) {
+  using S = PSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + S::STAGES * S::A_BYTES;
+  float* sU = reinterpret_cast<float*>(sB + S::STAGES * S::B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sU + 64 * 17);
+  uint64_t* empty = full + S::STAGES;
+  uint64_t* tfull = empty + S::STAGES;      // [2]
+  uint64_t* tempty = tfull + 2;             // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (K / BK) / splits;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma_prefetch_desc(&b_map);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tslot)),
+                 "r"(S::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  // PDL: everything above overlapped the previous kernel's tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int n_tiles = count_tiles<BN>(offs, a_maps, N, m_tiles, splits);
+
+  if (warp == 0) {
+    if (lane == 0) {                                  // ---- TMA producer
+      uint32_t it = 0;
+      for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+        Tile t;
+        find_tile<BN>(offs, a_maps, N, m_tiles, splits, t, ti);
+        const void* a_map = reinterpret_cast<const void*>(a_maps[t.e] + (MODE == 0 ? 0 : 128));
+        const int kb0 = t.split * nk;
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % S::STAGES;
+          const uint32_t ph = (it / S::STAGES) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          mbar_expect_tx(full + s, S::A_BYTES + S::B_BYTES);
+          const int kx = (kb0 + i) * BK;
+          tma_load_2d(sA + s * S::A_BYTES, a_map, full + s, kx, t.m_tile * BM);
+          tma_load_2d(sB + s * S::B_BYTES, &b_map, full + s, kx, t.row0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                  // ---- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(BM, BN < 16 ? 16 : BN);
+      uint32_t it = 0, tc = 0;
+      for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x, ++tc) {
+        const int acc = tc & 1;
+        const uint32_t aph = (tc >> 1) & 1;
+        mbar_wait(tempty + acc, aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * S::ACC_COLS;
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % S::STAGES;
+          const uint32_t ph = (it / S::STAGES) & 1;
+          mbar_wait(full + s, ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = sw128_desc(su32(sA + s * S::A_BYTES));
+          const uint64_t db = sw128_desc(su32(sB + s * S::B_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma(d, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+          umma_commit(empty + s);
+        }
+        umma_commit(tfull + acc);
+      }
+    }
+  } else {                                            // ---- epilogue (warps 2-5)
+    const int q = warp & 3;                           // TMEM lane quarter of this warp
+    const int r = q * 32 + lane;                      // accumulator row
+    uint32_t tc = 0;
+    for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x, ++tc) {
+      Tile t;
+      find_tile<BN>(offs, a_maps, N, m_tiles, splits, t, ti);
+      const int acc = tc & 1;
+      const uint32_t aph = (tc >> 1) & 1;
+      mbar_wait(tfull + acc, aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t lane_addr = tmem + acc * S::ACC_COLS + ((uint32_t)(q * 32) << 16);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(lane_addr + c0, v);
+        if (MODE == 0) {
+          if (r >= 64) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sU[(r - 64) * 17 + i] = v[i];
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (r < 64) {
+            const int j = t.m_tile * 64 + r;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int c = c0 + i;
+              if (c < t.n_valid) {
+                const float g = v[i], u = sU[r * 17 + i];
+                H[(int64_t)(t.row0 + c) * out_ld + j] = f32_to_bf16_bits(g / (1.0f + __expf(-g)) * u);
+              }
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        } else {
+          const int m = t.m_tile * BM + r;
+          float* y = Y + (int64_t)t.split * y_plane;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int c = c0 + i;
+            if (c < t.n_valid) y[(int64_t)(t.row0 + c) * out_ld + m] = v[i];
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(tempty + acc);
+    }
+  }
+  // let a dependent (PDL) grid start its prologue while we drain
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(S::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -325,6 +506,62 @@ static int launch_bn(const int32_t* offs, const uint64_t* maps, int N, int d, in
   return DALI_OK;
 }
 
+template <int BN>
+static int launch_persistent(const int32_t* offs, const uint64_t* maps, int N, int d, int f,
+                             int64_t rows, int n_gpu, uint16_t* hbuf, float* yp, int splits,
+                             const uint16_t* xp, cudaStream_t st, int n_sm) {
+  using S = PSmem<BN>;
+  CUtensorMap xmap, hmap;
+  const uint64_t cap_rows = (uint64_t)std::max<int64_t>(rows, 1);
+  int rc = make_map(&xmap, xp, cap_rows, d, BN);
+  if (rc) return rc;
+  rc = make_map(&hmap, hbuf, cap_rows, f, BN);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ffn_tc_persistent<BN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::BYTES);
+    cudaFuncSetAttribute(ffn_tc_persistent<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::BYTES);
+    attr = true;
+  }
+  const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;
+  const int m_up = (2 * f) / BM, m_dn = d / BM;
+  const unsigned g_up = (unsigned)std::min<int64_t>(ntile_bound * m_up, n_sm);
+  const unsigned g_dn = (unsigned)std::min<int64_t>(ntile_bound * m_dn * splits, n_sm);
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.stream = st;
+  cfg.gridDim = dim3(g_up);
+  cfg.attrs = nullptr;
+  cfg.numAttrs = 0;
+  cudaLaunchKernelEx(&cfg, ffn_tc_persistent<BN, 0>, xmap, offs, maps, N, d, m_up, 1, f, hbuf,
+                     (float*)nullptr, (int64_t)0);
+  DALI_LAUNCH_CHECK("ffn_tc_persistent<up>");
+  cfg.gridDim = dim3(g_dn);
+  cfg.attrs = attr_pdl;           // down projection prologue overlaps the up tail
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, ffn_tc_persistent<BN, 1>, hmap, offs, maps, N, f, m_dn, splits, d,
+                     (uint16_t*)nullptr, yp, rows * (int64_t)d);
+  DALI_LAUNCH_CHECK("ffn_tc_persistent<down>");
+  return DALI_OK;
+}
+
+static int sm_count_tc() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 }  // namespace tc
 }  // namespace dali
 
@@ -358,12 +595,13 @@ extern "C" int dali_expert_ffn_tc(const uint16_t* xp, const int32_t* offsets, in
   if (mr <= 32)
     return tc::launch_bn<32>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp, splits,
                              xp, st);
+  const int nsm = tc::sm_count_tc();
   if (mr <= 64)
-    return tc::launch_bn<64>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp, splits,
-                             xp, st);
+    return tc::launch_persistent<64>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf,
+                                     yp, splits, xp, st, nsm);
   if (mr <= 128)
-    return tc::launch_bn<128>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp,
-                              splits, xp, st);
-  return tc::launch_bn<256>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp, splits,
-                            xp, st);
+    return tc::launch_persistent<128>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf,
+                                      yp, splits, xp, st, nsm);
+  return tc::launch_persistent<256>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp,
+                                    splits, xp, st, nsm);
 }
