@@ -184,6 +184,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap b_map, const int32_t* __restri
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");     // PDL (no-op without it)
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer
@@ -252,6 +253,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap b_map, const int32_t* __restri
       }
     }
   }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
@@ -500,8 +502,18 @@ static int launch_bn(const int32_t* offs, const uint64_t* maps, int N, int d, in
       xmap, offs, maps, N, d, m_up, 1, f, hbuf, nullptr, 0);
   DALI_LAUNCH_CHECK("ffn_tc_kernel<up>");
   const int64_t g_dn = ntile_bound * m_dn * splits;
-  ffn_tc_kernel<BN, 1><<<(unsigned)g_dn, kThreads, S::BYTES, st>>>(
-      hmap, offs, maps, N, f, m_dn, splits, d, nullptr, yp, rows * (int64_t)d);
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)g_dn);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.stream = st;
+  cfg.attrs = pdl;                // down prologue overlaps the up kernel's last wave
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, ffn_tc_kernel<BN, 1>, hmap, offs, maps, N, f, m_dn, splits, d,
+                     (uint16_t*)nullptr, yp, rows * (int64_t)d);
   DALI_LAUNCH_CHECK("ffn_tc_kernel<down>");
   return DALI_OK;
 }
