@@ -60,6 +60,7 @@ class EngineConfig:
     max_records: int = 16384
     time_ffn: bool = False                  # CUDA events around every expert-FFN launch
     ffn_kernel: str = "tc"                  # "tc" (tcgen05 + TMA) | "simt" (weight streaming)
+    resident_fast: bool = True              # all-resident: no per-layer host wait
 
 
 @dataclass
@@ -174,6 +175,9 @@ class OffloadEngine:
                 device=self.dev)
         self._offs_cache: dict = {}
         self._wsd: dict = {}
+        self._res_maps = None
+        self._wl_log = None
+        self._pending, self._pending_ffn, self._pending_cap = [], [], []
         self.n_sm = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._load_initial_cache()
 
@@ -460,6 +464,8 @@ class OffloadEngine:
              is_eos: bool) -> torch.Tensor:
         if self.ep is not None:
             return self._moe_ep(l, x, h, step, token_index, is_eos)
+        if self.resident_mode and self.use_tc and self.cfg.resident_fast:
+            return self._moe_resident(l, x, h, step, token_index, is_eos)
         a = self.arch
         N, k, d = a.num_experts, a.top_k, a.hidden_dim
         T = h.shape[0]
@@ -500,6 +506,88 @@ class OffloadEngine:
                   y_shared.data_ptr() if y_shared is not None else None, T, k, d, splits,
                   R, out.data_ptr(), cs.cuda_stream)
         return out
+
+    def _moe_resident(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int,
+                      token_index: int, is_eos: bool) -> torch.Tensor:
+        """All-resident fast path (roofline reference): every expert lives in
+        HBM, so the decision needs no host action -- route, policy, plan,
+        permute, grouped FFN over the static per-layer map table and combine
+        are enqueued back to back with no host wait.  Records and workloads
+        are read after the step (``_finish_resident``): a CPU assignment
+        there would be a contract violation and raises."""
+        a = self.arch
+        N, k, d, f = a.num_experts, a.top_k, a.hidden_dim, a.ffn_dim
+        T = h.shape[0]
+        R = T * k
+        cs = torch.cuda.current_stream()
+        tp0 = time.perf_counter()
+        v = self._route(l, h)
+        ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], None, None)
+        if self._wl_log is None:
+            self._wl_log = torch.empty((self.policy.max_records, N), dtype=torch.int64,
+                                       pin_memory=True)
+        wl_h = self._wl_log[ri]
+        wl_h.copy_(v["wl"], non_blocking=True)
+        self._pending.append((step, l, ri, wl_h))
+        if self._res_maps is None:
+            tab = np.array([[self._map_addr(self.w.expert_index(ll, e)) for e in range(N)]
+                            for ll in range(a.num_layers)], dtype=np.int64)
+            self._res_maps = torch.from_numpy(tab).to(self.dev)
+        mr = min(T, R)                 # an expert sees each token at most once
+        bn = 16 if mr <= 16 else 32 if mr <= 32 else 64 if mr <= 64 else 128 if mr <= 128 else 256
+        tiles = min(N, R) * ((mr + bn - 1) // bn) * (d // 128)
+        splits = self._splits_for(tiles)
+        yp = self._ws("yp", (splits, R, d), torch.float32)
+        hbuf = self._ws("hbuf", (R, f), torch.bfloat16)
+        if self.cfg.time_ffn:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(cs)
+        _lib.call("dali_expert_ffn_tc", v["xp"].data_ptr(), v["offsets"].data_ptr(), N,
+                  self._res_maps[l].data_ptr(), d, f, R, mr, min(N, R), hbuf.data_ptr(),
+                  yp.data_ptr(), splits, cs.cuda_stream)
+        if self.cfg.time_ffn:
+            t1 = torch.cuda.Event(enable_timing=True)
+            t1.record(cs)
+            self._pending_ffn.append((t0, t1, step, l))
+        y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+        out = torch.empty_like(x)
+        _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
+                  v["pos"].data_ptr(), v["wts"].data_ptr(), None, None,
+                  y_shared.data_ptr() if y_shared is not None else None, T, k, d, splits, R,
+                  out.data_ptr(), cs.cuda_stream)
+        if self.cfg.capture:
+            hh = torch.empty((T, d), dtype=torch.bfloat16, pin_memory=True)
+            hh.copy_(h, non_blocking=True)
+            ih = torch.empty((T, k), dtype=torch.int32, pin_memory=True)
+            ih.copy_(v["idx"], non_blocking=True)
+            self._pending_cap.append((step, l, hh, ih))
+        tp1 = time.perf_counter()
+        self._acct(tp0, tp1, tp1, tp1, tp1)
+        return out
+
+    def _finish_resident(self):
+        """Drain the resident fast path's deferred bookkeeping (after a sync)."""
+        a = self.arch
+        d, f = a.hidden_dim, a.ffn_dim
+        for (step, l, ri, wl_h) in self._pending:
+            rec = self.policy.record(ri)
+            wl = wl_h.numpy().copy()
+            self.stats.workloads[(step, l)] = wl
+            if any(rec.C[e] for e in range(self.NL)):
+                raise SimulationError("all-resident mode: the policy assigned an expert to the "
+                                      "CPU (cost model contract violated)")
+            ng = int(sum(1 for e in range(self.NL) if rec.G[e]))
+            self.stats.gpu_expert_calls += ng
+        for (t0, t1, step, l) in self._pending_ffn:
+            wl = self.stats.workloads[(step, l)]
+            n_rows = int(wl.sum())
+            ng = int((wl > 0).sum())
+            byts = ng * self.w.expert_bytes + n_rows * (d * 2 + 2 * f * 2 + d * 4)
+            self.stats.ffn_events.append((t0, t1, byts, n_rows))
+        for (step, l, hh, ih) in self._pending_cap:
+            self.stats.captured.append((step, l, hh))
+            self.stats.topk[(step, l)] = ih.numpy().astype(np.int64).copy()
+        self._pending, self._pending_ffn, self._pending_cap = [], [], []
 
     def _acct(self, tp0, tp1, tp2, tp3, tp4):
         pr = self.stats.host_ms
@@ -662,6 +750,8 @@ class OffloadEngine:
                 self.stats.logits.append(logits.float().cpu())
         e2.record(cs)
         e2.synchronize()
+        if self._pending or self._pending_ffn or self._pending_cap:
+            self._finish_resident()
         st = self.stats
         st.prefill_ms = e0.elapsed_time(e1)
         st.decode_ms = e1.elapsed_time(e2)

@@ -311,3 +311,29 @@ def test_engine_wide_pool_replay_qwen_shape():
                 "total_time_ms"):
         assert rep[key] == orep[key], key
     assert any(r.event for r in recs if r.event) and st.cpu_expert_calls > 0
+
+
+def test_resident_fast_path_matches_offload_path():
+    """All-resident fast path (no host waits) vs the generic per-layer path
+    with every expert resident: identical decisions and logits."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    arch = preset("tiny-shared")
+    w = ModelWeights(arch, seed=4, resident=True)
+    cm = default_cost_model(shared_expert_gpu_time=0.5, non_moe_layer_time=1.0)
+    fast = OffloadEngine(arch, w, cm, EngineConfig(capture=True), max_seq=64)
+    slow = OffloadEngine(arch, w, cm, EngineConfig(capture=True, resident_fast=False), max_seq=64)
+    p = torch.randint(0, arch.vocab_size, (2, 10), generator=torch.Generator().manual_seed(2))
+    t1, s1 = fast.generate(p, 5)
+    d1 = fast.policy.decision_log()
+    t2, s2 = slow.generate(p, 5)
+    d2 = slow.policy.decision_log()
+    assert len(d1) == len(d2)
+    for a_, b_ in zip(d1, d2):
+        assert np.array_equal(a_["G"], b_["G"]) and not a_["C"].any()
+    for k_ in s1.workloads:
+        assert np.array_equal(s1.workloads[k_], s2.workloads[k_])
+    for l1, l2 in zip(s1.logits, s2.logits):
+        torch.testing.assert_close(l1, l2, rtol=RTOL, atol=RTOL * l1.abs().max().item())
