@@ -81,7 +81,7 @@ typedef struct dali_layer_record {
  * simulator.py:45-74, restricted to the hot-path policies). */
 typedef struct dali_policy_config {
   int32_t L, N, k;
-  int32_t assignment;        /* 0 = greedy, 1 = all-cpu                     */
+  int32_t assignment;        /* 0 = greedy, 1 = all-cpu, 2 = all-gpu        */
   int32_t gpu_capacity;      /* < 0 = unlimited                             */
   int32_t prefetch_size;     /* 0 = prefetch off                            */
   int32_t cache_enabled;

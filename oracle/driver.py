@@ -148,6 +148,10 @@ def run(steps, gates, cfg: DriverConfig, L: int, N: int, k: int):
             if cfg.assignment_policy == "greedy":
                 C, G, order = P.greedy(w, resident, cpu_t, gpu_t, cfg.gpu_capacity)
                 nodes = int((w > 0).sum())
+            elif cfg.assignment_policy == "all-gpu":
+                C, G = P.all_gpu(w, resident, cfg.gpu_capacity)
+                order = P.visit_order(w, cpu_t, gpu_t)
+                nodes = 0
             elif cfg.assignment_policy == "all-cpu":
                 C, G = P.all_cpu(w)
                 order = P.visit_order(w, cpu_t, gpu_t)

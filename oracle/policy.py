@@ -198,6 +198,22 @@ def greedy(workloads, resident, cpu_t, gpu_t, capacity=None):
     return C, G, order
 
 
+def all_gpu(workloads, resident, capacity=None):
+    """Everything on the GPU, capacity overflow to the CPU (assignment.py:387-402)."""
+    w = np.asarray(workloads)
+    C = np.zeros(len(w), np.int8)
+    G = np.zeros(len(w), np.int8)
+    slots = capacity
+    for e in np.flatnonzero(w > 0):
+        if slots is None or slots > 0 or bool(resident[e]):
+            G[e] = 1
+            if slots is not None and not resident[e]:
+                slots -= 1
+        else:
+            C[e] = 1
+    return C, G
+
+
 def all_cpu(workloads):
     """All activated experts on the CPU (assignment.py:380-384)."""
     w = np.asarray(workloads)

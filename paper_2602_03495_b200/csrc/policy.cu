@@ -282,6 +282,20 @@ policy_layer_kernel(dali_policy_config cfg, dali_cost_model cm, int step, int la
     if (cfg.assignment == 0) {
       greedy_scan(s, cfg.gpu_capacity);
       nodes = s.n_act;
+    } else if (cfg.assignment == 2) {
+      // all_gpu_assign (assignment.py:387-402): activated experts in index
+      // order; capacity overflow of non-resident experts falls back to CPU
+      int slots = cfg.gpu_capacity;
+      for (int j = 0; j < N; ++j) {
+        if (!(s.wl[j] > 0.0)) continue;
+        if (slots < 0 || slots > 0 || s.res[j]) {
+          s.G[j] = 1;
+          if (slots >= 0 && !s.res[j]) --slots;
+        } else {
+          s.C[j] = 1;
+        }
+      }
+      nodes = 0;
     } else {
       for (int r = 0; r < s.n_act; ++r) s.C[s.order[r]] = 1;
       nodes = 0;

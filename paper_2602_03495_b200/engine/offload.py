@@ -133,8 +133,10 @@ class OffloadEngine:
         self.residuals_np = residuals
         res_dev = torch.from_numpy(np.ascontiguousarray(residuals)).to(self.dev) \
             if residuals is not None else None
+        # all-resident mode is the roofline reference: every expert on the GPU
+        assignment = "all-gpu" if self.resident_mode else cfg.assignment
         self.policy = PolicyEngine(
-            L, N, k, cost_model, assignment=cfg.assignment, gpu_capacity=cfg.gpu_capacity,
+            L, N, k, cost_model, assignment=assignment, gpu_capacity=cfg.gpu_capacity,
             prefetch_size=cfg.prefetch_size if not self.resident_mode else 0,
             residuals=res_dev, cache_capacity=slots, w_size=cfg.w_size, u_size=cfg.u_size,
             seed=cfg.seed, max_records=cfg.max_records, all_resident=self.resident_mode,

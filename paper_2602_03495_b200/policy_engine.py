@@ -48,9 +48,9 @@ class PolicyEngine:
                  initial_on_gpu: np.ndarray | None = None):
         if N > _lib.MAX_EXPERTS:
             raise SimulationError(f"at most {_lib.MAX_EXPERTS} experts per layer")
-        if assignment not in ("greedy", "all-cpu"):
+        if assignment not in ("greedy", "all-cpu", "all-gpu"):
             raise SimulationError(f"assignment policy {assignment!r} is not on the B200 path "
-                                  f"(greedy | all-cpu)")
+                                  f"(greedy | all-cpu | all-gpu)")
         dev = _dev.require_cuda()
         self.L, self.N, self.k = L, N, k
         self.cm = cost_model
@@ -65,7 +65,7 @@ class PolicyEngine:
                    else cost_model.non_moe_layer_time)
         cfg = _lib.PolicyConfigC()
         cfg.L, cfg.N, cfg.k = L, N, k
-        cfg.assignment = 0 if assignment == "greedy" else 1
+        cfg.assignment = {"greedy": 0, "all-cpu": 1, "all-gpu": 2}[assignment]
         cfg.gpu_capacity = -1 if gpu_capacity is None else int(gpu_capacity)
         cfg.prefetch_size = self.prefetch_size
         cfg.cache_enabled = int(self.cache_enabled)

@@ -25,7 +25,7 @@ from .errors import SimulationError
 from .policy_engine import PolicyEngine, default_u_size  # noqa: F401  (re-export)
 from .trace import ResidualVectors, Trace
 
-ASSIGNMENT_POLICIES = ("greedy", "all-cpu")
+ASSIGNMENT_POLICIES = ("greedy", "all-cpu", "all-gpu")
 
 
 @dataclass

@@ -7,6 +7,8 @@ def run_cfgs(N):
     return [
         ("greedy", dict()),
         ("allcpu", dict(assignment_policy="all-cpu")),
+        ("allgpu_cache", dict(assignment_policy="all-gpu", cache_policy="workload",
+                              cache_capacity=cap, w_size=4, seed=3, gpu_capacity=1)),
         ("greedy_prefetch", dict(prefetch_kind="residual", prefetch_size=1)),
         ("greedy_prefetch_nm3", dict(prefetch_kind="residual", prefetch_size=2,
                                      non_moe_override=3.0)),
