@@ -768,3 +768,33 @@ class OffloadEngine:
         clock, hit rates, prefetch accuracy, replacement log)."""
         toks = [m[1] for m in self.stats.steps_meta]
         return self.policy.build_report(toks, self.stats.workloads, {})
+
+
+def export_trace(engine: "OffloadEngine", trace_path: str, gates_path: str | None = None,
+                 residuals_path: str | None = None, batch_size: int = 1):
+    """Write the last request as reference-format artifacts (SURVEY section 8f
+    rank 3): the per-step x per-layer workloads (plus gate inputs when the
+    engine captured them), the router sidecar and the residual sidecar, so
+    ``moesim`` can replay exactly the routing the B200 engine executed."""
+    from ..trace import (GateParams, ResidualVectors, Trace, TokenStep, save_gate_params,
+                         save_residuals, save_trace)
+    a, st = engine.arch, engine.stats
+    L = a.num_layers
+    hid = {}
+    for (s, l, h) in st.captured:
+        hid.setdefault(s, {})[l] = h.double().numpy()
+    steps = []
+    for s, (ti, ntok, eos) in enumerate(st.steps_meta):
+        wl = np.stack([st.workloads[(s, l)] for l in range(L)])
+        h = np.stack([hid[s][l] for l in range(L)]) if s in hid and len(hid[s]) == L else None
+        steps.append(TokenStep(ti, ntok, wl, h, eos))
+    cfg = a.routing
+    tr = Trace(cfg, batch_size, "decode", steps,
+               generator_params={"source": "paper_2602_03495_b200 engine", "arch": a.name})
+    save_trace(tr, trace_path)
+    if gates_path is not None:
+        save_gate_params(GateParams(np.stack([engine.w.router[l].double().cpu().numpy()
+                                              for l in range(L)])), gates_path)
+    if residuals_path is not None and engine.residuals_np is not None:
+        save_residuals(ResidualVectors(engine.residuals_np), residuals_path)
+    return tr

@@ -387,3 +387,75 @@ def load_residuals(path) -> ResidualVectors:
     if len(seen) != L - 1:
         raise TraceError(f"{path}: expected {L - 1} residual vectors, found {len(seen)}")
     return ResidualVectors(vals)
+
+
+def save_trace(trace: Trace, path) -> None:
+    """Write ``moesim-trace-v1`` line-delimited JSON (reference trace.py:
+    385-406): one header object, then one record per step.  Lets the
+    reference's own tools (simulate / cache-eval / report) replay a run the
+    B200 engine executed."""
+    header = {"format": TRACE_FORMAT, "model_config": trace.model_config.to_dict(),
+              "batch_size": trace.batch_size, "phase": trace.phase,
+              "generator_seed": trace.generator_seed, "has_features": trace.has_features,
+              "generator_params": trace.generator_params}
+    with open(path, "w") as f:
+        f.write(json.dumps(header) + "\n")
+        for st in trace.steps:
+            rec = {"token_index": int(st.token_index), "tokens": int(st.tokens),
+                   "eos": bool(st.eos), "workloads": st.workloads.tolist()}
+            if st.hidden is not None:
+                rec["hidden"] = st.hidden.tolist()
+            f.write(json.dumps(rec) + "\n")
+
+
+def load_trace(path) -> Trace:
+    """Read a ``moesim-trace-v1`` file (reference trace.py:409-473 semantics:
+    structural validation with the offending line number)."""
+    with open(path) as f:
+        lines = f.readlines()
+    if not lines:
+        raise TraceError(f"{path}: empty trace file")
+    try:
+        header = json.loads(lines[0])
+    except json.JSONDecodeError as e:
+        raise TraceError(f"{path}:1: malformed record: {e}") from e
+    if header.get("format") != TRACE_FORMAT:
+        raise TraceError(f"{path}:1: not a trace file (format tag {header.get('format')!r})")
+    cfg = ModelConfig.from_dict(header["model_config"])
+    L, N, d = cfg.num_layers, cfg.num_routed_experts, cfg.hidden_dim
+    B = int(header["batch_size"])
+    steps = []
+    for lineno, line in enumerate(lines[1:], start=2):
+        if not line.strip():
+            continue
+        try:
+            rec = json.loads(line)
+        except json.JSONDecodeError as e:
+            raise TraceError(f"{path}:{lineno}: malformed record: {e}") from e
+        wl = np.asarray(rec.get("workloads"), dtype=np.int64)
+        if wl.shape != (L, N) or (wl < 0).any():
+            raise TraceError(f"{path}:{lineno}: workloads must be ({L}, {N}) nonnegative ints")
+        tokens = int(rec.get("tokens", B))
+        hid = None
+        if "hidden" in rec:
+            hid = np.asarray(rec["hidden"], dtype=np.float64)
+            if hid.shape != (L, tokens, d):
+                raise TraceError(f"{path}:{lineno}: hidden shape {hid.shape} != ({L}, {tokens}, {d})")
+        steps.append(TokenStep(int(rec.get("token_index", lineno - 2)), tokens, wl, hid,
+                               bool(rec.get("eos", False))))
+    tr = Trace(cfg, B, header["phase"], steps, int(header.get("generator_seed", 0)),
+               generator_params=header.get("generator_params", {}))
+    tr.validate()
+    return tr
+
+
+def save_gate_params(gate: GateParams, path, spec: dict | None = None) -> None:
+    """``moesim-gates-v1`` sidecar (reference trace.py:486-496)."""
+    L, d, N = gate.weights.shape
+    header = {"format": GATES_FORMAT, "num_layers": L, "hidden_dim": d, "num_routed_experts": N}
+    if spec is not None:
+        header["spec"] = spec
+    with open(path, "w") as f:
+        f.write(json.dumps(header) + "\n")
+        for l in range(L):
+            f.write(json.dumps({"layer": l, "weights": gate.weights[l].tolist()}) + "\n")
