@@ -75,6 +75,7 @@ typedef struct dali_layer_record {
   int16_t cand[DALI_MAX_EXPERTS];     /* pset minus cache[layer+1]        */
   int16_t evicted[DALI_MAX_EXPERTS];
   int16_t admitted[DALI_MAX_EXPERTS];
+  int32_t workload[DALI_MAX_EXPERTS]; /* realised workloads of this layer  */
 } dali_layer_record;
 
 /* Scalar knobs of the fused per-layer policy step (SimConfig,
@@ -204,6 +205,23 @@ int dali_policy_layer(const dali_policy_config* cfg, const dali_cost_model* cm,
                       double* scores, int32_t* counters, uint8_t* arrived,
                       int32_t* slot_of, dali_layer_record* rec, void* stream);
 
+/* Same step with the per-step scalars read from a DEVICE descriptor so the
+ * launch can live inside a CUDA graph replayed every decode step:
+ *   desc [dev] int32[8] = {step, token_index, eos_at_step, record_index,
+ *                          pos, len, L, unused}
+ *   is_eos = (step == eos_at_step); the record written is
+ *   rec_base[record_index + layer].  dali_step_advance moves the
+ *   descriptor to the next step (step, token_index, pos, len += 1;
+ *   record_index += L) on device. */
+int dali_policy_layer_desc(const dali_policy_config* cfg,
+                           const dali_cost_model* cm, int32_t layer,
+                           const int32_t* desc, const int64_t* workloads,
+                           const int64_t* predicted, uint8_t* on_gpu,
+                           double* scores, int32_t* counters, uint8_t* arrived,
+                           int32_t* slot_of, dali_layer_record* rec_base,
+                           void* stream);
+int dali_step_advance(int32_t* desc, void* stream);
+
 /* ---- (5) expert execution -------------------------------------------------
  * Plan: stable counting sort of the T*k (token, slot) pairs by expert.
  *   topk_idx [dev] (T,k) i32 -> offsets [dev] (N+1) i32,
@@ -274,6 +292,23 @@ int dali_unpermute_combine(const uint16_t* x, const float* yp,
 int dali_add_rmsnorm(const uint16_t* x, const uint16_t* a, const uint16_t* w,
                      float eps, int64_t T, int32_t d, uint16_t* x_out,
                      uint16_t* h, void* stream);
+
+/* Decode attention plumbing (one query token per sequence; position and
+ * valid length read from device scalars, graph-capturable):
+ *   dali_rope_append: qkv (B, (H+2KV)*hd) bf16 -> q (B,H,hd) rotated (rotate-
+ *     half RoPE, fp32 tables cos/sin (max_pos, hd/2)); rotated k and v stored
+ *     at *pos in caches laid out (B, KV, max_len, hd).
+ *   dali_decode_attention: split-K GQA attention over positions [0, *len),
+ *     head_dim 128; workspace f32 (B*H*splits*(hd+2)). */
+int dali_rope_append(const uint16_t* qkv, const float* cos_t, const float* sin_t,
+                     const int32_t* pos, int32_t B, int32_t H, int32_t KV,
+                     int32_t hd, int32_t max_len, uint16_t* q_out,
+                     uint16_t* k_cache, uint16_t* v_cache, void* stream);
+int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
+                          const uint16_t* v_cache, const int32_t* len, int32_t B,
+                          int32_t H, int32_t KV, int32_t hd, int32_t max_len,
+                          int32_t splits, float scale, float* workspace,
+                          uint16_t* out, void* stream);
 
 /* Deterministic counter-hash weight init (uniform, given std):
  * out[i] = bf16(std * sqrt(3) * (2*u(seed, offset+i) - 1)). */

@@ -52,7 +52,7 @@ class LayerRecordC(C.Structure):
                 ("resident", C.c_uint8 * MAX_EXPERTS), ("hit", C.c_uint8 * MAX_EXPERTS),
                 ("order", C.c_int16 * MAX_EXPERTS), ("pset", C.c_int16 * MAX_EXPERTS),
                 ("cand", C.c_int16 * MAX_EXPERTS), ("evicted", C.c_int16 * MAX_EXPERTS),
-                ("admitted", C.c_int16 * MAX_EXPERTS)]
+                ("admitted", C.c_int16 * MAX_EXPERTS), ("workload", C.c_int32 * MAX_EXPERTS)]
 
 
 RECORD_BYTES = C.sizeof(LayerRecordC)
@@ -84,6 +84,11 @@ SIGNATURES = {
     "dali_init_uniform_bf16": [_P, _I64, C.c_uint64, C.c_uint64, C.c_float, _P],
     "dali_host_alloc": [C.c_size_t, _I32, C.POINTER(C.c_void_p)],
     "dali_host_free": [_P, C.c_size_t],
+    "dali_policy_layer_desc": [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "dali_step_advance": [_P, _P],
+    "dali_rope_append": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P],
+    "dali_decode_attention": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, C.c_float, _P,
+                              _P, _P],
     "dali_add_rmsnorm": [_P, _P, _P, C.c_float, _I64, _I32, _P, _P, _P],
     "dali_host_alloc_shared": [C.c_size_t, _I32, _I32, C.POINTER(C.c_int32), _I32,
                                C.POINTER(C.c_void_p)],

@@ -249,8 +249,15 @@ policy_layer_kernel(dali_policy_config cfg, dali_cost_model cm, int step, int la
                     int token_index, int is_eos, const int64_t* __restrict__ workloads,
                     const int64_t* __restrict__ predicted, uint8_t* on_gpu_all,
                     double* scores_all, int32_t* counters_all, uint8_t* arrived_all,
-                    int32_t* slot_of_all, dali_layer_record* rec) {
+                    int32_t* slot_of_all, dali_layer_record* rec,
+                    const int32_t* __restrict__ desc) {
   __shared__ PolShared s;
+  if (desc) {                     // graph replay: per-step scalars live on device
+    step = desc[0];
+    token_index = desc[1];
+    is_eos = step == desc[2];
+    rec += desc[3] + layer;
+  }
   __shared__ double sh_d[8];
   const int N = cfg.N, L = cfg.L;
   const int e = threadIdx.x;
@@ -350,6 +357,7 @@ policy_layer_kernel(dali_policy_config cfg, dali_cost_model cm, int step, int la
   if (e < N) {
     rec->C[e] = s.C[e];
     rec->G[e] = s.G[e];
+    rec->workload[e] = (int32_t)workloads[e];
     rec->resident[e] = s.res[e];
     rec->hit[e] = (cfg.cache_enabled && s.G[e] && on_gpu[e]) ? 1 : 0;
     rec->order[e] = (int16_t)s.order[e];
@@ -496,7 +504,39 @@ extern "C" int dali_policy_layer(const dali_policy_config* cfg, const dali_cost_
   DALI_REQUIRE(!cfg->cache_enabled || cfg->u_size <= DALI_MAX_EXPERTS, DALI_ESIM, "u_size");
   dali::policy_layer_kernel<<<1, dali::kPolThreads, 0, dali::as_stream(stream)>>>(
       *cfg, *cm, step, layer, token_index, is_eos, workloads, predicted, on_gpu, scores,
-      counters, arrived, slot_of, rec);
+      counters, arrived, slot_of, rec, nullptr);
   DALI_LAUNCH_CHECK("policy_layer_kernel");
+  return DALI_OK;
+}
+
+extern "C" int dali_policy_layer_desc(const dali_policy_config* cfg, const dali_cost_model* cm,
+                                      int32_t layer, const int32_t* desc,
+                                      const int64_t* workloads, const int64_t* predicted,
+                                      uint8_t* on_gpu, double* scores, int32_t* counters,
+                                      uint8_t* arrived, int32_t* slot_of,
+                                      dali_layer_record* rec_base, void* stream) {
+  DALI_REQUIRE(cfg != nullptr && dali::valid_cm(cm) && desc != nullptr, DALI_ESIM,
+               "invalid config / cost model / descriptor");
+  DALI_REQUIRE(layer >= 0 && layer < cfg->L, DALI_ESIM, "layer %d out of range", layer);
+  dali::policy_layer_kernel<<<1, dali::kPolThreads, 0, dali::as_stream(stream)>>>(
+      *cfg, *cm, 0, layer, 0, 0, workloads, predicted, on_gpu, scores, counters, arrived,
+      slot_of, rec_base, desc);
+  DALI_LAUNCH_CHECK("policy_layer_kernel(desc)");
+  return DALI_OK;
+}
+
+namespace dali {
+__global__ void step_advance_kernel(int32_t* desc) {
+  desc[0] += 1;            // step
+  desc[1] += 1;            // token_index
+  desc[3] += desc[6];      // record_index += L
+  desc[4] += 1;            // pos
+  desc[5] += 1;            // len
+}
+}  // namespace dali
+
+extern "C" int dali_step_advance(int32_t* desc, void* stream) {
+  dali::step_advance_kernel<<<1, 1, 0, dali::as_stream(stream)>>>(desc);
+  DALI_LAUNCH_CHECK("step_advance_kernel");
   return DALI_OK;
 }

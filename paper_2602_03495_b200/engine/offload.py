@@ -26,6 +26,7 @@ captured gate inputs reproduces every decision bit-for-bit.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import os
 import time
@@ -61,6 +62,7 @@ class EngineConfig:
     time_ffn: bool = False                  # CUDA events around every expert-FFN launch
     ffn_kernel: str = "tc"                  # "tc" (tcgen05 + TMA) | "simt" (weight streaming)
     resident_fast: bool = True              # all-resident: no per-layer host wait
+    use_graph: bool = True                  # all-resident decode steps replay one CUDA graph
 
 
 @dataclass
@@ -179,7 +181,13 @@ class OffloadEngine:
         self._wsd: dict = {}
         self._res_maps = None
         self._wl_log = None
-        self._pending, self._pending_ffn, self._pending_cap = [], [], []
+        self.desc_dev = torch.zeros((8,), dtype=torch.int32, device=self.dev)
+        self.desc_host = torch.zeros((8,), dtype=torch.int32, pin_memory=True)
+        self._graph = None
+        self._in_capture = False
+        self._eos_at = -1
+        self._pending_ffn, self._pending_cap = [], []
+        self._used_fast = False
         self.n_sm = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self._load_initial_cache()
 
@@ -524,13 +532,19 @@ class OffloadEngine:
         cs = torch.cuda.current_stream()
         tp0 = time.perf_counter()
         v = self._route(l, h)
-        ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], None, None)
-        if self._wl_log is None:
-            self._wl_log = torch.empty((self.policy.max_records, N), dtype=torch.int64,
-                                       pin_memory=True)
-        wl_h = self._wl_log[ri]
-        wl_h.copy_(v["wl"], non_blocking=True)
-        self._pending.append((step, l, ri, wl_h))
+        if T == self.kv.k.shape[1] and self.stats.steps_meta:     # decode: device descriptor
+            ri = self.policy.n_records + l
+            _lib.call("dali_policy_layer_desc", C.addressof(self.policy.cfg),
+                      C.addressof(self.policy.cm_c), l, self.desc_dev.data_ptr(),
+                      v["wl"].data_ptr(), None, self.policy.on_gpu.data_ptr(),
+                      self.policy.scores.data_ptr(), self.policy.counters.data_ptr(),
+                      self.policy.arrived.data_ptr(), self.policy.slot_of.data_ptr(),
+                      self.policy.record_ptr(0), cs.cuda_stream)
+            if l == a.num_layers - 1 and not self._in_capture:
+                self.policy.n_records += a.num_layers
+        else:
+            ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], None, None)
+        self._used_fast = True
         if self._res_maps is None:
             tab = np.array([[self._map_addr(self.w.expert_index(ll, e)) for e in range(N)]
                             for ll in range(a.num_layers)], dtype=np.int64)
@@ -568,18 +582,18 @@ class OffloadEngine:
         return out
 
     def _finish_resident(self):
-        """Drain the resident fast path's deferred bookkeeping (after a sync)."""
+        """Deferred bookkeeping of the resident fast path / graph replays (after
+        a sync): workloads and assignments come from the decision records."""
         a = self.arch
-        d, f = a.hidden_dim, a.ffn_dim
-        for (step, l, ri, wl_h) in self._pending:
-            rec = self.policy.record(ri)
-            wl = wl_h.numpy().copy()
-            self.stats.workloads[(step, l)] = wl
-            if any(rec.C[e] for e in range(self.NL)):
+        d, f, NL = a.hidden_dim, a.ffn_dim, self.NL
+        for i in range(self.policy.n_records):
+            rec = self.policy.record(i)
+            key = (rec.step, rec.layer)
+            self.stats.workloads[key] = np.array(rec.workload[:NL], dtype=np.int64)
+            if any(rec.C[e] for e in range(NL)):
                 raise SimulationError("all-resident mode: the policy assigned an expert to the "
                                       "CPU (cost model contract violated)")
-            ng = int(sum(1 for e in range(self.NL) if rec.G[e]))
-            self.stats.gpu_expert_calls += ng
+            self.stats.gpu_expert_calls += int(sum(1 for e in range(NL) if rec.G[e]))
         for (t0, t1, step, l) in self._pending_ffn:
             wl = self.stats.workloads[(step, l)]
             n_rows = int(wl.sum())
@@ -589,7 +603,8 @@ class OffloadEngine:
         for (step, l, hh, ih) in self._pending_cap:
             self.stats.captured.append((step, l, hh))
             self.stats.topk[(step, l)] = ih.numpy().astype(np.int64).copy()
-        self._pending, self._pending_ffn, self._pending_cap = [], [], []
+        self._pending_ffn, self._pending_cap = [], []
+        self._used_fast = False
 
     def _acct(self, tp0, tp1, tp2, tp3, tp4):
         pr = self.stats.host_ms
@@ -674,6 +689,27 @@ class OffloadEngine:
         return out
 
     # ------------------------------------------------------------- forward
+    def _attn_decode(self, l: int, hn: torch.Tensor, B: int) -> torch.Tensor:
+        """One-token GQA attention: qkv GEMM, fused RoPE + KV append and
+        split-K decode attention reading pos / len from the device step
+        descriptor (graph-capturable), o-proj GEMM."""
+        a, W = self.arch, self.w
+        H, KV, hd = a.num_heads, a.num_kv_heads, a.head_dim
+        sp = torch.cuda.current_stream().cuda_stream
+        qkv = hn @ W.wqkv[l].t()
+        q = self._ws("q_dec", (B, H, hd), torch.bfloat16)
+        kc, vc = self.kv.k[l], self.kv.v[l]
+        _lib.call("dali_rope_append", qkv.data_ptr(), self.rope.cos.data_ptr(),
+                  self.rope.sin.data_ptr(), self.desc_dev.data_ptr() + 16, B, H, KV, hd,
+                  self.max_seq, q.data_ptr(), kc.data_ptr(), vc.data_ptr(), sp)
+        splits = 16
+        ws = self._ws("attn_ws", (B * H * splits * (hd + 2),), torch.float32)
+        o = self._ws("o_dec", (B, H * hd), torch.bfloat16)
+        _lib.call("dali_decode_attention", q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
+                  self.desc_dev.data_ptr() + 20, B, H, KV, hd, self.max_seq, splits,
+                  1.0 / math.sqrt(hd), ws.data_ptr(), o.data_ptr(), sp)
+        return o @ W.wo[l].t()
+
     def _forward(self, tokens_dev: torch.Tensor, B: int, S: int, pos0: int, step: int,
                  token_index: int, is_eos: bool) -> torch.Tensor:
         a, W = self.arch, self.w
@@ -682,10 +718,14 @@ class OffloadEngine:
         sp = torch.cuda.current_stream().cuda_stream
         hn = self._ws("hn", (T, d), torch.bfloat16)
         h = self._ws("h", (T, d), torch.bfloat16)
+        dev_attn = S == 1 and a.head_dim == 128
         for l in range(a.num_layers):
             _lib.call("dali_add_rmsnorm", x.data_ptr(), None, W.attn_norm[l].data_ptr(),
                       a.rms_eps, T, d, None, hn.data_ptr(), sp)
-            att = attention(a, hn, W.wqkv[l], W.wo[l], self.rope, self.kv, l, B, S, pos0)
+            if dev_attn:
+                att = self._attn_decode(l, hn, B)
+            else:
+                att = attention(a, hn, W.wqkv[l], W.wo[l], self.rope, self.kv, l, B, S, pos0)
             x2 = torch.empty_like(x)
             _lib.call("dali_add_rmsnorm", x.data_ptr(), att.data_ptr(), W.moe_norm[l].data_ptr(),
                       a.rms_eps, T, d, x2.data_ptr(), h.data_ptr(), sp)
@@ -693,15 +733,26 @@ class OffloadEngine:
         last = x.view(B, S, -1)[:, -1]
         return rms_norm(last, W.final_norm, a.rms_eps) @ W.lm_head.t()
 
+    def _set_desc(self, step: int, token_index: int, eos_at: int, rec_index: int, pos: int):
+        """Write the device step descriptor (stream-ordered H2D)."""
+        dh = self.desc_host
+        dh.copy_(torch.tensor([step, token_index, eos_at, rec_index, pos, pos + 1,
+                               self.arch.num_layers, 0], dtype=torch.int32))
+        self.desc_dev.copy_(dh, non_blocking=True)
+
     def start_request(self, batch: int) -> np.ndarray:
         """New policy run for one request; cache residency carries over."""
-        self.kv = KVCache(self.arch, batch, self.max_seq, self.dev)
+        if self.kv is None or self.kv.k.shape[1] != batch:
+            self.kv = KVCache(self.arch, batch, self.max_seq, self.dev)
+            self._graph = None
+        self.kv.len = 0
         for key in list(self.prefetched):
             i, ev = self.prefetched.pop(key)
             self.staging.release(i, ev)
         init = self.policy.new_run()
         self.stats = RunStats(initial_on_gpu=init)
         self._step = 0
+        self._eos_at = -1
         return init
 
     def prefill(self, prompt_dev: torch.Tensor, is_eos: bool = False) -> torch.Tensor:
@@ -710,17 +761,69 @@ class OffloadEngine:
         self.stats.steps_meta.append((0, B * S, is_eos))
         self._step += 1
         self.kv.len = S
+        # device descriptor of the first decode step (pos = S)
+        self._set_desc(self._step, self._step, self._eos_at, self.policy.n_records, S)
         return logits
+
+    def _graphable(self) -> bool:
+        return (self.resident_mode and self.use_tc and self.cfg.resident_fast and
+                self.cfg.use_graph and self.arch.head_dim == 128 and self.ep is None and
+                not self.cfg.capture)
 
     def decode(self, tok_dev: torch.Tensor, is_eos: bool = False) -> torch.Tensor:
         B = tok_dev.shape[0]
         pos = self.kv.len
         ti = self._step
-        logits = self._forward(tok_dev.view(B, 1), B, 1, pos, self._step, ti, is_eos)
+        if self._graphable():
+            logits = self._decode_graph(tok_dev)
+        else:
+            logits = self._forward(tok_dev.view(B, 1), B, 1, pos, self._step, ti, is_eos)
+            _lib.call("dali_step_advance", self.desc_dev.data_ptr(),
+                      torch.cuda.current_stream().cuda_stream)
         self.stats.steps_meta.append((ti, B, is_eos))
         self._step += 1
         self.kv.len = pos + 1
         return logits
+
+    def _decode_graph(self, tok_dev: torch.Tensor) -> torch.Tensor:
+        """All-resident decode step as one CUDA graph: every per-step scalar
+        (step, token index, record slot, KV position) lives in the device
+        descriptor, which the graph advances itself, so a replay needs no
+        host input.  The first decode step runs eagerly (warms workspaces)
+        and the graph is captured on the second."""
+        B = tok_dev.shape[0]
+        L = self.arch.num_layers
+        if self._graph is not None:
+            self._graph_in.copy_(tok_dev.view(B))
+            self._graph.replay()
+            self.policy.n_records += L
+            return self._graph_logits
+        if not getattr(self, "_graph_warm", False):
+            logits = self._forward(tok_dev.view(B, 1), B, 1, self.kv.len, self._step, self._step,
+                                   False)
+            _lib.call("dali_step_advance", self.desc_dev.data_ptr(),
+                      torch.cuda.current_stream().cuda_stream)
+            self._graph_warm = True
+            return logits
+        self._graph_in = torch.zeros((B,), dtype=torch.int64, device=self.dev)
+        self._graph_in.copy_(tok_dev.view(B))
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        saved = self.cfg.time_ffn
+        self.cfg.time_ffn = False                 # no timing events inside the graph
+        self._in_capture = True
+        n0 = self.policy.n_records
+        with torch.cuda.graph(g):
+            out = self._forward(self._graph_in.view(B, 1), B, 1, 0, 0, 0, False)
+            _lib.call("dali_step_advance", self.desc_dev.data_ptr(),
+                      torch.cuda.current_stream().cuda_stream)
+        self._in_capture = False
+        self.cfg.time_ffn = saved
+        self.policy.n_records = n0
+        self._graph, self._graph_logits = g, out
+        g.replay()
+        self.policy.n_records += L
+        return out
 
     def generate(self, prompt: torch.Tensor, max_new_tokens: int, host_io: bool = True):
         """Greedy generation for one request.
@@ -752,7 +855,7 @@ class OffloadEngine:
                 self.stats.logits.append(logits.float().cpu())
         e2.record(cs)
         e2.synchronize()
-        if self._pending or self._pending_ffn or self._pending_cap:
+        if self._used_fast:
             self._finish_resident()
         st = self.stats
         st.prefill_ms = e0.elapsed_time(e1)

@@ -337,3 +337,68 @@ def test_resident_fast_path_matches_offload_path():
         assert np.array_equal(s1.workloads[k_], s2.workloads[k_])
     for l1, l2 in zip(s1.logits, s2.logits):
         torch.testing.assert_close(l1, l2, rtol=RTOL, atol=RTOL * l1.abs().max().item())
+
+
+def _mini_mixtral():
+    import dataclasses
+
+    from paper_2602_03495_b200.engine import preset
+    return dataclasses.replace(preset("mixtral-8x7b"), name="mini-mixtral", num_layers=3,
+                               hidden_dim=512, ffn_dim=1024, vocab_size=2048)
+
+
+@pytest.mark.parametrize("resident", [False, True])
+def test_decode_attention_kernel_logits_vs_cpu_model(resident):
+    """head_dim-128 decode path (fused RoPE/KV append + split-K GQA attention,
+    device step descriptor) against the fp32 CPU model, offload and
+    all-resident modes."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine
+    arch = _mini_mixtral()
+    w = ModelWeights(arch, seed=8, resident=resident)
+    cfg = EngineConfig(cache_slots_per_layer=0 if resident else 2, capture=True, seed=1)
+    eng = OffloadEngine(arch, w, default_cost_model(non_moe_layer_time=1.0), cfg, max_seq=64)
+    prompt = torch.randint(0, arch.vocab_size, (2, 9), generator=torch.Generator().manual_seed(6))
+    toks, st = eng.generate(prompt, 7)
+    seq = torch.cat([prompt, toks[:, :-1]], dim=1)
+    S0 = prompt.shape[1]
+    over = {}
+    for l in range(arch.num_layers):
+        parts = [torch.from_numpy(st.topk[(0, l)]).view(2, S0, -1)]
+        for s_ in range(1, len(st.steps_meta)):
+            parts.append(torch.from_numpy(st.topk[(s_, l)]).view(2, 1, -1))
+        over[l] = torch.cat(parts, dim=1).reshape(-1, arch.top_k)
+    dense = M.dense_from_weights(w)
+    blk = (lambda l, e: w.expert_dev(l, e).cpu()) if resident else \
+        (lambda l, e: w.expert_host(l, e))
+    logits, _ = M.forward(arch, dense, blk, seq, over)
+    for s_, lg in enumerate(st.logits):
+        ref = logits[:, S0 - 1 + s_]
+        torch.testing.assert_close(lg, ref, rtol=RTOL, atol=RTOL * ref.abs().max().item())
+
+
+def test_resident_graph_replay_matches_eager():
+    """All-resident decode as one CUDA graph per step == eager launches."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine
+    arch = _mini_mixtral()
+    w = ModelWeights(arch, seed=3, resident=True)
+    cm = default_cost_model(non_moe_layer_time=1.0)
+    g_eng = OffloadEngine(arch, w, cm, EngineConfig(use_graph=True), max_seq=64)
+    e_eng = OffloadEngine(arch, w, cm, EngineConfig(use_graph=False), max_seq=64)
+    prompt = torch.randint(0, arch.vocab_size, (1, 8), generator=torch.Generator().manual_seed(4))
+    for rep in range(2):                    # second request replays the captured graph
+        tg, sg = g_eng.generate(prompt, 10)
+        te, se = e_eng.generate(prompt, 10)
+        assert g_eng._graph is not None
+        assert torch.equal(tg, te), rep
+        for key in se.workloads:
+            assert np.array_equal(sg.workloads[key], se.workloads[key]), (rep, key)
+        dg, de = g_eng.policy.decision_log(), e_eng.policy.decision_log()
+        assert [(r["step"], r["layer"]) for r in dg] == [(r["step"], r["layer"]) for r in de]
+        for a_, b_ in zip(dg, de):
+            assert np.array_equal(a_["G"], b_["G"])
