@@ -310,6 +310,14 @@ int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
                           int32_t splits, float scale, float* workspace,
                           uint16_t* out, void* stream);
 
+/* ---- CPU expert worker (host; DALI hybrid execution) ---------------------
+ * SwiGLU of R token rows x (R, d) bf16 [host] with one expert block [host]
+ * (the engine's W13/W2 layout), y (R, d) f32 [host]; AVX-512 BF16
+ * weight-streaming kernel on a persistent pool of `nthreads` threads.  The
+ * SwiGLU intermediate is rounded to bf16 like the GPU kernel's. */
+int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f,
+                    const uint16_t* x, int32_t R, float* y, int32_t nthreads);
+
 /* Deterministic counter-hash weight init (uniform, given std):
  * out[i] = bf16(std * sqrt(3) * (2*u(seed, offset+i) - 1)). */
 int dali_init_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed,

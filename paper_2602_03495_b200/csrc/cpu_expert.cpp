@@ -1,0 +1,171 @@
+// CPU expert worker (DALI hybrid execution: experts the greedy assignment
+// puts on the CPU run on the host).  Native AVX-512 BF16 kernel for the
+// decode regime (few tokens per expert), where the work is a weight-streaming
+// GEMV bound by host DRAM bandwidth: one pass over the expert block
+// [W13 (2f, d) | W2 (d, f)] bf16 per call, all rows of the token batch
+// multiplied against each 64-byte weight chunk while it is in registers.
+//
+// Threads: a persistent pool partitions weight rows; phase 1 (W13, SwiGLU
+// into a bf16 intermediate -- the same rounding point as the GPU kernel),
+// barrier, phase 2 (W2 -> fp32 outputs).
+#include <immintrin.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "../../include/dali.h"
+
+namespace {
+
+constexpr int kMaxRows = 16;
+
+inline float bf2f(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+inline uint16_t f2bf(float f) {  // round to nearest even
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+class Pool {
+ public:
+  explicit Pool(int n) : n_(n) {
+    for (int i = 1; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return n_; }
+  // run fn(tid) on every thread (caller is tid 0), return when all finished
+  void run(const std::function<void(int)>& fn) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void loop(int tid) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* fn;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        fn = fn_;
+      }
+      (*fn)(tid);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* fn_ = nullptr;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
+Pool* pool_for(int n) {
+  static Pool* p = nullptr;
+  static std::mutex m;
+  std::lock_guard<std::mutex> g(m);
+  if (!p || p->size() != n) {
+    delete p;
+    p = new Pool(n);
+  }
+  return p;
+}
+
+// dot of one weight row (K bf16) with R token rows (K bf16 each) -> R floats
+inline void row_dot(const uint16_t* w, const uint16_t* x, int64_t ldx, int K, int R,
+                    float* out) {
+  __m512 acc[kMaxRows];
+  for (int r = 0; r < R; ++r) acc[r] = _mm512_setzero_ps();
+  for (int k = 0; k < K; k += 32) {
+    const __m512bh wv = (__m512bh)_mm512_loadu_si512(w + k);
+    for (int r = 0; r < R; ++r) {
+      const __m512bh xv = (__m512bh)_mm512_loadu_si512(x + r * ldx + k);
+      acc[r] = _mm512_dpbf16_ps(acc[r], wv, xv);
+    }
+  }
+  for (int r = 0; r < R; ++r) out[r] = _mm512_reduce_add_ps(acc[r]);
+}
+
+}  // namespace
+
+extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, const uint16_t* x,
+                               int32_t R, float* y, int32_t nthreads) {
+  if (!block || !x || !y || d % 32 || f % 64 || R < 0) return DALI_ETRACE;
+  if (R == 0) return DALI_OK;
+  if (R > kMaxRows) {
+    for (int r0 = 0; r0 < R; r0 += kMaxRows) {
+      const int n = R - r0 < kMaxRows ? R - r0 : kMaxRows;
+      int rc = dali_cpu_expert(block, d, f, x + (int64_t)r0 * d, n, y + (int64_t)r0 * d, nthreads);
+      if (rc) return rc;
+    }
+    return DALI_OK;
+  }
+  if (nthreads < 1) nthreads = 1;
+  Pool* pool = pool_for(nthreads);
+  const uint16_t* w13 = block;
+  const uint16_t* w2 = block + (int64_t)2 * f * d;
+  std::vector<uint16_t> hbuf((size_t)R * f);           // SwiGLU intermediate, bf16
+  const int groups = f / 64;
+  // phase 1: group b = rows [128b, 128b+64) gate + [128b+64, 128b+128) up
+  pool->run([&](int tid) {
+    const int g0 = (int)((int64_t)groups * tid / nthreads);
+    const int g1 = (int)((int64_t)groups * (tid + 1) / nthreads);
+    float gv[kMaxRows], uv[kMaxRows];
+    for (int b = g0; b < g1; ++b) {
+      for (int i = 0; i < 64; ++i) {
+        row_dot(w13 + (int64_t)(128 * b + i) * d, x, d, d, R, gv);
+        row_dot(w13 + (int64_t)(128 * b + 64 + i) * d, x, d, d, R, uv);
+        for (int r = 0; r < R; ++r) {
+          const float g = gv[r];
+          hbuf[(size_t)r * f + 64 * b + i] = f2bf(g / (1.0f + std::exp(-g)) * uv[r]);
+        }
+      }
+    }
+  });
+  // phase 2: y[r, m] = h_r . W2_m
+  pool->run([&](int tid) {
+    const int m0 = (int)((int64_t)d * tid / nthreads);
+    const int m1 = (int)((int64_t)d * (tid + 1) / nthreads);
+    float acc[kMaxRows];
+    for (int m = m0; m < m1; ++m) {
+      row_dot(w2 + (int64_t)m * f, hbuf.data(), f, f, R, acc);
+      for (int r = 0; r < R; ++r) y[(int64_t)r * d + m] = acc[r];
+    }
+  });
+  return DALI_OK;
+}

@@ -50,7 +50,7 @@ def build_engine(name: str, cfg: EngineConfig, seed: int = 0, cost_model=None,
     w = weights if weights is not None else ModelWeights(arch, seed=seed, resident=resident,
                                                          experts=experts)
     if cost_model is None:
-        cost_model = profile_cost_model(arch, w, log=log)
+        cost_model = profile_cost_model(arch, w, log=log, threads=cfg.cpu_threads)
     if residuals is None and cfg.prefetch_size > 0 and not resident:
         g = torch.Generator().manual_seed(seed + 99)
         prompts = torch.randint(0, arch.vocab_size, (1, calib_prompt_len), generator=g)

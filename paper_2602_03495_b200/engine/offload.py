@@ -41,6 +41,7 @@ from ..errors import SimulationError
 from ..policy_engine import PolicyEngine
 from ..trace import route_device
 from .arch import MoEArch
+from .cpu_worker import cpu_expert_rows
 from .layers import KVCache, Rope, attention, rms_norm
 from .weights import ModelWeights
 
@@ -459,14 +460,8 @@ class OffloadEngine:
             r0, r1 = int(offs_np[e]), int(offs_np[e + 1])
             if r1 <= r0:
                 continue
-            W13, W2 = self.w.split_expert(self._host_block(l, e).view(torch.bfloat16))
-            xr = rows_host[r0:r1]
-            n = r1 - r0
-            gu = (xr @ W13.t()).view(n, f // 64, 2, 64)
-            g = gu[:, :, 0, :].reshape(n, f).float()
-            u = gu[:, :, 1, :].reshape(n, f).float()
-            act = (torch.nn.functional.silu(g) * u).to(torch.bfloat16)
-            out[r0:r1].copy_((act @ W2.t()).float())
+            cpu_expert_rows(self._host_block(l, e).view(torch.bfloat16), rows_host[r0:r1], d,
+                            f, self.cpu_threads, out=out[r0:r1])
             self.stats.cpu_expert_calls += 1
         return out.to(self.dev, non_blocking=True)
 

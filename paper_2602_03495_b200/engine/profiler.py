@@ -20,15 +20,11 @@ import torch
 from .. import _lib
 from ..cost_model import CostModel, fit_cost_model, quantize_ms
 from .arch import MoEArch
+from .cpu_worker import cpu_expert_rows
 
 
-def _cpu_expert(h: torch.Tensor, W13: torch.Tensor, W2: torch.Tensor, f: int) -> torch.Tensor:
-    R = h.shape[0]
-    gu = (h @ W13.t()).view(R, f // 64, 2, 64)
-    g = gu[:, :, 0, :].reshape(R, f).float()
-    u = gu[:, :, 1, :].reshape(R, f).float()
-    act = (torch.nn.functional.silu(g) * u).to(torch.bfloat16)
-    return (act @ W2.t()).float()
+def _cpu_expert(h: torch.Tensor, blk: torch.Tensor, d: int, f: int, threads: int):
+    return cpu_expert_rows(blk, h, d, f, threads)
 
 
 def _monotone(samples):
@@ -40,7 +36,8 @@ def _monotone(samples):
 
 
 def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
-                       non_moe_ms: float | None = None, log=None, tc: bool = True) -> CostModel:
+                       non_moe_ms: float | None = None, log=None, tc: bool = True,
+                       threads: int | None = None) -> CostModel:
     dev = torch.device("cuda", torch.cuda.current_device())
     d, f, N = arch.hidden_dim, arch.ffn_dim, arch.num_experts
     ws = [1 << i for i in range(0, 32) if (1 << i) <= max_w]
@@ -49,15 +46,16 @@ def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
         blk = weights.expert_host(0, 0)
     else:
         blk = weights.expert_dev(0, 0).cpu()
-    W13, W2 = weights.split_expert(blk)
+    threads = threads or torch.get_num_threads()
+    torch.set_num_threads(threads)
     cpu = []
     for w in ws:
         h = torch.randn(w, d).to(torch.bfloat16)
-        _cpu_expert(h, W13, W2, f)
+        _cpu_expert(h, blk, d, f, threads)
         ts = []
-        for _ in range(reps):
+        for _ in range(reps + 2):
             t0 = time.perf_counter()
-            _cpu_expert(h, W13, W2, f)
+            _cpu_expert(h, blk, d, f, threads)
             ts.append((time.perf_counter() - t0) * 1e3)
         cpu.append((w, quantize_ms(statistics.median(ts))))
     # GPU compute: grouped FFN kernel, one expert resident, w tokens
