@@ -171,8 +171,6 @@ def main():
         arrays[f"{name}_pred"] = np.array(pred)
         arrays[f"{name}_psets"] = np.array(psets)
         meta["traces"][name] = info
-        if d > 256 and name != "tiny_prefill":
-            continue  # full runs only on the small-d traces (and tiny prefill)
         for rn, over in run_cfgs(N):
             cm_run = default_cost_model(non_moe_layer_time=3.0 if "nm3" in rn else 0.0)
             sc = dict(cost_model=cm_run)

@@ -90,5 +90,6 @@ if args.mode in ("decode", "both"):
 if args.mode in ("prefill", "both"):
     run([128] * 8, "prefill 8x128")
 if args.mode == "all":
-    for c in ([1, 1, 0, 0, 0, 0, 0, 0], [4] * 8, [16] * 8, [64] * 8, [256] * 8, [512] * 8):
+    for c in ([1, 0, 0, 0, 0, 0, 0, 0], [1, 1, 0, 0, 0, 0, 0, 0], [2, 1, 0, 0, 0, 0, 0, 0],
+              [4] * 8, [16] * 8, [64] * 8, [128] * 8, [256] * 8, [512] * 8):
         run(c, f"counts {c[0]}x{sum(1 for x in c if x)}")
