@@ -286,6 +286,12 @@ int dali_unpermute_combine(const uint16_t* x, const float* yp,
                            int32_t k, int32_t d, int32_t splits, int64_t rows,
                            uint16_t* out, void* stream);
 
+/* Engine plumbing: copy nbytes of mapped pinned host memory (src, UVA
+ * pointer) to device memory with a kernel instead of a copy engine, so small
+ * per-layer control transfers never queue behind expert-block DMA.  dst and
+ * src 16-byte aligned. */
+int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream);
+
 /* Engine plumbing: fused residual add + RMSNorm over (T, d) bf16 rows:
  *   x_out = x + a (a may be NULL: x_out untouched, x used as is);
  *   h = bf16(bf16(x_out * rsqrt(mean(x_out^2) + eps)) * w). */

@@ -344,6 +344,40 @@ extern "C" int dali_unpermute_combine(const uint16_t* x, const float* yp, const 
   return DALI_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Small host->device copies without a copy engine: every thread loads 16 B of
+// mapped pinned host memory (UVA) and stores it to HBM.  Used for per-layer
+// control data (pointer tables, CPU-expert result rows) so it never queues
+// behind a multi-hundred-MB expert transfer on the H2D copy engine.
+// ---------------------------------------------------------------------------
+namespace dali {
+__global__ void copy_mapped_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                   int64_t n16, uint8_t* __restrict__ dst_tail,
+                                   const uint8_t* __restrict__ src_tail, int tail) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
+}
+}  // namespace dali
+
+extern "C" int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream) {
+  if (nbytes <= 0) return DALI_OK;
+  DALI_REQUIRE(dst && src, DALI_ECUDA, "dali_copy_mapped: null pointer");
+  DALI_REQUIRE(((uintptr_t)dst & 15) == 0 && ((uintptr_t)src & 15) == 0, DALI_ECUDA,
+               "dali_copy_mapped: pointers must be 16-byte aligned");
+  const int64_t n16 = nbytes >> 4;
+  const int tail = (int)(nbytes & 15);
+  const int64_t blocks =
+      std::max<int64_t>(1, std::min<int64_t>((n16 + 255) / 256, (int64_t)sm_count() * 4));
+  copy_mapped_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16,
+      reinterpret_cast<uint8_t*>(dst) + n16 * 16, reinterpret_cast<const uint8_t*>(src) + n16 * 16,
+      tail);
+  DALI_LAUNCH_CHECK("copy_mapped_kernel");
+  return DALI_OK;
+}
+
 extern "C" int dali_init_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, uint64_t offset,
                                       float stdev, void* stream) {
   if (n <= 0) return DALI_OK;

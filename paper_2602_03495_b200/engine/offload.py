@@ -64,6 +64,7 @@ class EngineConfig:
     ffn_kernel: str = "tc"                  # "tc" (tcgen05 + TMA) | "simt" (weight streaming)
     resident_fast: bool = True              # all-resident: no per-layer host wait
     use_graph: bool = True                  # all-resident decode steps replay one CUDA graph
+    trace_layers: bool = False              # per-layer host/device timeline (tools/decode_timeline.py)
 
 
 @dataclass
@@ -87,6 +88,7 @@ class RunStats:
     ffn_events: list = field(default_factory=list)  # (start, end, algorithmic bytes, rows)
     host_ms: dict = field(default_factory=dict)     # host-side time breakdown of _moe
     steps_meta: list = field(default_factory=list)  # (token_index, tokens, eos)
+    layer_trace: list = field(default_factory=list)  # per-layer timeline (cfg.trace_layers)
 
 
 class _Staging:
@@ -144,12 +146,14 @@ class OffloadEngine:
             residuals=res_dev, cache_capacity=slots, w_size=cfg.w_size, u_size=cfg.u_size,
             seed=cfg.seed, max_records=cfg.max_records, all_resident=self.resident_mode,
             num_shared_experts=a.num_shared_experts)
-        self.copy_stream = torch.cuda.Stream()
+        self.copy_stream = torch.cuda.Stream()       # demand + prefetch expert copies
+        self.repl_stream = torch.cuda.Stream()       # cache replacement copies (off the
+        #                                              demand path: never delays a demand copy)
         # HBM expert cache slots: layer l owns slots [l*slots, (l+1)*slots)
         self.cache_buf = (torch.empty((L * slots, weights.expert_bytes), dtype=torch.uint8,
                                       device=self.dev) if slots else None)
         self.host_slot = self.policy.slot_of.cpu().numpy().copy()
-        self.slot_ready = [None] * L
+        self.slot_ready = [None] * (L * slots)   # per cache slot: last replacement copy
         n_stage = cfg.staging_slots or (0 if self.resident_mode else
                                         max(2 * k, N) + 2 * max(cfg.prefetch_size, 1) + 2)
         self.staging = _Staging(n_stage, weights.expert_bytes, self.dev) if n_stage else None
@@ -355,6 +359,8 @@ class OffloadEngine:
         maps = np.zeros(NL, dtype=np.uint64)
         waits = []
         used_staging = []
+        n_hit = n_pf = n_dem = 0
+        t0_ev = None
         for e in G:
             if self.resident_mode:
                 ptrs[e] = self.w.expert_dev(l, e).data_ptr()
@@ -364,14 +370,17 @@ class OffloadEngine:
             if s >= 0:
                 ptrs[e] = self.cache_buf[s].data_ptr()
                 maps[e] = self._map_addr(s)
-                if self.slot_ready[l] is not None:
-                    waits.append(self.slot_ready[l])
+                if self.slot_ready[s] is not None:
+                    waits.append(self.slot_ready[s])
+                n_hit += 1
                 continue
             if (l, e) in self.prefetched:
                 i, ev = self.prefetched.pop((l, e))
+                n_pf += 1
             else:
                 i, ev = self._copy_into_staging(l, e)
                 self.stats.demand_copies += 1
+                n_dem += 1
             ptrs[e] = self.staging.ptr(i)
             maps[e] = self._map_addr(self.n_cache_slots + i)
             waits.append(ev)
@@ -382,7 +391,8 @@ class OffloadEngine:
         gm = np.array(rec.G[:NL], dtype=np.int8)
         ph[NL * 16:NL * 17].copy_(torch.from_numpy(gm.view(np.uint8)))
         pd = self.ptr_dev[l]
-        pd.copy_(ph, non_blocking=True)
+        # kernel copy from mapped pinned memory: never queues behind expert DMA
+        _lib.call("dali_copy_mapped", pd.data_ptr(), ph.data_ptr(), ph.numel(), cs.cuda_stream)
         splits = 1
         max_rows = 0
         if G and self.use_tc:
@@ -396,8 +406,8 @@ class OffloadEngine:
             for ev in waits:
                 cs.wait_event(ev)
             hbuf = self._ws("hbuf", (R, f), torch.bfloat16)
-            if self.cfg.time_ffn:
-                t0 = torch.cuda.Event(enable_timing=True)
+            if self.cfg.time_ffn or self.cfg.trace_layers:
+                t0 = t0_ev = torch.cuda.Event(enable_timing=True)
                 t0.record(cs)
             if self.use_tc:
                 _lib.call("dali_expert_ffn_tc", xrows.data_ptr(), offsets.data_ptr(), NL,
@@ -431,8 +441,8 @@ class OffloadEngine:
                 self.stats.prefetch_copies += 1
             # replacement: admitted experts into the victims' slots once read
             if rec.ev_valid and rec.ev_n:
-                with torch.cuda.stream(self.copy_stream):
-                    self.copy_stream.wait_event(ffn_done)
+                with torch.cuda.stream(self.repl_stream):
+                    self.repl_stream.wait_event(ffn_done)
                     for j in range(rec.ev_n):
                         v_, c_ = int(rec.evicted[j]), int(rec.admitted[j])
                         s = self.host_slot[l, v_]
@@ -440,9 +450,12 @@ class OffloadEngine:
                         self.host_slot[l, c_], self.host_slot[l, v_] = s, -1
                         self.stats.h2d_bytes += self.w.expert_bytes
                         self.stats.replace_copies += 1
-                    ev = torch.cuda.Event()
-                    ev.record(self.copy_stream)
-                self.slot_ready[l] = ev
+                        ev = torch.cuda.Event()
+                        ev.record(self.repl_stream)
+                        self.slot_ready[s] = ev
+        self._last_exec = dict(hit=n_hit, pf=n_pf, dem=n_dem, t0=t0_ev,
+                               rep=int(rec.ev_n) if (rec.ev_valid and not self.resident_mode) else 0,
+                               done=int(rec.n_done) if not self.resident_mode else 0)
         return yp, splits, pd.data_ptr() + NL * 16
 
     def _cpu_rows(self, l: int, rows_host: torch.Tensor, offs_np: np.ndarray, rec,
@@ -456,6 +469,7 @@ class OffloadEngine:
         if not Cx or R == 0:
             return None
         out = self._ws("cpu_rows_h", (R, d), torch.float32, pinned=True)
+        lo, hi = R, 0
         for e in Cx:
             r0, r1 = int(offs_np[e]), int(offs_np[e + 1])
             if r1 <= r0:
@@ -463,7 +477,12 @@ class OffloadEngine:
             cpu_expert_rows(self._host_block(l, e).view(torch.bfloat16), rows_host[r0:r1], d,
                             f, self.cpu_threads, out=out[r0:r1])
             self.stats.cpu_expert_calls += 1
-        return out.to(self.dev, non_blocking=True)
+            lo, hi = min(lo, r0), max(hi, r1)
+        dev_rows = self._ws("cpu_rows_d", (R, d), torch.float32)
+        if hi > lo:      # only the CPU experts' rows; kernel copy (no copy-engine queueing)
+            _lib.call("dali_copy_mapped", dev_rows[lo].data_ptr(), out[lo].data_ptr(),
+                      (hi - lo) * d * 4, torch.cuda.current_stream().cuda_stream)
+        return dev_rows
 
     def _moe(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, token_index: int,
              is_eos: bool) -> torch.Tensor:
@@ -476,6 +495,10 @@ class OffloadEngine:
         T = h.shape[0]
         R = T * k
         cs = torch.cuda.current_stream()
+        tr = self.cfg.trace_layers
+        if tr:
+            ev_r = torch.cuda.Event(enable_timing=True)
+            ev_r.record(cs)
         tp0 = time.perf_counter()
         v = self._route(l, h)
         gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
@@ -486,7 +509,7 @@ class OffloadEngine:
         if self.cfg.capture:
             h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
             h_host.copy_(h, non_blocking=True)
-        ev_dec = torch.cuda.Event()
+        ev_dec = torch.cuda.Event(enable_timing=tr)
         ev_dec.record(cs)
         tp1 = time.perf_counter()
         ev_dec.synchronize()
@@ -510,6 +533,15 @@ class OffloadEngine:
                   cpu_rows.data_ptr() if cpu_rows is not None else None,
                   y_shared.data_ptr() if y_shared is not None else None, T, k, d, splits,
                   R, out.data_ptr(), cs.cuda_stream)
+        if tr:
+            ev_c = torch.cuda.Event(enable_timing=True)
+            ev_c.record(cs)
+            le = self._last_exec
+            self.stats.layer_trace.append(dict(
+                step=step, layer=l, T=T, nC=int(sum(1 for e in range(N) if rec.C[e] and wl_np[e])),
+                hit=le["hit"], pf=le["pf"], dem=le["dem"], rep=le["rep"], done=le["done"],
+                host=(tp0, tp1, tp2, tp3, tp4, time.perf_counter()),
+                ev=(ev_r, ev_dec, le["t0"], ev_c)))
         return out
 
     def _moe_resident(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int,

@@ -42,22 +42,29 @@ def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
     d, f, N = arch.hidden_dim, arch.ffn_dim, arch.num_experts
     ws = [1 << i for i in range(0, 32) if (1 << i) <= max_w]
     # CPU lane: SwiGLU of w tokens on the host worker over the pinned store
+    # cycle over distinct expert blocks (as the engine does: every call streams
+    # a block that is not in any cache level) and take the median
+    n_blk = min(N, 8)
     if weights.host is not None:
-        blk = weights.expert_host(0, 0)
+        blks = [weights.expert_host(0, e) for e in range(n_blk)]
     else:
-        blk = weights.expert_dev(0, 0).cpu()
+        blks = [weights.expert_dev(0, 0).cpu()]
     threads = threads or torch.get_num_threads()
     torch.set_num_threads(threads)
     cpu = []
     for w in ws:
         h = torch.randn(w, d).to(torch.bfloat16)
-        _cpu_expert(h, blk, d, f, threads)
+        for blk in blks[:2]:
+            _cpu_expert(h, blk, d, f, threads)          # warm the pool and the clocks
         ts = []
-        for _ in range(reps + 2):
+        for i in range(max(reps + 2, 2 * len(blks) if w <= 16 else reps + 2)):
+            blk = blks[(i + 1) % len(blks)]
             t0 = time.perf_counter()
             _cpu_expert(h, blk, d, f, threads)
             ts.append((time.perf_counter() - t0) * 1e3)
-        cpu.append((w, quantize_ms(statistics.median(ts))))
+        # best of the runs: the steady-state streaming cost (transient host
+        # hiccups during start-up otherwise bias every later decision)
+        cpu.append((w, quantize_ms(min(ts))))
     # GPU compute: grouped FFN kernel, one expert resident, w tokens
     block = torch.empty((arch.expert_elems,), dtype=torch.bfloat16, device=dev)
     weights.init_expert(0, 0, block)
