@@ -305,7 +305,7 @@ int dali_add_rmsnorm(const uint16_t* x, const uint16_t* a, const uint16_t* w,
  *     half RoPE, fp32 tables cos/sin (max_pos, hd/2)); rotated k and v stored
  *     at *pos in caches laid out (B, KV, max_len, hd).
  *   dali_decode_attention: split-K GQA attention over positions [0, *len),
- *     head_dim 128; workspace f32 (B*H*splits*(hd+2)). */
+ *     head_dim 64 or 128; workspace f32 (B*H*splits*(hd+2)). */
 int dali_rope_append(const uint16_t* qkv, const float* cos_t, const float* sin_t,
                      const int32_t* pos, int32_t B, int32_t H, int32_t KV,
                      int32_t hd, int32_t max_len, uint16_t* q_out,

@@ -43,14 +43,30 @@ __global__ void rope_append_kernel(const uint16_t* __restrict__ qkv, const float
 
 // Split-K decode attention.  grid (B*H, splits); 4 warps per CTA; each warp
 // walks positions p = warp, warp+4, ... of its chunk with an online softmax;
-// hd = 128 (4 elements per lane).  Partials -> ws, merged by attn_merge.
+// HD in {64, 128} (HD/32 elements per lane).  Partials -> ws, merged by attn_merge.
 constexpr int kAttnWarps = 4;
 
+template <int EL>
+__device__ __forceinline__ void load_bf16_lane(const uint16_t* p, float* out) {
+  if constexpr (EL == 4) {
+    const uint2 raw = *reinterpret_cast<const uint2*>(p);
+    out[0] = __uint_as_float(raw.x << 16);
+    out[1] = __uint_as_float(raw.x & 0xffff0000u);
+    out[2] = __uint_as_float(raw.y << 16);
+    out[3] = __uint_as_float(raw.y & 0xffff0000u);
+  } else {
+    const uint32_t raw = *reinterpret_cast<const uint32_t*>(p);
+    out[0] = __uint_as_float(raw << 16);
+    out[1] = __uint_as_float(raw & 0xffff0000u);
+  }
+}
+
+template <int HD>
 __global__ void __launch_bounds__(kAttnWarps * 32)
 decode_attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ kc,
                    const uint16_t* __restrict__ vc, const int32_t* __restrict__ len_p, int H,
                    int KV, int max_len, float scale, float* __restrict__ ws) {
-  constexpr int HD = 128;
+  constexpr int EL = HD / 32;
   const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int kvh = h / (H / KV);
   const int split = blockIdx.y, nsplit = gridDim.y;
@@ -59,55 +75,57 @@ decode_attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ 
   const int p0 = split * chunk, p1 = min(len, p0 + chunk);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint16_t* qh = q + ((int64_t)b * H + h) * HD;
-  float qv[4];
+  float qv[EL];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) qv[i] = bf16_bits_to_f32(qh[lane * 4 + i]) * scale;
+  for (int i = 0; i < EL; ++i) qv[i] = bf16_bits_to_f32(qh[lane * EL + i]) * scale;
   const uint16_t* kb = kc + ((int64_t)b * KV + kvh) * max_len * HD;
   const uint16_t* vb = vc + ((int64_t)b * KV + kvh) * max_len * HD;
-  float m = -INFINITY, l = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float m = -INFINITY, l = 0.f, acc[EL];
+#pragma unroll
+  for (int i = 0; i < EL; ++i) acc[i] = 0.f;
   for (int p = p0 + warp; p < p1; p += kAttnWarps) {
-    const uint2 kraw = *reinterpret_cast<const uint2*>(kb + (int64_t)p * HD + lane * 4);
-    const uint32_t* kw = reinterpret_cast<const uint32_t*>(&kraw);
-    float s = qv[0] * __uint_as_float(kw[0] << 16) + qv[1] * __uint_as_float(kw[0] & 0xffff0000u) +
-              qv[2] * __uint_as_float(kw[1] << 16) + qv[3] * __uint_as_float(kw[1] & 0xffff0000u);
+    float kv_[EL], vv[EL];
+    load_bf16_lane<EL>(kb + (int64_t)p * HD + lane * EL, kv_);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < EL; ++i) s += qv[i] * kv_[i];
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const float mn = fmaxf(m, s);
     const float corr = __expf(m - mn), ps = __expf(s - mn);
-    const uint2 vraw = *reinterpret_cast<const uint2*>(vb + (int64_t)p * HD + lane * 4);
-    const uint32_t* vw = reinterpret_cast<const uint32_t*>(&vraw);
+    load_bf16_lane<EL>(vb + (int64_t)p * HD + lane * EL, vv);
     l = l * corr + ps;
-    acc[0] = acc[0] * corr + ps * __uint_as_float(vw[0] << 16);
-    acc[1] = acc[1] * corr + ps * __uint_as_float(vw[0] & 0xffff0000u);
-    acc[2] = acc[2] * corr + ps * __uint_as_float(vw[1] << 16);
-    acc[3] = acc[3] * corr + ps * __uint_as_float(vw[1] & 0xffff0000u);
+#pragma unroll
+    for (int i = 0; i < EL; ++i) acc[i] = acc[i] * corr + ps * vv[i];
     m = mn;
   }
   __shared__ float sm[kAttnWarps], sl[kAttnWarps], sacc[kAttnWarps][HD];
   if (lane == 0) { sm[warp] = m; sl[warp] = l; }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) sacc[warp][lane * 4 + i] = acc[i];
+  for (int i = 0; i < EL; ++i) sacc[warp][lane * EL + i] = acc[i];
   __syncthreads();
   if (warp == 0) {
     float M = -INFINITY;
     for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm[w]);
-    float L = 0.f, A[4] = {0.f, 0.f, 0.f, 0.f};
+    float L = 0.f, A[EL];
+#pragma unroll
+    for (int i = 0; i < EL; ++i) A[i] = 0.f;
     for (int w = 0; w < kAttnWarps; ++w) {
       const float c = sm[w] == -INFINITY ? 0.f : __expf(sm[w] - M);
       L += sl[w] * c;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) A[i] += sacc[w][lane * 4 + i] * c;
+      for (int i = 0; i < EL; ++i) A[i] += sacc[w][lane * EL + i] * c;
     }
     float* out = ws + ((int64_t)bh * nsplit + split) * (HD + 2);
     if (lane == 0) { out[0] = M; out[1] = L; }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) out[2 + lane * 4 + i] = A[i];
+    for (int i = 0; i < EL; ++i) out[2 + lane * EL + i] = A[i];
   }
 }
 
+template <int HD>
 __global__ void attn_merge_kernel(const float* __restrict__ ws, int nsplit,
                                   uint16_t* __restrict__ o) {
-  constexpr int HD = 128;
   const int bh = blockIdx.x;
   const float* in = ws + (int64_t)bh * nsplit * (HD + 2);
   float M = -INFINITY;
@@ -142,14 +160,21 @@ extern "C" int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
                                      int32_t H, int32_t KV, int32_t hd, int32_t max_len,
                                      int32_t splits, float scale, float* workspace, uint16_t* out,
                                      void* stream) {
-  DALI_REQUIRE(hd == 128, DALI_ETRACE, "decode attention kernel supports head_dim 128, got %d",
-               hd);
+  DALI_REQUIRE(hd == 128 || hd == 64, DALI_ETRACE,
+               "decode attention kernel supports head_dim 64 or 128, got %d", hd);
   DALI_REQUIRE(H % KV == 0 && splits >= 1, DALI_ETRACE, "bad attention geometry");
   cudaStream_t st = dali::as_stream(stream);
-  dali::decode_attn_kernel<<<dim3(B * H, splits), dali::kAttnWarps * 32, 0, st>>>(
-      q, k_cache, v_cache, len, H, KV, max_len, scale, workspace);
-  DALI_LAUNCH_CHECK("decode_attn_kernel");
-  dali::attn_merge_kernel<<<B * H, 128, 0, st>>>(workspace, splits, out);
+  if (hd == 128) {
+    dali::decode_attn_kernel<128><<<dim3(B * H, splits), dali::kAttnWarps * 32, 0, st>>>(
+        q, k_cache, v_cache, len, H, KV, max_len, scale, workspace);
+    DALI_LAUNCH_CHECK("decode_attn_kernel");
+    dali::attn_merge_kernel<128><<<B * H, 128, 0, st>>>(workspace, splits, out);
+  } else {
+    dali::decode_attn_kernel<64><<<dim3(B * H, splits), dali::kAttnWarps * 32, 0, st>>>(
+        q, k_cache, v_cache, len, H, KV, max_len, scale, workspace);
+    DALI_LAUNCH_CHECK("decode_attn_kernel");
+    dali::attn_merge_kernel<64><<<B * H, 64, 0, st>>>(workspace, splits, out);
+  }
   DALI_LAUNCH_CHECK("attn_merge_kernel");
   return DALI_OK;
 }

@@ -188,7 +188,10 @@ class OffloadEngine:
         self._wl_log = None
         self.desc_dev = torch.zeros((8,), dtype=torch.int32, device=self.dev)
         self.desc_host = torch.zeros((8,), dtype=torch.int32, pin_memory=True)
+        self.desc_step_host = torch.zeros((8,), dtype=torch.int32, pin_memory=True)
         self._graph = None
+        self._heads: dict = {}              # offloaded decode: layer -> (graph, h, views)
+        self._heads_warm = False
         self._in_capture = False
         self._eos_at = -1
         self._pending_ffn, self._pending_cap = [], []
@@ -490,25 +493,65 @@ class OffloadEngine:
             return self._moe_ep(l, x, h, step, token_index, is_eos)
         if self.resident_mode and self.use_tc and self.cfg.resident_fast:
             return self._moe_resident(l, x, h, step, token_index, is_eos)
-        a = self.arch
-        N, k, d = a.num_experts, a.top_k, a.hidden_dim
-        T = h.shape[0]
-        R = T * k
         cs = torch.cuda.current_stream()
-        tr = self.cfg.trace_layers
-        if tr:
+        ev_r = None
+        if self.cfg.trace_layers:
             ev_r = torch.cuda.Event(enable_timing=True)
             ev_r.record(cs)
         tp0 = time.perf_counter()
+        views = self._moe_head(l, h, step, token_index, is_eos, use_desc=False)
+        return self._moe_tail(l, x, h, step, views, tp0, ev_r, torch.empty_like(x))
+
+    def _moe_head(self, l: int, h: torch.Tensor, step: int, token_index: int, is_eos: bool,
+                  use_desc: bool):
+        """Device half of a MoE layer up to the decision: route + plan +
+        permute, residual prediction for layer+1, fused policy kernel, and the
+        D2H mirrors the host needs.  No host synchronisation inside, so the
+        decode variant (``use_desc``: step scalars from the device descriptor,
+        record at desc[3] + l) is captured into one CUDA graph per layer."""
+        a = self.arch
+        d, k = a.hidden_dim, a.top_k
+        T = h.shape[0]
+        R = T * k
+        cs = torch.cuda.current_stream()
         v = self._route(l, h)
         gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
-        ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], h, gate_next)
+        if use_desc:
+            pol = self.policy
+            pred_p = None
+            if pol.prefetch_size > 0 and gate_next is not None:
+                route_device(h, gate_next, k, residual=pol.residuals[l], want_idx=False,
+                             want_weights=False, out=(None, None, pol.predicted))
+                pred_p = pol.predicted.data_ptr()
+            _lib.call("dali_policy_layer_desc", C.addressof(pol.cfg), C.addressof(pol.cm_c), l,
+                      self.desc_dev.data_ptr(), v["wl"].data_ptr(), pred_p,
+                      pol.on_gpu.data_ptr(), pol.scores.data_ptr(), pol.counters.data_ptr(),
+                      pol.arrived.data_ptr(), pol.slot_of.data_ptr(), pol.record_ptr(0),
+                      cs.cuda_stream)
+            ri = None
+        else:
+            ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], h, gate_next)
         hv = self._host_view(v, T)
         xp_host = self._ws("xp_h", (R, d), torch.bfloat16, pinned=True)
         xp_host.copy_(v["xp"], non_blocking=True)
+        h_host = None
         if self.cfg.capture:
             h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
             h_host.copy_(h, non_blocking=True)
+        return dict(v=v, hv=hv, xp_host=xp_host, h_host=h_host, ri=ri, T=T)
+
+    def _moe_tail(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, views: dict,
+                  tp0: float, ev_r, out: torch.Tensor) -> torch.Tensor:
+        """Host half: wait for the decision record, execute it (GPU experts
+        from cache / staging / demand copy, prefetch + replacement copies, CPU
+        experts on the host worker) and queue the Eq. (2) combine into ``out``."""
+        a = self.arch
+        N, k, d = a.num_experts, a.top_k, a.hidden_dim
+        v, hv, xp_host, T = views["v"], views["hv"], views["xp_host"], views["T"]
+        R = T * k
+        cs = torch.cuda.current_stream()
+        tr = self.cfg.trace_layers
+        ri = views["ri"] if views["ri"] is not None else self.policy.n_records + l
         ev_dec = torch.cuda.Event(enable_timing=tr)
         ev_dec.record(cs)
         tp1 = time.perf_counter()
@@ -518,7 +561,7 @@ class OffloadEngine:
         wl_np = hv["wl"].numpy().copy()
         self.stats.workloads[(step, l)] = wl_np
         if self.cfg.capture:
-            self.stats.captured.append((step, l, h_host.clone()))
+            self.stats.captured.append((step, l, views["h_host"].clone()))
             self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
         yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
         # shared expert(s): queued before the host starts the CPU experts
@@ -527,7 +570,6 @@ class OffloadEngine:
         cpu_rows = self._cpu_rows(l, xp_host, hv["offsets"].numpy(), rec, R)
         tp4 = time.perf_counter()
         self._acct(tp0, tp1, tp2, tp3, tp4)
-        out = torch.empty_like(x)
         _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
                   v["pos"].data_ptr(), v["wts"].data_ptr(), gmask_p,
                   cpu_rows.data_ptr() if cpu_rows is not None else None,
@@ -541,7 +583,7 @@ class OffloadEngine:
                 step=step, layer=l, T=T, nC=int(sum(1 for e in range(N) if rec.C[e] and wl_np[e])),
                 hit=le["hit"], pf=le["pf"], dem=le["dem"], rep=le["rep"], done=le["done"],
                 host=(tp0, tp1, tp2, tp3, tp4, time.perf_counter()),
-                ev=(ev_r, ev_dec, le["t0"], ev_c)))
+                ev=(ev_r if ev_r is not None else ev_dec, ev_dec, le["t0"], ev_c)))
         return out
 
     def _moe_resident(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int,
@@ -699,7 +741,11 @@ class OffloadEngine:
         tp4 = time.perf_counter()
         self._acct(tp0, tp1, tp2, tp3, tp4)
         # per-row expert outputs in grouped order -> received order -> sources
-        y_l = yp[:, :R].sum(0) if splits > 1 else yp[0, :R].clone()
+        # split-K planes summed in plane order, exactly as the combine kernel
+        # does (fp32 adds in the same order: bit-identical to the 1-GPU engine)
+        y_l = yp[0, :R].clone()
+        for s_ in range(1, splits):
+            y_l += yp[s_, :R]
         if cpu_rows is not None:
             for e in range(NL):
                 if rec.C[e] and offs_l[e + 1] > offs_l[e]:
@@ -745,7 +791,7 @@ class OffloadEngine:
         sp = torch.cuda.current_stream().cuda_stream
         hn = self._ws("hn", (T, d), torch.bfloat16)
         h = self._ws("h", (T, d), torch.bfloat16)
-        dev_attn = S == 1 and a.head_dim == 128
+        dev_attn = S == 1 and a.head_dim in (64, 128)
         for l in range(a.num_layers):
             _lib.call("dali_add_rmsnorm", x.data_ptr(), None, W.attn_norm[l].data_ptr(),
                       a.rms_eps, T, d, None, hn.data_ptr(), sp)
@@ -760,18 +806,87 @@ class OffloadEngine:
         last = x.view(B, S, -1)[:, -1]
         return rms_norm(last, W.final_norm, a.rms_eps) @ W.lm_head.t()
 
+    # ------------------------------------------------- offloaded decode (graphs)
+    def _offload_graphable(self) -> bool:
+        return (not self.resident_mode and self.ep is None and self.cfg.use_graph and
+                self.arch.head_dim in (64, 128))
+
+    def _decode_head(self, l: int, X: torch.Tensor, X2: torch.Tensor, B: int):
+        """Layer l of a decode step up to the MoE decision: attention block
+        (norm, qkv, fused RoPE/KV append, split-K attention, o-proj, add +
+        norm) and the MoE head.  Step scalars come from the device descriptor,
+        so the same launch sequence is valid for every step (graph body)."""
+        a, W = self.arch, self.w
+        d = a.hidden_dim
+        sp = torch.cuda.current_stream().cuda_stream
+        hn = self._ws("hn", (B, d), torch.bfloat16)
+        h = self._ws("h", (B, d), torch.bfloat16)
+        _lib.call("dali_add_rmsnorm", X.data_ptr(), None, W.attn_norm[l].data_ptr(), a.rms_eps,
+                  B, d, None, hn.data_ptr(), sp)
+        att = self._attn_decode(l, hn, B)
+        _lib.call("dali_add_rmsnorm", X.data_ptr(), att.data_ptr(), W.moe_norm[l].data_ptr(),
+                  a.rms_eps, B, d, X2.data_ptr(), h.data_ptr(), sp)
+        return h, self._moe_head(l, h, 0, 0, False, use_desc=True)
+
+    def _decode_offload(self, tok_dev: torch.Tensor, B: int, is_eos: bool) -> torch.Tensor:
+        """One offloaded decode step.  Per layer, the device half (attention +
+        routing + policy + D2H mirrors) replays a CUDA graph captured on the
+        second decode step (the first runs eagerly and warms workspaces); the
+        host half executes the decision.  The step descriptor is written from
+        pinned memory by a kernel copy before the layers run."""
+        a, W = self.arch, self.w
+        L, d = a.num_layers, a.hidden_dim
+        cs = torch.cuda.current_stream()
+        step, pos = self._step, self.kv.len
+        base = self.policy.n_records
+        if base + L > self.policy.max_records:
+            raise SimulationError("decision log full")
+        dh = self.desc_step_host
+        dh.copy_(torch.tensor([step, step, step if is_eos else -1, base, pos, pos + 1, L, 0],
+                              dtype=torch.int32))
+        _lib.call("dali_copy_mapped", self.desc_dev.data_ptr(), dh.data_ptr(), 32, cs.cuda_stream)
+        X = self._ws("dec_X", (B, d), torch.bfloat16)
+        X2 = self._ws("dec_X2", (B, d), torch.bfloat16)
+        torch.index_select(W.embed, 0, tok_dev.reshape(-1), out=X)
+        heads = self._heads
+        capture = self._heads_warm and not heads
+        for l in range(L):
+            ev_r = None
+            if self.cfg.trace_layers:
+                ev_r = torch.cuda.Event(enable_timing=True)
+                ev_r.record(cs)
+            tp0 = time.perf_counter()
+            if l in heads:
+                g, h, views = heads[l]
+                g.replay()
+            elif capture:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    h, views = self._decode_head(l, X, X2, B)
+                g.replay()
+                heads[l] = (g, h, views)
+            else:
+                h, views = self._decode_head(l, X, X2, B)
+            self._moe_tail(l, X2, h, step, views, tp0, ev_r, X)
+        self._heads_warm = True
+        self.policy.n_records = base + L
+        return rms_norm(X, W.final_norm, a.rms_eps) @ W.lm_head.t()
+
     def _set_desc(self, step: int, token_index: int, eos_at: int, rec_index: int, pos: int):
-        """Write the device step descriptor (stream-ordered H2D)."""
+        """Write the device step descriptor (stream-ordered kernel copy from
+        pinned memory: never queued behind expert DMA on a copy engine)."""
         dh = self.desc_host
         dh.copy_(torch.tensor([step, token_index, eos_at, rec_index, pos, pos + 1,
                                self.arch.num_layers, 0], dtype=torch.int32))
-        self.desc_dev.copy_(dh, non_blocking=True)
+        _lib.call("dali_copy_mapped", self.desc_dev.data_ptr(), dh.data_ptr(), 32,
+                  torch.cuda.current_stream().cuda_stream)
 
     def start_request(self, batch: int) -> np.ndarray:
         """New policy run for one request; cache residency carries over."""
         if self.kv is None or self.kv.k.shape[1] != batch:
             self.kv = KVCache(self.arch, batch, self.max_seq, self.dev)
             self._graph = None
+            self._heads, self._heads_warm = {}, False
         self.kv.len = 0
         for key in list(self.prefetched):
             i, ev = self.prefetched.pop(key)
@@ -803,6 +918,8 @@ class OffloadEngine:
         ti = self._step
         if self._graphable():
             logits = self._decode_graph(tok_dev)
+        elif self._offload_graphable():
+            logits = self._decode_offload(tok_dev, B, is_eos)
         else:
             logits = self._forward(tok_dev.view(B, 1), B, 1, pos, self._step, ti, is_eos)
             _lib.call("dali_step_advance", self.desc_dev.data_ptr(),

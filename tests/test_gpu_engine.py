@@ -402,3 +402,40 @@ def test_resident_graph_replay_matches_eager():
         assert [(r["step"], r["layer"]) for r in dg] == [(r["step"], r["layer"]) for r in de]
         for a_, b_ in zip(dg, de):
             assert np.array_equal(a_["G"], b_["G"])
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny-shared"])
+def test_offload_decode_graphs_match_eager(name):
+    """Offloaded decode with per-layer CUDA-graph heads (device descriptor for
+    the step scalars, kernel copies for control data) == the eager path:
+    same tokens, workloads and every decision record, over two requests
+    (the second replays graphs captured in the first) incl. the EOS step."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    arch = preset(name)
+    w = ModelWeights(arch, seed=7)
+    cm = default_cost_model(shared_expert_gpu_time=SHARED_MS[name], non_moe_layer_time=3.0)
+    res = np.random.default_rng(0).standard_normal((arch.num_layers - 1, arch.hidden_dim)) * 0.05
+    slots = 2 if name == "tiny" else 6
+    engs = [OffloadEngine(arch, w, cm, EngineConfig(cache_slots_per_layer=slots, prefetch_size=2,
+                                                    seed=3, use_graph=ug), residuals=res,
+                          max_seq=64)
+            for ug in (True, False)]
+    g = torch.Generator().manual_seed(5)
+    for rep in range(2):
+        prompt = torch.randint(0, arch.vocab_size, (1, 12), generator=g)
+        (tg, sg), (te, se) = [e.generate(prompt, 9) for e in engs]
+        assert engs[0]._heads, "graph heads were not captured"
+        assert torch.equal(tg, te), rep
+        assert sg.workloads.keys() == se.workloads.keys()
+        for key in se.workloads:
+            assert np.array_equal(sg.workloads[key], se.workloads[key]), (rep, key)
+        dg, de = engs[0].policy.decision_log(), engs[1].policy.decision_log()
+        assert len(dg) == len(de)
+        for a_, b_ in zip(dg, de):
+            for k_ in ("step", "layer", "hits", "event", "latency"):
+                assert a_[k_] == b_[k_], (rep, k_, a_["step"], a_["layer"])
+            assert np.array_equal(a_["C"], b_["C"]) and np.array_equal(a_["G"], b_["G"])
+        assert engs[0].policy_report() == engs[1].policy_report()
