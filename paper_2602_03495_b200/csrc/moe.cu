@@ -202,12 +202,15 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
                                const float* __restrict__ cpu_rows,
                                const float* __restrict__ extra, int64_t T, int k, int d,
                                int splits, int64_t plane, uint16_t* __restrict__ out) {
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // one thread per (token, 8-column chunk): all of a row's chunks load their
+  // k x splits partial rows concurrently (decode: T=1 is latency-bound)
   const int d8 = d >> 3;
-  for (int64_t t = warp; t < T; t += nw) {
-    for (int c = lane; c < d8; c += 32) {
+  const int64_t items = T * d8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += stride) {
+    const int64_t t = it / d8;
+    const int c = (int)(it - t * d8);
+    {
       float acc[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.f;
@@ -334,7 +337,7 @@ extern "C" int dali_unpermute_combine(const uint16_t* x, const float* yp, const 
                                       void* stream) {
   DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
   if (T <= 0) return DALI_OK;
-  const int64_t blocks = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 8);
+  const int64_t blocks = std::min<int64_t>((T * (d / 8) + 255) / 256, (int64_t)sm_count() * 8);
   combine_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(x, yp, topk_idx, pos, topk_w,
                                                                   gpu_mask, cpu_rows, extra, T, k,
                                                                   d,

@@ -17,7 +17,13 @@ namespace dali {
 constexpr int kRouteThreads = 256;
 // tokens per CTA (TB <= warps per CTA) is a template parameter: 8 for long
 // prompts, fewer when T is small so the grid still covers the SMs.
-constexpr int kRouteCH = 256;    // hidden chunk staged per iteration
+// hidden chunk staged per iteration: as much of the CTA's rows as fits the
+// 64 KB staging budget (decode: the whole row in one pass, so the loop is not
+// a chain of global-load latencies).  Always a multiple of S = 256 / N's
+// largest value (256), so every thread visits its d-slice in the same order
+// whatever the chunking (bit-identical sums).
+constexpr int kRouteStageBytes = 64 * 1024;
+template <int TB> constexpr int route_ch() { return kRouteStageBytes / (8 * TB); }
 
 template <typename TH, typename TW, int kRouteTB>
 __global__ void __launch_bounds__(kRouteThreads)
@@ -25,11 +31,13 @@ route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
              const TW* __restrict__ gate, int64_t T, int d, int N, int k,
              int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
              unsigned long long* __restrict__ workloads) {
-  __shared__ double sh_h[kRouteTB][kRouteCH];
+  constexpr int kRouteCH = route_ch<kRouteTB>();
   __shared__ double sh_red[kRouteTB * DALI_MAX_EXPERTS];   // logits, then probs
   __shared__ int sh_hist[DALI_MAX_EXPERTS];
   __shared__ int sh_sel[kRouteTB][DALI_MAX_TOPK];
-  extern __shared__ double sh_part[];                      // [TB][N][S]
+  extern __shared__ double sh_dyn[];
+  double (*sh_h)[kRouteCH] = reinterpret_cast<double (*)[kRouteCH]>(sh_dyn);   // [TB][CH]
+  double* sh_part = sh_dyn + kRouteTB * kRouteCH;                              // [TB][N][S]
 
   const int tid = threadIdx.x;
   const int S = kRouteThreads / N;                          // >= 1 (N <= 256)
@@ -59,6 +67,7 @@ route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
     }
     __syncthreads();
     if (active) {
+#pragma unroll 8
       for (int i = s; i < cn; i += S) {
         const double w = to_f64(gate[(int64_t)(c0 + i) * N + e]);
 #pragma unroll
@@ -149,28 +158,29 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
   if (T == 0) return DALI_OK;
   const int S = kRouteThreads / N;
   DALI_REQUIRE((T + 1) / 2 < (1ll << 31), DALI_ETRACE, "too many tokens");
-  static bool attr_set = false;   // static smem (up to 34 KB) + dynamic (16 KB) > 48 KB default
+  // dynamic smem = staged hidden rows (64 KB) + partial logits (TB*N*S doubles)
+  static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(route_kernel<TH, TW, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         64 * 1024);
+                         kRouteStageBytes + 8 * 8 * kRouteThreads);
     cudaFuncSetAttribute(route_kernel<TH, TW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         64 * 1024);
+                         kRouteStageBytes + 8 * 4 * kRouteThreads);
     cudaFuncSetAttribute(route_kernel<TH, TW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         64 * 1024);
+                         kRouteStageBytes + 8 * 2 * kRouteThreads);
     attr_set = true;
   }
   auto* ul = reinterpret_cast<unsigned long long*>(workloads);
   if (T >= 8 * 148) {
     route_kernel<TH, TW, 8><<<(unsigned)((T + 7) / 8), kRouteThreads,
-                              sizeof(double) * 8 * N * S, st>>>(
+                              kRouteStageBytes + sizeof(double) * 8 * N * S, st>>>(
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
   } else if (T >= 4 * 148) {
     route_kernel<TH, TW, 4><<<(unsigned)((T + 3) / 4), kRouteThreads,
-                              sizeof(double) * 4 * N * S, st>>>(
+                              kRouteStageBytes + sizeof(double) * 4 * N * S, st>>>(
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
   } else {
     route_kernel<TH, TW, 2><<<(unsigned)((T + 1) / 2), kRouteThreads,
-                              sizeof(double) * 2 * N * S, st>>>(
+                              kRouteStageBytes + sizeof(double) * 2 * N * S, st>>>(
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
   }
   DALI_LAUNCH_CHECK("route_kernel");
