@@ -286,10 +286,11 @@ int dali_unpermute_combine(const uint16_t* x, const float* yp,
                            int32_t k, int32_t d, int32_t splits, int64_t rows,
                            uint16_t* out, void* stream);
 
-/* Engine plumbing: copy nbytes of mapped pinned host memory (src, UVA
- * pointer) to device memory with a kernel instead of a copy engine, so small
- * per-layer control transfers never queue behind expert-block DMA.  dst and
- * src 16-byte aligned. */
+/* Engine plumbing: copy nbytes between UVA addresses (device memory and/or
+ * mapped pinned host memory, either direction) with a kernel instead of a
+ * copy engine, so small per-layer control transfers and per-token reads never
+ * queue behind expert-block DMA.  16-byte aligned pointers take the vector
+ * path; unaligned copies are byte-wise and limited to 1 MiB. */
 int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream);
 
 /* Engine plumbing: fused residual add + RMSNorm over (T, d) bf16 rows:

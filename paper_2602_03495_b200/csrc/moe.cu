@@ -362,13 +362,25 @@ __global__ void copy_mapped_kernel(uint4* __restrict__ dst, const uint4* __restr
     dst[i] = src[i];
   if (blockIdx.x == 0 && threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
 }
+__global__ void copy_bytes_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                  int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
 }  // namespace dali
 
 extern "C" int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream) {
   if (nbytes <= 0) return DALI_OK;
   DALI_REQUIRE(dst && src, DALI_ECUDA, "dali_copy_mapped: null pointer");
-  DALI_REQUIRE(((uintptr_t)dst & 15) == 0 && ((uintptr_t)src & 15) == 0, DALI_ECUDA,
-               "dali_copy_mapped: pointers must be 16-byte aligned");
+  const bool aligned = (((uintptr_t)dst | (uintptr_t)src) & 15) == 0;
+  if (!aligned) {             // small unaligned transfers (token ids): byte copies
+    DALI_REQUIRE(nbytes <= (1 << 20), DALI_ECUDA,
+                 "dali_copy_mapped: unaligned copies are limited to 1 MiB");
+    copy_bytes_kernel<<<(unsigned)((nbytes + 255) / 256), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src), nbytes);
+    DALI_LAUNCH_CHECK("copy_bytes_kernel");
+    return DALI_OK;
+  }
   const int64_t n16 = nbytes >> 4;
   const int tail = (int)(nbytes & 15);
   const int64_t blocks =

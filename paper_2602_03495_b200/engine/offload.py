@@ -983,18 +983,39 @@ class OffloadEngine:
         cs = torch.cuda.current_stream()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(cs)
-        p_dev = prompt.to(self.dev, non_blocking=True) if host_io else prompt
-        fetch = (lambda t: t.to("cpu")) if host_io else (lambda t: t)
+        if host_io:
+            # host I/O through pinned staging + kernel copies (UVA): neither the
+            # prompt upload nor the per-token read can queue behind expert DMA
+            # on a copy engine
+            p_pin = self._ws("prompt_h", (B, S), torch.int64, pinned=True)
+            p_pin.copy_(prompt)
+            p_dev = self._ws("prompt_d", (B, S), torch.int64)
+            _lib.call("dali_copy_mapped", p_dev.data_ptr(), p_pin.data_ptr(), B * S * 8,
+                      cs.cuda_stream)
+            toks_h = self._ws("tokens_h", (max(max_new_tokens, 1), B), torch.int64, pinned=True)
+
+            def fetch(t, i):
+                _lib.call("dali_copy_mapped", toks_h[i].data_ptr(), t.data_ptr(), B * 8,
+                          torch.cuda.current_stream().cuda_stream)
+                ev = torch.cuda.Event()
+                ev.record()
+                ev.synchronize()
+                return toks_h[i].clone()
+        else:
+            p_dev = prompt
+
+            def fetch(t, i):
+                return t
         logits = self.prefill(p_dev, is_eos=(max_new_tokens <= 1))
         nxt = logits.argmax(-1)
-        out = [fetch(nxt)]
+        out = [fetch(nxt, 0)]
         if self.cfg.capture:
             self.stats.logits.append(logits.float().cpu())
         e1.record(cs)
         for i in range(max_new_tokens - 1):
             logits = self.decode(nxt, is_eos=(i == max_new_tokens - 2))
             nxt = logits.argmax(-1)
-            out.append(fetch(nxt))
+            out.append(fetch(nxt, i + 1))
             if self.cfg.capture:
                 self.stats.logits.append(logits.float().cpu())
         e2.record(cs)
