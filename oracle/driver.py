@@ -27,13 +27,22 @@ class DriverConfig:
     """Subset of the reference ``SimConfig`` (simulator.py:45-74) on the path."""
 
     tables: P.CostTables
-    assignment_policy: str = "greedy"          # "greedy" | "all-cpu"
+    assignment_policy: str = "greedy"          # greedy | all-cpu | all-gpu | beam |
+    #                                            optimal | static-threshold
     gpu_capacity: int | None = None
+    beam_width: int = 2
+    threshold: float | None = None
+    exact_solver_limit: int = 24
     prefetch_size: int = 0                     # 0 = prefetch off
+    prefetch_kind: str = "residual"            # residual | feature | statistical | random
     residuals: np.ndarray | None = None        # (L-1, d)
+    frequency_table: np.ndarray | None = None  # (L, N) statistical predictor
     cache_capacity: int = 0                    # 0 = cache off
+    cache_policy: str = "workload"             # workload | lru | score
     w_size: int = 4
     u_size: int | None = None
+    insert_demand_fetched: bool = False
+    insert_prefetched: bool = False
     scheduling_overhead_ms: float = 0.0
     solver_node_cost_ms: float = 0.0
     prefetch_compute_ms: float = 0.0
@@ -62,6 +71,7 @@ class LayerRecord:
     C: np.ndarray
     G: np.ndarray
     lookups: list                 # [(expert, hit)]
+    inserts: list = field(default_factory=list)   # [(layer, victim, expert, kind)]
     predicted: np.ndarray | None = None
     prefetch_set: np.ndarray | None = None
     candidates: list = field(default_factory=list)
@@ -104,11 +114,13 @@ def run(steps, gates, cfg: DriverConfig, L: int, N: int, k: int):
     non_moe = cfg.non_moe_override if cfg.non_moe_override is not None \
         else tb.non_moe_layer_time
     prefetch_on = cfg.prefetch_size > 0
+    rng = np.random.default_rng(cfg.seed) if cfg.prefetch_kind == "random" else None
     caches = None
     if cfg.cache_capacity > 0:
         u = cfg.u_size if cfg.u_size is not None \
             else P.default_u_size(N, cfg.cache_capacity)
-        caches = [P.new_cache(l, N, cfg.cache_capacity, cfg.w_size, u, cfg.seed)
+        caches = [P.new_cache(l, N, cfg.cache_capacity, cfg.w_size, u, cfg.seed,
+                              policy=cfg.cache_policy)
                   for l in range(L)]
         if cfg.initial_on_gpu is not None:
             for l in range(L):
@@ -156,6 +168,18 @@ def run(steps, gates, cfg: DriverConfig, L: int, N: int, k: int):
                 C, G = P.all_cpu(w)
                 order = P.visit_order(w, cpu_t, gpu_t)
                 nodes = 0
+            elif cfg.assignment_policy == "beam":
+                C, G = P.beam(w, resident, cpu_t, gpu_t, cfg.gpu_capacity, cfg.beam_width)
+                order = P.visit_order(w, cpu_t, gpu_t)
+                nodes = int((w > 0).sum()) * cfg.beam_width
+            elif cfg.assignment_policy == "optimal":
+                C, G, nodes = P.optimal(w, resident, cpu_t, gpu_t, cfg.gpu_capacity,
+                                        cfg.exact_solver_limit)
+                order = P.visit_order(w, cpu_t, gpu_t)
+            elif cfg.assignment_policy == "static-threshold":
+                C, G = P.static_threshold(w, resident, cfg.gpu_capacity, cfg.threshold)
+                order = P.visit_order(w, cpu_t, gpu_t)
+                nodes = 0
             else:
                 raise ValueError(cfg.assignment_policy)
             cpu_busy, gpu_mk, demand = layer_schedule(w, resident, C, G, order, tb, cpu_t)
@@ -167,16 +191,31 @@ def run(steps, gates, cfg: DriverConfig, L: int, N: int, k: int):
 
             if caches is not None:
                 for e in np.flatnonzero(G):
-                    hit = bool(caches[l].on_gpu[e])
+                    hit, victim = P.lookup(caches[l], int(e))
                     rec.lookups.append((int(e), hit))
                     lookups_all.append((l, st.token_index, hit))
+                    if victim is not None:
+                        rec.inserts.append((l, victim, int(e), "lru"))
+                    if (not hit and cfg.insert_demand_fetched and cfg.cache_policy != "lru"
+                            and not resident[e]):
+                        v = P.force_insert(caches[l], int(e))
+                        if v is not None:
+                            rec.inserts.append((l, v, int(e), "demand"))
 
             demand_end = demand[-1][1] if demand else 0.0
             rec.demand_end = demand_end
             if prefetch_on and l < L - 1:
-                res = cfg.residuals[l] if cfg.residuals is not None else None
-                predicted, pset = P.predict_next(st.hidden[l], res, gates[l + 1],
-                                                 k, cfg.prefetch_size)
+                if cfg.prefetch_kind in ("residual", "feature"):
+                    res = (cfg.residuals[l] if cfg.residuals is not None
+                           and cfg.prefetch_kind == "residual" else None)
+                    predicted, pset = P.predict_next(st.hidden[l], res, gates[l + 1],
+                                                     k, cfg.prefetch_size)
+                else:
+                    predicted = (np.asarray(cfg.frequency_table[l + 1], np.int64).copy()
+                                 if cfg.prefetch_kind == "statistical"
+                                 else rng.permutation(N).astype(np.int64))
+                    pset = P.stable_topk(predicted.astype(np.float64),
+                                         min(cfg.prefetch_size, N))
                 rec.predicted, rec.prefetch_set = predicted, pset
                 true_next = st.workloads[l + 1]
                 acc1.setdefault(l + 1, []).append(P.accuracy(pset, true_next, 1))
@@ -195,10 +234,18 @@ def run(steps, gates, cfg: DriverConfig, L: int, N: int, k: int):
                 pcie_prefetch[l] += consumed
                 arrivals[l + 1] = np.asarray(done, dtype=np.int64)
                 rec.candidates, rec.completed = cands, list(done)
+                if caches is not None and cfg.insert_prefetched:
+                    for e in done:
+                        v = P.force_insert(caches[l + 1], int(e))
+                        if v is not None:
+                            rec.inserts.append((l + 1, v, int(e), "prefetch"))
 
             boundary = 0.0
             if caches is not None:
-                ev = P.window_update(caches[l], w, st.eos)
+                gss = None
+                if cfg.cache_policy == "score":
+                    gss = P.gate_probs(st.hidden[l], gates[l]).sum(axis=0)
+                ev = P.window_update(caches[l], w, st.eos, gss)
                 if ev is not None:
                     evicted, admitted = ev
                     boundary = len(admitted) * tb.trans_time

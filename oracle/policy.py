@@ -221,6 +221,137 @@ def all_cpu(workloads):
 
 
 # ---------------------------------------------------------------------------
+# Baseline solvers (reference assignment.py:154-402)
+# ---------------------------------------------------------------------------
+
+
+def makespan(cpu_t, gpu_t, C, G):
+    """(T_cpu, T_gpu, max) with numpy dot products (assignment.py:154-169)."""
+    tc = float(cpu_t @ C)
+    tg = float(gpu_t @ G)
+    return tc, tg, max(tc, tg)
+
+
+def beam(workloads, resident, cpu_t, gpu_t, capacity, beam_width: int):
+    """Beam search over the greedy visit order (assignment.py:202-247).
+
+    States (t_cpu, t_gpu, used, gpu tuple, cpu tuple); each expands to its
+    greedy-preferred child first, children are stably sorted by makespan and
+    the first ``beam_width`` survive; the greedy schedule wins if strictly
+    better.  Returns (C, G)."""
+    order = visit_order(workloads, cpu_t, gpu_t)
+    states = [(0.0, 0.0, 0, (), ())]
+    for idx in order:
+        g, c = float(gpu_t[idx]), float(cpu_t[idx])
+        needs = not bool(resident[idx])
+        kids = []
+        for (tc, tg, used, gs, cs) in states:
+            gk = None
+            if capacity is None or not needs or used < capacity:
+                gk = (tc, tg + g, used + (1 if needs else 0), gs + (int(idx),), cs)
+            ck = (tc + c, tg, used, gs, cs + (int(idx),))
+            if gk is not None and tg + g <= tc + c:
+                kids += [gk, ck]
+            elif gk is not None:
+                kids += [ck, gk]
+            else:
+                kids.append(ck)
+        kids.sort(key=lambda st: max(st[0], st[1]))
+        states = kids[:beam_width]
+    best = states[0]
+    gC, gG, _ = greedy(workloads, resident, cpu_t, gpu_t, capacity)
+    if makespan(cpu_t, gpu_t, gC, gG)[2] < max(best[0], best[1]):
+        return gC, gG
+    n = len(workloads)
+    C = np.zeros(n, np.int8)
+    G = np.zeros(n, np.int8)
+    G[list(best[3])] = 1
+    C[list(best[4])] = 1
+    return C, G
+
+
+def optimal(workloads, resident, cpu_t, gpu_t, capacity, limit: int = 24):
+    """Branch and bound for the minimum makespan (assignment.py:268-346):
+    lower bound max(Tc, Tg, (Tc+Tg+rem)/2), locally better device first,
+    ties toward fewer GPU experts then the smallest sorted GPU index tuple.
+    Returns (C, G, nodes); raises ValueError above ``limit`` activated."""
+    order = visit_order(workloads, cpu_t, gpu_t)
+    n_act = len(order)
+    if n_act > limit:
+        raise ValueError(f"exact solver limited to {limit} activated experts, "
+                         f"instance has {n_act}")
+    ct, gt = cpu_t[order], gpu_t[order]
+    needs = (~np.asarray(resident, bool)[order]).astype(np.int64)
+    rem = np.concatenate([np.cumsum(np.minimum(ct, gt)[::-1])[::-1], [0.0]])
+    gC, gG, _ = greedy(workloads, resident, cpu_t, gpu_t, capacity)
+    best = [makespan(cpu_t, gpu_t, gC, gG)[2], int(gG.sum()),
+            tuple(np.flatnonzero(gG).tolist())]
+    best_choice = [None]
+    nodes = [0]
+    choice = np.zeros(n_act, np.int8)
+
+    def dfs(depth, tc, tg, used, ng):
+        nodes[0] += 1
+        lb = max(tc, tg, (tc + tg + rem[depth]) / 2.0)
+        if lb > best[0]:
+            return
+        if lb == best[0] and ng > best[1]:
+            return
+        if depth == n_act:
+            gidx = tuple(sorted(int(order[i]) for i in range(n_act) if choice[i]))
+            key = [max(tc, tg), len(gidx), gidx]
+            if key < best:
+                best[:] = key
+                best_choice[0] = choice.copy()
+            return
+        ok = capacity is None or used + needs[depth] <= capacity
+        first_gpu = tg + gt[depth] <= tc + ct[depth]
+        for dev in ((1, 0) if first_gpu else (0, 1)):
+            if dev == 1:
+                if not ok:
+                    continue
+                choice[depth] = 1
+                dfs(depth + 1, tc, tg + gt[depth], used + needs[depth], ng + 1)
+            else:
+                choice[depth] = 0
+                dfs(depth + 1, tc + ct[depth], tg, used, ng)
+        choice[depth] = 0
+
+    dfs(0, 0.0, 0.0, 0, 0)
+    if best_choice[0] is None:
+        return gC, gG, nodes[0]
+    n = len(workloads)
+    C = np.zeros(n, np.int8)
+    G = np.zeros(n, np.int8)
+    for i, dv in enumerate(best_choice[0]):
+        (G if dv else C)[order[i]] = 1
+    return C, G, nodes[0]
+
+
+def static_threshold(workloads, resident, capacity, threshold=None):
+    """GPU iff w >= threshold (default: median positive workload), capacity
+    overflow to the CPU in descending-workload order (assignment.py:349-377)."""
+    w = np.asarray(workloads)
+    n = len(w)
+    C = np.zeros(n, np.int8)
+    G = np.zeros(n, np.int8)
+    act = np.flatnonzero(w > 0)
+    if len(act) == 0:
+        return C, G
+    if threshold is None:
+        threshold = float(np.median(w[act]))
+    slots = capacity
+    for e in act[np.argsort(-w[act], kind="stable")]:
+        if w[e] >= threshold and (slots is None or slots > 0 or bool(resident[e])):
+            G[e] = 1
+            if slots is not None and not resident[e]:
+                slots -= 1
+        else:
+            C[e] = 1
+    return C, G
+
+
+# ---------------------------------------------------------------------------
 # Residual prefetch (reference prefetch.py:88-168)
 # ---------------------------------------------------------------------------
 
@@ -253,6 +384,16 @@ def predict_next(hidden_l, residual_l, gate_next, k: int, prefetch_size: int):
     return predicted, pset
 
 
+def frequency_table(step_workloads) -> np.ndarray:
+    """Per-layer summed workloads over calibration steps, (L, N) int64
+    (activation_frequency_table, prefetch.py:76-85)."""
+    table = None
+    for w in step_workloads:
+        w = np.asarray(w, dtype=np.int64)
+        table = w.copy() if table is None else table + w
+    return table
+
+
 def accuracy(pset, true_workloads, k: int) -> float:
     """|set[:k] & topk(true, k)| / k (prefetch.py:159-168)."""
     truth = stable_topk(np.asarray(true_workloads, dtype=np.float64), k)
@@ -274,10 +415,49 @@ class LayerCache:
     scores: np.ndarray = None
     window: int = 0
     stopped: bool = False
+    policy: str = "workload"          # "workload" | "lru" | "score"
+    lru_clock: np.ndarray = None
+    clock: int = 0
 
     def __post_init__(self):
         if self.scores is None:
             self.scores = np.zeros(len(self.on_gpu), np.float64)
+        if self.lru_clock is None:
+            self.lru_clock = np.zeros(len(self.on_gpu), np.int64)
+
+
+def lookup(c: LayerCache, e: int) -> tuple[bool, int | None]:
+    """Hit iff cached; LRU refreshes on a hit and inserts on a miss, evicting
+    the least recently used (first minimum in index order) (cache.py:104-125).
+    Returns (hit, LRU victim or None)."""
+    hit = bool(c.on_gpu[e])
+    victim = None
+    if c.policy == "lru":
+        c.clock += 1
+        if hit:
+            c.lru_clock[e] = c.clock
+        else:
+            cached = np.flatnonzero(c.on_gpu)
+            victim = int(cached[np.argmin(c.lru_clock[cached])])
+            c.on_gpu[victim] = False
+            c.on_gpu[e] = True
+            c.lru_clock[e] = c.clock
+    return hit, victim
+
+
+def force_insert(c: LayerCache, e: int) -> int | None:
+    """Insert outside the window (demand / prefetch toggles, cache.py:128-143):
+    evict the lowest-score cached expert (LRU: least recently used)."""
+    if c.on_gpu[e]:
+        return None
+    cached = np.flatnonzero(c.on_gpu)
+    if c.policy == "lru":
+        victim = int(cached[np.argmin(c.lru_clock[cached])])
+    else:
+        victim = int(cached[np.argsort(c.scores[cached], kind="stable")[0]])
+    c.on_gpu[victim] = False
+    c.on_gpu[e] = True
+    return victim
 
 
 def initial_residents(layer: int, num_experts: int, capacity: int, seed: int):
@@ -288,25 +468,30 @@ def initial_residents(layer: int, num_experts: int, capacity: int, seed: int):
     return mask
 
 
-def new_cache(layer, num_experts, capacity, w_size, u_size, seed=0) -> LayerCache:
+def new_cache(layer, num_experts, capacity, w_size, u_size, seed=0,
+              policy: str = "workload") -> LayerCache:
     return LayerCache(initial_residents(layer, num_experts, capacity, seed),
-                      int(w_size), int(u_size))
+                      int(w_size), int(u_size), policy=policy)
 
 
-def window_update(c: LayerCache, workload, is_eos: bool):
-    """Workload policy: accumulate, and at the window boundary swap up to u
-    pairs while the incoming score >= outgoing (cache.py:146-214).
+def window_update(c: LayerCache, workload, is_eos: bool, gate_score_sums=None):
+    """Workload (score) policy: accumulate workloads (summed gate scores),
+    and at the window boundary swap up to u pairs while the incoming score
+    >= outgoing; LRU only honours EOS (cache.py:146-214).
 
     Returns None (no window boundary) or (evicted list, admitted list).
     """
     if c.stopped:
         return None
-    c.scores = c.scores + np.asarray(workload, dtype=np.float64)
-    c.window += 1
+    if c.policy in ("workload", "score"):
+        vec = (np.asarray(workload, dtype=np.float64) if c.policy == "workload"
+               else np.asarray(gate_score_sums, dtype=np.float64))
+        c.scores = c.scores + vec
+        c.window += 1
     if is_eos:
         c.stopped = True
         return None
-    if c.window < c.w_size:
+    if c.policy == "lru" or c.window < c.w_size:
         return None
     off = np.flatnonzero(~c.on_gpu)
     on = np.flatnonzero(c.on_gpu)

@@ -35,7 +35,7 @@ from moesim.trace import (ModelConfig, ResidualVectors, derive_workloads,  # noq
                           generate_synthetic_trace, topk_indices)
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from make_golden_cfgs import run_cfgs  # noqa: E402
+from make_golden_cfgs import baseline_cfgs, run_cfgs  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -70,7 +70,7 @@ TRACES = [
 def main():
     arrays = {}
     meta = {"moesim_version": moesim.__version__, "numpy": np.__version__,
-            "traces": {}, "runs": {}, "greedy": {}, "cache": {}}
+            "traces": {}, "runs": {}, "runs_baseline": {}, "greedy": {}, "cache": {}}
 
     # --- gating hand cases (test_trace.py:37-72) --------------------------
     gate = np.array([[3.0, 1.0, 2.0, 0.0], [0.0, 2.0, 1.0, 3.0], [2.0, 3.0, 0.0, 1.0]])
@@ -181,6 +181,21 @@ def main():
             rep.pop("spec")
             rep.pop("timelines")
             meta["runs"][f"{name}/{rn}"] = rep
+        for rn, over in baseline_cfgs(N):
+            cm_run = default_cost_model(non_moe_layer_time=3.0 if "nm3" in rn else 0.0)
+            sc = dict(cost_model=cm_run)
+            sc.update(over)
+            if sc.get("prefetch_kind") == "residual":
+                sc["residuals"] = res
+            if sc.get("prefetch_kind") == "statistical":
+                sc["frequency_table"] = mp.activation_frequency_table(tr)
+            try:
+                rep = simulate_run(tr, SimConfig(**sc)).to_dict()
+                rep.pop("spec")
+                rep.pop("timelines")
+            except moesim.errors.MoesimError as exc:
+                rep = {"error": type(exc).__name__, "message": str(exc)}
+            meta["runs_baseline"][f"{name}/{rn}"] = rep
 
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as f:

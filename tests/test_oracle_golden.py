@@ -106,7 +106,11 @@ def _driver_cfg(name, over, N):
          "non_moe_override": "non_moe_override",
          "scheduling_overhead_ms": "scheduling_overhead_ms",
          "solver_node_cost_ms": "solver_node_cost_ms",
-         "prefetch_compute_ms": "prefetch_compute_ms"}
+         "prefetch_compute_ms": "prefetch_compute_ms", "beam_width": "beam_width",
+         "threshold": "threshold", "exact_solver_limit": "exact_solver_limit",
+         "prefetch_kind": "prefetch_kind", "cache_policy": "cache_policy",
+         "insert_demand_fetched": "insert_demand_fetched",
+         "insert_prefetched": "insert_prefetched"}
     for key, val in over.items():
         if key in m:
             kw[m[key]] = val
@@ -128,5 +132,35 @@ def test_driver_reports_match_reference(golden, traces):
             cfg.residuals = P.calibrate([s.hidden for s in tr.steps])
         steps = [D.StepInput(s.token_index, s.tokens, s.workloads, s.hidden, s.eos)
                  for s in tr.steps]
+        rep, _ = D.run(steps, tr.gates, cfg, info["L"], info["N"], info["k"])
+        assert rep == want, key
+
+
+def test_driver_baseline_reports_match_reference(golden, traces):
+    """Alternative policies: beam / optimal / static
+    solvers, LRU and score caches, insert toggles, feature / statistical /
+    random predictors -- whole reports equal the reference's, and the exact
+    solver refuses the same instances."""
+    import sys
+    sys.path.insert(0, __file__.rsplit("/", 1)[0] + "/golden")
+    from make_golden_cfgs import baseline_cfgs  # noqa
+    _, meta = golden
+    assert len(meta["runs_baseline"]) >= 80
+    for key, want in meta["runs_baseline"].items():
+        tname, rname = key.split("/")
+        tr = traces[tname]
+        info = meta["traces"][tname]
+        over = dict(baseline_cfgs(info["N"]))[rname]
+        cfg = _driver_cfg(rname, over, info["N"])
+        if over.get("prefetch_kind") == "residual":
+            cfg.residuals = P.calibrate([s.hidden for s in tr.steps])
+        if over.get("prefetch_kind") == "statistical":
+            cfg.frequency_table = P.frequency_table([s.workloads for s in tr.steps])
+        steps = [D.StepInput(s.token_index, s.tokens, s.workloads, s.hidden, s.eos)
+                 for s in tr.steps]
+        if "error" in want:
+            with pytest.raises(ValueError, match="exact solver limited"):
+                D.run(steps, tr.gates, cfg, info["L"], info["N"], info["k"])
+            continue
         rep, _ = D.run(steps, tr.gates, cfg, info["L"], info["N"], info["k"])
         assert rep == want, key
