@@ -57,7 +57,7 @@ typedef struct dali_layer_record {
   int32_t step, layer, token_index, n_act;
   int32_t n_gpu, n_cpu, n_demand, n_pset;
   int32_t n_cand, n_done, ev_valid, ev_n;
-  int32_t nodes, stopped, pad0, pad1;
+  int32_t nodes, stopped, n_ins, err; /* err 1: exact solver refused   */
   double cpu_busy;      /* cpu_times @ C                                  */
   double gpu_makespan;  /* engine_t of the GPU-lane pipeline              */
   double latency;       /* layer_latency                                  */
@@ -76,25 +76,42 @@ typedef struct dali_layer_record {
   int16_t evicted[DALI_MAX_EXPERTS];
   int16_t admitted[DALI_MAX_EXPERTS];
   int32_t workload[DALI_MAX_EXPERTS]; /* realised workloads of this layer  */
+  /* cache insertions outside the window (baseline policies): LRU miss
+   * inserts and demand toggles act on this layer, prefetch toggles on
+   * layer+1; ins_kind 0 = lru, 1 = demand, 2 = prefetch */
+  int16_t ins_victim[DALI_MAX_EXPERTS];
+  int16_t ins_expert[DALI_MAX_EXPERTS];
+  int8_t ins_kind[DALI_MAX_EXPERTS];
 } dali_layer_record;
 
 /* Scalar knobs of the fused per-layer policy step (SimConfig,
- * simulator.py:45-74, restricted to the hot-path policies). */
+ * simulator.py:45-74). */
 typedef struct dali_policy_config {
   int32_t L, N, k;
-  int32_t assignment;        /* 0 = greedy, 1 = all-cpu, 2 = all-gpu        */
+  int32_t assignment;        /* 0 = greedy, 1 = all-cpu, 2 = all-gpu,
+                              * 3 = beam, 4 = optimal (branch and bound),
+                              * 5 = static-threshold (assignment.py:202-402) */
   int32_t gpu_capacity;      /* < 0 = unlimited                             */
   int32_t prefetch_size;     /* 0 = prefetch off                            */
   int32_t cache_enabled;
   int32_t w_size, u_size;
   int32_t has_shared;        /* num_shared_experts > 0                      */
   int32_t all_resident;      /* every expert in HBM (roofline reference)     */
+  int32_t cache_policy;      /* 0 = workload, 1 = lru, 2 = score            */
+  int32_t insert_demand;     /* insert_demand_fetched toggle                */
+  int32_t insert_prefetched; /* insert_prefetched toggle                    */
+  int32_t beam_width;        /* 1..DALI_MAX_BEAM                            */
+  int32_t exact_solver_limit;
+  int32_t has_threshold;     /* static-threshold: 0 = median of positives   */
   int32_t pad;
   double scheduling_overhead_ms;
   double solver_node_cost_ms;
   double prefetch_compute_ms;
   double non_moe;            /* resolved non_moe_override / table value     */
+  double threshold;
 } dali_policy_config;
+
+#define DALI_MAX_BEAM 32
 
 /* ---- library ----------------------------------------------------------- */
 const char* dali_last_error(void);
@@ -147,6 +164,15 @@ int dali_route_bf16(const uint16_t* hidden, const double* residual,
 int dali_prefetch_select(const int64_t* predicted, int32_t N, int32_t P,
                          int32_t* set, void* stream);
 
+/* Per-token gate scores softmax(hidden @ W_g) in fp64 (gate_scores,
+ * trace.py:242-250) -> probs [dev] (T, N) f64; the score cache policy sums
+ * them over tokens (simulator.py:426-429).  Same arithmetic as dali_route. */
+int dali_gate_probs_f64(const double* hidden, const double* gate, int64_t T,
+                        int32_t d, int32_t N, double* probs, void* stream);
+int dali_gate_probs_bf16(const uint16_t* hidden, const uint16_t* gate,
+                         int64_t T, int32_t d, int32_t N, double* probs,
+                         void* stream);
+
 /* ---- (2) greedy assignment (single CTA) ----------------------------------
  * Replaces AssignmentInstance times + sorted_order + greedy_assign
  * (assignment.py:53-123,172-199; cost_model.py:19-27,70-103).
@@ -180,6 +206,28 @@ int dali_cache_record(uint8_t* on_gpu, double* scores, int32_t* counters,
                       const double* workload, int32_t is_eos, int32_t* ev,
                       void* stream);
 
+/* One assignment instance with any reference solver (assignment.py:172-402):
+ *   policy 0 greedy, 1 all-cpu, 2 all-gpu, 3 beam (beam_width <= DALI_MAX_BEAM),
+ *   4 optimal (branch and bound; *nodes = explored nodes, -1 when more than
+ *   exact_solver_limit experts are activated -- the caller raises), 5
+ *   static-threshold (has_threshold = 0: median positive workload).
+ *   Times from the cost model or explicit [dev] vectors as in dali_greedy;
+ *   C, G [dev] (N,) int8; nodes [dev] int64 (may be NULL). */
+int dali_assign(int32_t policy, const int64_t* workloads, const uint8_t* resident,
+                int32_t N, int32_t gpu_capacity, const dali_cost_model* cm,
+                const double* cpu_times, const double* gpu_times, int32_t beam_width,
+                int32_t exact_solver_limit, int32_t has_threshold, double threshold,
+                int8_t* C, int8_t* G, int64_t* nodes, void* stream);
+
+/* One cache operation on a layer's state (cache.py:104-143): op 0 = lookup
+ * (LRU: clock tick, refresh on hit, insert + evict least recently used on a
+ * miss), op 1 = force_insert (evict the lowest score / oldest clock).
+ *   on_gpu [dev] (N,) u8, scores [dev] (N,) f64, lru_state [dev] (N+1) i64
+ *   (clock last; may be NULL unless use_lru); out [dev] int32[2] =
+ *   {hit | inserted, victim or -1}. */
+int dali_cache_op(uint8_t* on_gpu, const double* scores, int64_t* lru_state, int32_t N,
+                  int32_t use_lru, int32_t expert, int32_t op, int32_t* out, void* stream);
+
 /* ---- fused per-layer policy step -----------------------------------------
  * One single-CTA kernel per (step, layer) that performs, in the reference
  * driver's order (simulator.py:359-444): residency = cache | arrived,
@@ -197,13 +245,21 @@ int dali_cache_record(uint8_t* on_gpu, double* scores, int32_t* counters,
  *             current step; row layer+1 is written, row layer is consumed
  *   slot_of   [dev] (L, N) int32 HBM slot per cached expert or -1; swaps
  *             move the victim's slot to the admitted expert (may be NULL)
+ *   lru_state [dev] (L, N+1) int64 LRU clocks (+ the layer's clock last);
+ *             used by cache_policy 1 (may be NULL otherwise)
+ *   gate_probs [dev] (n_tokens, N) f64 this layer's gate scores
+ *             (dali_gate_probs); used by cache_policy 2 (may be NULL)
+ * predicted also carries the statistical / random predictors' vectors
+ * (frequency-table row, permutation): the kernel only ranks it.
  */
 int dali_policy_layer(const dali_policy_config* cfg, const dali_cost_model* cm,
                       int32_t step, int32_t layer, int32_t token_index,
                       int32_t is_eos, const int64_t* workloads,
                       const int64_t* predicted, uint8_t* on_gpu,
                       double* scores, int32_t* counters, uint8_t* arrived,
-                      int32_t* slot_of, dali_layer_record* rec, void* stream);
+                      int32_t* slot_of, int64_t* lru_state,
+                      const double* gate_probs, int32_t n_tokens,
+                      dali_layer_record* rec, void* stream);
 
 /* Same step with the per-step scalars read from a DEVICE descriptor so the
  * launch can live inside a CUDA graph replayed every decode step:
@@ -218,8 +274,9 @@ int dali_policy_layer_desc(const dali_policy_config* cfg,
                            const int32_t* desc, const int64_t* workloads,
                            const int64_t* predicted, uint8_t* on_gpu,
                            double* scores, int32_t* counters, uint8_t* arrived,
-                           int32_t* slot_of, dali_layer_record* rec_base,
-                           void* stream);
+                           int32_t* slot_of, int64_t* lru_state,
+                           const double* gate_probs, int32_t n_tokens,
+                           dali_layer_record* rec_base, void* stream);
 int dali_step_advance(int32_t* desc, void* stream);
 
 /* ---- (5) expert execution -------------------------------------------------

@@ -33,9 +33,13 @@ class PolicyConfigC(C.Structure):
                 ("assignment", C.c_int32), ("gpu_capacity", C.c_int32),
                 ("prefetch_size", C.c_int32), ("cache_enabled", C.c_int32),
                 ("w_size", C.c_int32), ("u_size", C.c_int32), ("has_shared", C.c_int32),
-                ("all_resident", C.c_int32), ("pad", C.c_int32),
+                ("all_resident", C.c_int32), ("cache_policy", C.c_int32),
+                ("insert_demand", C.c_int32), ("insert_prefetched", C.c_int32),
+                ("beam_width", C.c_int32), ("exact_solver_limit", C.c_int32),
+                ("has_threshold", C.c_int32), ("pad", C.c_int32),
                 ("scheduling_overhead_ms", C.c_double), ("solver_node_cost_ms", C.c_double),
-                ("prefetch_compute_ms", C.c_double), ("non_moe", C.c_double)]
+                ("prefetch_compute_ms", C.c_double), ("non_moe", C.c_double),
+                ("threshold", C.c_double)]
 
 
 class LayerRecordC(C.Structure):
@@ -43,8 +47,8 @@ class LayerRecordC(C.Structure):
                 ("n_act", C.c_int32), ("n_gpu", C.c_int32), ("n_cpu", C.c_int32),
                 ("n_demand", C.c_int32), ("n_pset", C.c_int32), ("n_cand", C.c_int32),
                 ("n_done", C.c_int32), ("ev_valid", C.c_int32), ("ev_n", C.c_int32),
-                ("nodes", C.c_int32), ("stopped", C.c_int32), ("pad0", C.c_int32),
-                ("pad1", C.c_int32),
+                ("nodes", C.c_int32), ("stopped", C.c_int32), ("n_ins", C.c_int32),
+                ("err", C.c_int32),
                 ("cpu_busy", C.c_double), ("gpu_makespan", C.c_double), ("latency", C.c_double),
                 ("demand_end", C.c_double), ("demand_ms", C.c_double), ("consumed", C.c_double),
                 ("boundary", C.c_double), ("pad2", C.c_double),
@@ -52,10 +56,13 @@ class LayerRecordC(C.Structure):
                 ("resident", C.c_uint8 * MAX_EXPERTS), ("hit", C.c_uint8 * MAX_EXPERTS),
                 ("order", C.c_int16 * MAX_EXPERTS), ("pset", C.c_int16 * MAX_EXPERTS),
                 ("cand", C.c_int16 * MAX_EXPERTS), ("evicted", C.c_int16 * MAX_EXPERTS),
-                ("admitted", C.c_int16 * MAX_EXPERTS), ("workload", C.c_int32 * MAX_EXPERTS)]
+                ("admitted", C.c_int16 * MAX_EXPERTS), ("workload", C.c_int32 * MAX_EXPERTS),
+                ("ins_victim", C.c_int16 * MAX_EXPERTS), ("ins_expert", C.c_int16 * MAX_EXPERTS),
+                ("ins_kind", C.c_int8 * MAX_EXPERTS)]
 
 
 RECORD_BYTES = C.sizeof(LayerRecordC)
+MAX_BEAM = 32
 
 _P = C.c_void_p
 _I32 = C.c_int32
@@ -72,7 +79,13 @@ SIGNATURES = {
     "dali_greedy": [_P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
     "dali_cost_eval": [_P, _P, _I64, _P, _P, _P],
     "dali_cache_record": [_P, _P, _P, _I32, _I32, _I32, _P, _I32, _P, _P],
-    "dali_policy_layer": [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "dali_policy_layer": [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                          _I32, _P, _P],
+    "dali_gate_probs_f64": [_P, _P, _I64, _I32, _I32, _P, _P],
+    "dali_assign": [_I32, _P, _P, _I32, _I32, _P, _P, _P, _I32, _I32, _I32, C.c_double, _P, _P,
+                    _P, _P],
+    "dali_cache_op": [_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P],
+    "dali_gate_probs_bf16": [_P, _P, _I64, _I32, _I32, _P, _P],
     "dali_moe_plan": [_P, _I64, _I32, _I32, _P, _P, _P, _P],
     "dali_permute": [_P, _P, _I64, _I32, _P, _P],
     "dali_expert_ffn": [_P, _P, _I32, _P, _I32, _I32, _I64, _I32, _P, _P, _P],
@@ -84,7 +97,8 @@ SIGNATURES = {
     "dali_init_uniform_bf16": [_P, _I64, C.c_uint64, C.c_uint64, C.c_float, _P],
     "dali_host_alloc": [C.c_size_t, _I32, C.POINTER(C.c_void_p)],
     "dali_host_free": [_P, C.c_size_t],
-    "dali_policy_layer_desc": [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "dali_policy_layer_desc": [_P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P,
+                               _P],
     "dali_step_advance": [_P, _P],
     "dali_rope_append": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P],
     "dali_decode_attention": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, C.c_float, _P,

@@ -2,9 +2,11 @@
 
 ``greedy_assign`` runs the single-CTA greedy kernel (``dali_greedy``):
 cost evaluation, the stable |t_gpu - t_cpu| ordering and Algorithm 1 all
-happen on device.  ``validate`` / ``makespan`` are host-side constraint
-checks (assignment.py:126-169); ``all_cpu_assign`` / ``all_gpu_assign`` are
-the trivial baselines the breakdown needs.
+happen on device.  The reference's comparison solvers -- beam search,
+branch-and-bound ``optimal_assign`` and the static threshold -- run in the
+same single-CTA kernel family (``dali_assign``).  ``validate`` /
+``makespan`` are host-side constraint checks (assignment.py:126-169);
+``all_cpu_assign`` / ``all_gpu_assign`` are the trivial baselines.
 """
 
 from __future__ import annotations
@@ -18,6 +20,8 @@ import torch
 from . import _dev, _lib
 from .cost_model import CostModel
 from .errors import AssignmentError, ConstraintViolation
+
+EXACT_SOLVER_LIMIT = 24          # assignment.py:23
 
 
 @dataclass
@@ -214,4 +218,82 @@ def all_gpu_assign(instance: AssignmentInstance) -> Assignment:
                 slots -= 1
         else:
             C_[idx] = 1
+    return Assignment(C=C_, G=G_)
+
+
+def _run_policy(inst: AssignmentInstance, policy: int, beam_width: int = 2,
+                limit: int = EXACT_SOLVER_LIMIT, threshold: float | None = None):
+    """Launch ``dali_assign`` for one instance -> (C, G, nodes)."""
+    n = inst.n_experts
+    if n > _lib.MAX_EXPERTS:
+        raise AssignmentError(f"at most {_lib.MAX_EXPERTS} experts supported, got {n}")
+    if n == 0:
+        z = np.zeros(0, np.int8)
+        return z, z, 0
+    w = _dev.to_dev(inst.workloads, torch.int64)
+    r = _dev.to_dev(inst.resident.astype(np.uint8), torch.uint8)
+    use_times = getattr(inst, "_cpu_times", None) is not None
+    ct = _dev.to_dev(inst._cpu_times, torch.float64) if use_times else None
+    gt = _dev.to_dev(inst._gpu_times, torch.float64) if use_times else None
+    Cd = _dev.empty((n,), torch.int8)
+    Gd = _dev.empty((n,), torch.int8)
+    nd = _dev.zeros((1,), torch.int64)
+    cm = inst.cost_model.to_c() if inst.cost_model is not None else None
+    cap = -1 if inst.gpu_capacity is None else int(inst.gpu_capacity)
+    _lib.call("dali_assign", policy, w.data_ptr(), r.data_ptr(), n, cap,
+              C.addressof(cm) if cm is not None else None, _dev.ptr(ct), _dev.ptr(gt),
+              int(beam_width), int(limit), int(threshold is not None),
+              float(threshold) if threshold is not None else 0.0, Cd.data_ptr(), Gd.data_ptr(),
+              nd.data_ptr(), _dev.stream_ptr())
+    return Cd.cpu().numpy(), Gd.cpu().numpy(), int(nd.cpu().item())
+
+
+def beam_assign(instance: AssignmentInstance, beam_width: int = 2) -> Assignment:
+    """Beam search over the greedy order, greedy kept as fallback
+    (assignment.py:202-247), on device."""
+    if beam_width < 1:
+        raise AssignmentError(f"beam_width must be >= 1, got {beam_width}")
+    if beam_width > _lib.MAX_BEAM:
+        raise AssignmentError(f"beam_width must be <= {_lib.MAX_BEAM} on the device solver, "
+                              f"got {beam_width}")
+    C_, G_, _ = _run_policy(instance, 3, beam_width=beam_width)
+    return Assignment(C=C_, G=G_)
+
+
+def optimal_assign_with_stats(instance: AssignmentInstance,
+                              max_activated: int = EXACT_SOLVER_LIMIT):
+    """Exact minimum-makespan placement by branch and bound with the
+    reference's bound, branch order and tie-break (assignment.py:268-346),
+    on device.  Returns (assignment, makespan, explored nodes)."""
+    n_act = len(instance.activated)
+    if n_act > max_activated:
+        raise AssignmentError(
+            f"exact solver limited to {max_activated} activated experts, instance has "
+            f"{n_act}; use greedy_assign instead")
+    C_, G_, nodes = _run_policy(instance, 4, limit=max_activated)
+    a = Assignment(C=C_, G=G_)
+    if a == greedy_assign(instance):
+        mk = makespan(instance, a)[2]
+    else:                       # incumbent's lane totals accumulate in visit order
+        order = instance.sorted_order()
+        tc = tg = 0.0
+        for e in order:
+            if a.G[e]:
+                tg += float(instance.gpu_times[e])
+            else:
+                tc += float(instance.cpu_times[e])
+        mk = max(tc, tg)
+    return a, float(mk), nodes
+
+
+def optimal_assign(instance: AssignmentInstance, max_activated: int = EXACT_SOLVER_LIMIT):
+    a, mk, _ = optimal_assign_with_stats(instance, max_activated)
+    return a, mk
+
+
+def static_threshold_assign(instance: AssignmentInstance,
+                            threshold: float | None = None) -> Assignment:
+    """GPU iff w >= threshold (default: median positive workload); capacity
+    overflow to the CPU in descending-workload order (assignment.py:349-377)."""
+    C_, G_, _ = _run_policy(instance, 5, threshold=threshold)
     return Assignment(C=C_, G=G_)

@@ -6,7 +6,10 @@ seed it; ``record_and_maybe_replace`` runs the window update on device
 (``dali_cache_record``: score accumulation, stable candidate/victim ranking,
 dominance-guarded swaps) and writes the state back.  The engine keeps the
 same state resident in HBM and updates it inside the fused policy kernel.
-LRU / score policies are baselines outside the B200 path.
+The LRU and score policies and the insert toggles (the reference's
+comparison baselines) use the same device state: ``lookup`` /
+``force_insert`` run ``dali_cache_op``, the score policy feeds the summed
+gate scores through the window kernel.
 """
 
 from __future__ import annotations
@@ -19,7 +22,7 @@ import torch
 from . import _dev, _lib
 from .errors import CacheError
 
-CACHE_POLICIES = ("workload",)
+CACHE_POLICIES = ("workload", "lru", "score")
 
 
 @dataclass
@@ -42,6 +45,8 @@ class CacheState:
     scores: np.ndarray = field(default=None)
     tokens_in_window: int = 0
     stopped: bool = False
+    lru_clock: np.ndarray = field(default=None)
+    clock: int = 0
     insert_demand_fetched: bool = False
     insert_prefetched: bool = False
 
@@ -67,8 +72,7 @@ def init_cache(layer: int, num_experts: int, capacity: int, w_size: int, u_size:
                policy: str = "workload", seed: int = 0, insert_demand_fetched: bool = False,
                insert_prefetched: bool = False) -> CacheState:
     if policy not in CACHE_POLICIES:
-        raise CacheError(f"unknown cache policy {policy!r}; choose from {CACHE_POLICIES} "
-                         f"(lru/score baselines are not on the B200 path)")
+        raise CacheError(f"unknown cache policy {policy!r}; choose from {CACHE_POLICIES}")
     if not (0 < capacity < num_experts):
         raise CacheError(f"capacity must satisfy 0 < capacity < num_experts, got "
                          f"capacity={capacity}, num_experts={num_experts}")
@@ -77,19 +81,52 @@ def init_cache(layer: int, num_experts: int, capacity: int, w_size: int, u_size:
     if not (0 <= u_size <= min(capacity, num_experts - capacity)):
         raise CacheError(f"u_size must be in [0, min(capacity, N - capacity)] = "
                          f"[0, {min(capacity, num_experts - capacity)}], got {u_size}")
-    if insert_demand_fetched or insert_prefetched:
-        raise CacheError("insert toggles are baselines outside the B200 path")
     return CacheState(layer=layer, num_experts=num_experts, capacity=capacity,
                       window_size=w_size, update_size=u_size, policy=policy,
                       on_gpu=initial_resident_set(layer, num_experts, capacity, seed),
-                      scores=np.zeros(num_experts, dtype=np.float64))
+                      scores=np.zeros(num_experts, dtype=np.float64),
+                      lru_clock=np.zeros(num_experts, dtype=np.int64),
+                      insert_demand_fetched=insert_demand_fetched,
+                      insert_prefetched=insert_prefetched)
+
+
+def _cache_op(state: CacheState, expert: int, op: int) -> tuple[int, int]:
+    N = state.num_experts
+    on = _dev.to_dev(state.on_gpu.astype(np.uint8), torch.uint8)
+    sc = _dev.to_dev(state.scores, torch.float64)
+    lru = _dev.to_dev(np.concatenate([state.lru_clock, [state.clock]]).astype(np.int64),
+                      torch.int64)
+    out = _dev.zeros((2,), torch.int32)
+    _lib.call("dali_cache_op", on.data_ptr(), sc.data_ptr(), lru.data_ptr(), N,
+              int(state.policy == "lru"), int(expert), op, out.data_ptr(), _dev.stream_ptr())
+    state.on_gpu = on.cpu().numpy().astype(bool)
+    lv = lru.cpu().numpy()
+    state.lru_clock, state.clock = lv[:N].copy(), int(lv[N])
+    o = out.cpu().numpy()
+    return int(o[0]), int(o[1])
 
 
 def lookup(state: CacheState, expert: int) -> bool:
-    """Hit iff cached; the workload policy does not mutate (cache.py:104-117)."""
+    """Hit iff cached (cache.py:104-117); under LRU the call also ticks the
+    clock, refreshes a hit and inserts a miss over the least recently used."""
     if not (0 <= expert < state.num_experts):
         raise CacheError(f"expert {expert} out of range [0, {state.num_experts})")
-    return bool(state.on_gpu[expert])
+    if state.policy != "lru":
+        return bool(state.on_gpu[expert])
+    hit, _ = _cache_op(state, expert, 0)
+    return bool(hit)
+
+
+def force_insert(state: CacheState, expert: int) -> int | None:
+    """Insert outside the windowed mechanism (demand / prefetch toggles,
+    cache.py:128-143): evicts the lowest-score (LRU: least recently used)
+    cached expert and returns it, or None if already cached."""
+    if not (0 <= expert < state.num_experts):
+        raise CacheError(f"expert {expert} out of range [0, {state.num_experts})")
+    if state.on_gpu[expert]:
+        return None
+    _, victim = _cache_op(state, expert, 1)
+    return victim
 
 
 def record_and_maybe_replace(state: CacheState, workload, token_index: int,
@@ -101,11 +138,22 @@ def record_and_maybe_replace(state: CacheState, workload, token_index: int,
     if workload.shape != (state.num_experts,):
         raise CacheError(f"workload vector length {workload.shape} != ({state.num_experts},)")
     N = state.num_experts
+    if state.policy == "score":
+        if gate_scores is None:
+            raise CacheError("score policy requires per-expert gate scores")
+        gate_scores = np.asarray(gate_scores, dtype=np.float64)
+        if gate_scores.shape != (N,):
+            raise CacheError(f"gate score vector length {gate_scores.shape} != ({N},)")
+    if state.policy == "lru":          # no windowing; EOS still stops it
+        if is_eos:
+            state.stopped = True
+        return None
+    vec = workload if state.policy == "workload" else gate_scores
     on = _dev.to_dev(state.on_gpu.astype(np.uint8), torch.uint8)
     sc = _dev.to_dev(state.scores, torch.float64)
     ctr = _dev.to_dev(np.array([state.tokens_in_window, int(state.stopped)], np.int32),
                       torch.int32)
-    wl = _dev.to_dev(workload.astype(np.float64), torch.float64)
+    wl = _dev.to_dev(np.asarray(vec, dtype=np.float64), torch.float64)
     ev = _dev.zeros((2 + 2 * _lib.MAX_EXPERTS,), torch.int32)
     _lib.call("dali_cache_record", on.data_ptr(), sc.data_ptr(), ctr.data_ptr(), N,
               state.window_size, state.update_size, wl.data_ptr(), int(bool(is_eos)),

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(kRouteThreads)
 route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
              const TW* __restrict__ gate, int64_t T, int d, int N, int k,
              int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
-             unsigned long long* __restrict__ workloads) {
+             unsigned long long* __restrict__ workloads, double* __restrict__ probs) {
   constexpr int kRouteCH = route_ch<kRouteTB>();
   __shared__ double sh_red[kRouteTB * DALI_MAX_EXPERTS];   // logits, then probs
   __shared__ int sh_hist[DALI_MAX_EXPERTS];
@@ -106,6 +106,8 @@ route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
     for (int j = lane; j < N; j += 32) row[j] = row[j] / sum;
     __syncwarp();
     const int64_t t = t0 + warp;
+    if (probs)
+      for (int j = lane; j < N; j += 32) probs[t * N + j] = row[j];
     for (int j = lane; j < N; j += 32) {
       const double pj = row[j];
       int rank = 0;
@@ -132,8 +134,9 @@ route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
     }
   }
   __syncthreads();
-  for (int i = tid; i < N; i += kRouteThreads)
-    if (sh_hist[i]) atomicAdd(workloads + i, (unsigned long long)sh_hist[i]);
+  if (workloads)
+    for (int i = tid; i < N; i += kRouteThreads)
+      if (sh_hist[i]) atomicAdd(workloads + i, (unsigned long long)sh_hist[i]);
 }
 
 __global__ void zero_i64(int64_t* p, int n) {
@@ -145,16 +148,19 @@ template <typename TH, typename TW>
 static int launch_route(const TH* hidden, const double* residual, const TW* gate,
                         int64_t T, int32_t d, int32_t N, int32_t k, int32_t renorm,
                         int32_t* topk_idx, float* topk_w, int64_t* workloads,
-                        void* stream) {
+                        void* stream, double* probs = nullptr) {
   DALI_REQUIRE(N >= 1 && N <= DALI_MAX_EXPERTS, DALI_ETRACE,
                "num experts %d outside [1, %d]", N, DALI_MAX_EXPERTS);
   DALI_REQUIRE(k >= 1 && k <= N, DALI_ETRACE, "top_k %d out of range for %d experts", k, N);
   DALI_REQUIRE(k <= DALI_MAX_TOPK, DALI_ETRACE, "top_k %d exceeds %d", k, DALI_MAX_TOPK);
   DALI_REQUIRE(d >= 1 && T >= 0, DALI_ETRACE, "bad shape T=%lld d=%d", (long long)T, d);
-  DALI_REQUIRE(workloads != nullptr, DALI_ETRACE, "workloads output required");
+  DALI_REQUIRE(workloads != nullptr || probs != nullptr, DALI_ETRACE,
+               "workloads output required");
   cudaStream_t st = as_stream(stream);
-  zero_i64<<<(N + 255) / 256, 256, 0, st>>>(workloads, N);
-  DALI_LAUNCH_CHECK("zero_i64");
+  if (workloads) {
+    zero_i64<<<(N + 255) / 256, 256, 0, st>>>(workloads, N);
+    DALI_LAUNCH_CHECK("zero_i64");
+  }
   if (T == 0) return DALI_OK;
   const int S = kRouteThreads / N;
   DALI_REQUIRE((T + 1) / 2 < (1ll << 31), DALI_ETRACE, "too many tokens");
@@ -173,15 +179,15 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
   if (T >= 8 * 148) {
     route_kernel<TH, TW, 8><<<(unsigned)((T + 7) / 8), kRouteThreads,
                               kRouteStageBytes + sizeof(double) * 8 * N * S, st>>>(
-        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
+        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   } else if (T >= 4 * 148) {
     route_kernel<TH, TW, 4><<<(unsigned)((T + 3) / 4), kRouteThreads,
                               kRouteStageBytes + sizeof(double) * 4 * N * S, st>>>(
-        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
+        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   } else {
     route_kernel<TH, TW, 2><<<(unsigned)((T + 1) / 2), kRouteThreads,
                               kRouteStageBytes + sizeof(double) * 2 * N * S, st>>>(
-        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul);
+        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   }
   DALI_LAUNCH_CHECK("route_kernel");
   return DALI_OK;
@@ -226,4 +232,18 @@ extern "C" int dali_prefetch_select(const int64_t* predicted, int32_t N, int32_t
   dali::prefetch_select_kernel<<<1, 256, 0, dali::as_stream(stream)>>>(predicted, N, P, set);
   DALI_LAUNCH_CHECK("prefetch_select_kernel");
   return DALI_OK;
+}
+
+extern "C" int dali_gate_probs_f64(const double* hidden, const double* gate, int64_t T, int32_t d,
+                                   int32_t N, double* probs, void* stream) {
+  DALI_REQUIRE(probs != nullptr, DALI_ETRACE, "probs output required");
+  return dali::launch_route<double, double>(hidden, nullptr, gate, T, d, N, 1, 0, nullptr,
+                                            nullptr, nullptr, stream, probs);
+}
+
+extern "C" int dali_gate_probs_bf16(const uint16_t* hidden, const uint16_t* gate, int64_t T,
+                                    int32_t d, int32_t N, double* probs, void* stream) {
+  DALI_REQUIRE(probs != nullptr, DALI_ETRACE, "probs output required");
+  return dali::launch_route<uint16_t, uint16_t>(hidden, nullptr, gate, T, d, N, 1, 0, nullptr,
+                                                nullptr, nullptr, stream, probs);
 }

@@ -518,19 +518,17 @@ class OffloadEngine:
         gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
         if use_desc:
             pol = self.policy
-            pred_p = None
-            if pol.prefetch_size > 0 and gate_next is not None:
-                route_device(h, gate_next, k, residual=pol.residuals[l], want_idx=False,
-                             want_weights=False, out=(None, None, pol.predicted))
-                pred_p = pol.predicted.data_ptr()
+            pred_p = pol.predicted_ptr(l, h, gate_next, rec_index=pol.n_records + l)
+            probs_p, n_tok = pol.gate_probs_ptr(h, self.w.router[l])
             _lib.call("dali_policy_layer_desc", C.addressof(pol.cfg), C.addressof(pol.cm_c), l,
                       self.desc_dev.data_ptr(), v["wl"].data_ptr(), pred_p,
                       pol.on_gpu.data_ptr(), pol.scores.data_ptr(), pol.counters.data_ptr(),
-                      pol.arrived.data_ptr(), pol.slot_of.data_ptr(), pol.record_ptr(0),
-                      cs.cuda_stream)
+                      pol.arrived.data_ptr(), pol.slot_of.data_ptr(), pol.lru_state.data_ptr(),
+                      probs_p, n_tok, pol.record_ptr(0), cs.cuda_stream)
             ri = None
         else:
-            ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], h, gate_next)
+            ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], h, gate_next,
+                                        gate_this=self.w.router[l])
         hv = self._host_view(v, T)
         xp_host = self._ws("xp_h", (R, d), torch.bfloat16, pinned=True)
         xp_host.copy_(v["xp"], non_blocking=True)
@@ -608,7 +606,8 @@ class OffloadEngine:
                       v["wl"].data_ptr(), None, self.policy.on_gpu.data_ptr(),
                       self.policy.scores.data_ptr(), self.policy.counters.data_ptr(),
                       self.policy.arrived.data_ptr(), self.policy.slot_of.data_ptr(),
-                      self.policy.record_ptr(0), cs.cuda_stream)
+                      self.policy.lru_state.data_ptr(), None, 0, self.policy.record_ptr(0),
+                      cs.cuda_stream)
             if l == a.num_layers - 1 and not self._in_capture:
                 self.policy.n_records += a.num_layers
         else:
@@ -808,8 +807,9 @@ class OffloadEngine:
 
     # ------------------------------------------------- offloaded decode (graphs)
     def _offload_graphable(self) -> bool:
+        # the random predictor draws on the host every step: not graph-capturable
         return (not self.resident_mode and self.ep is None and self.cfg.use_graph and
-                self.arch.head_dim in (64, 128))
+                self.arch.head_dim in (64, 128) and self.policy.prefetch_kind != "random")
 
     def _decode_head(self, l: int, X: torch.Tensor, X2: torch.Tensor, B: int):
         """Layer l of a decode step up to the MoE decision: attention block

@@ -26,8 +26,13 @@ import torch
 from . import _dev, _lib
 from .cache import initial_resident_set
 from .cost_model import CostModel
-from .errors import SimulationError
+from .errors import AssignmentError, CacheError, SimulationError
 from .trace import route_device, topk_indices
+
+
+ASSIGNMENT_CODES = {"greedy": 0, "all-cpu": 1, "all-gpu": 2, "beam": 3, "optimal": 4,
+                    "static-threshold": 5}
+CACHE_CODES = {"workload": 0, "lru": 1, "score": 2}
 
 
 def default_u_size(num_experts: int, capacity: int) -> int:
@@ -45,12 +50,26 @@ class PolicyEngine:
                  scheduling_overhead_ms: float = 0.0, solver_node_cost_ms: float = 0.0,
                  prefetch_compute_ms: float = 0.0, non_moe_override: float | None = None,
                  max_records: int = 4096, all_resident: bool = False,
-                 initial_on_gpu: np.ndarray | None = None):
+                 initial_on_gpu: np.ndarray | None = None, beam_width: int = 2,
+                 threshold: float | None = None, exact_solver_limit: int = 24,
+                 cache_policy: str = "workload", insert_demand_fetched: bool = False,
+                 insert_prefetched: bool = False, prefetch_kind: str = "residual",
+                 frequency_table: np.ndarray | None = None):
         if N > _lib.MAX_EXPERTS:
             raise SimulationError(f"at most {_lib.MAX_EXPERTS} experts per layer")
-        if assignment not in ("greedy", "all-cpu", "all-gpu"):
-            raise SimulationError(f"assignment policy {assignment!r} is not on the B200 path "
-                                  f"(greedy | all-cpu | all-gpu)")
+        if assignment not in ASSIGNMENT_CODES:
+            raise SimulationError(f"unknown assignment policy {assignment!r}; choose from "
+                                  f"{tuple(ASSIGNMENT_CODES)}")
+        if cache_policy not in CACHE_CODES:
+            raise SimulationError(f"unknown cache policy {cache_policy!r}")
+        if prefetch_kind not in ("residual", "feature", "statistical", "random"):
+            raise SimulationError(f"unknown prefetch kind {prefetch_kind!r}")
+        if assignment == "beam" and not (1 <= beam_width <= _lib.MAX_BEAM):
+            raise SimulationError(f"beam_width must be in [1, {_lib.MAX_BEAM}] on the device "
+                                  f"solver, got {beam_width}")
+        if prefetch_kind == "statistical" and prefetch_size > 0 and frequency_table is None:
+            raise SimulationError("statistical prefetching requires a calibration frequency "
+                                  "table")
         dev = _dev.require_cuda()
         self.L, self.N, self.k = L, N, k
         self.cm = cost_model
@@ -65,7 +84,18 @@ class PolicyEngine:
                    else cost_model.non_moe_layer_time)
         cfg = _lib.PolicyConfigC()
         cfg.L, cfg.N, cfg.k = L, N, k
-        cfg.assignment = {"greedy": 0, "all-cpu": 1, "all-gpu": 2}[assignment]
+        cfg.assignment = ASSIGNMENT_CODES[assignment]
+        cfg.beam_width = int(beam_width)
+        cfg.exact_solver_limit = int(exact_solver_limit)
+        cfg.has_threshold = int(threshold is not None)
+        cfg.threshold = float(threshold) if threshold is not None else 0.0
+        cfg.cache_policy = CACHE_CODES[cache_policy]
+        cfg.insert_demand = int(bool(insert_demand_fetched))
+        cfg.insert_prefetched = int(bool(insert_prefetched))
+        self.assignment = assignment
+        self.cache_policy = cache_policy
+        self.prefetch_kind = prefetch_kind
+        self.seed = int(seed)
         cfg.gpu_capacity = -1 if gpu_capacity is None else int(gpu_capacity)
         cfg.prefetch_size = self.prefetch_size
         cfg.cache_enabled = int(self.cache_enabled)
@@ -97,11 +127,24 @@ class PolicyEngine:
         self.counters = torch.zeros((L, 2), dtype=torch.int32, device=dev)
         self.arrived = torch.zeros((L, N), dtype=torch.uint8, device=dev)
         self.predicted = torch.zeros((N,), dtype=torch.int64, device=dev)
+        # LRU clocks (cache.py:96-99): (L, N+1) int64, the layer's clock last
+        self.lru_state = torch.zeros((L, N + 1), dtype=torch.int64, device=dev)
+        self._probs = None                  # score policy: (T, N) f64 gate scores
         self.residuals = residuals
-        if self.prefetch_size > 0 and residuals is None:
+        if self.prefetch_size > 0 and residuals is None and prefetch_kind in ("residual",
+                                                                               "feature"):
             raise SimulationError("residual prefetching requires calibrated residual vectors; "
                                   "run the calibrate step first")
+        self.freq = (torch.from_numpy(np.ascontiguousarray(frequency_table, dtype=np.int64))
+                     .to(dev) if frequency_table is not None else None)
         self.max_records = max_records
+        # random predictor: numpy's PCG64 stream (prefetch.py:58-60,150-151) drawn
+        # on the host, one permutation per decision, staged in pinned memory
+        self._rng = None
+        self._perm_host = (torch.zeros((max_records, N), dtype=torch.int64, pin_memory=True)
+                           if prefetch_kind == "random" and self.prefetch_size > 0 else None)
+        self._perm_dev = (torch.zeros((N,), dtype=torch.int64, device=dev)
+                          if self._perm_host is not None else None)
         self.records = (_lib.LayerRecordC * max_records)()
         self._rec_buf = torch.empty((max_records * _lib.RECORD_BYTES,), dtype=torch.uint8,
                                     pin_memory=True)
@@ -115,7 +158,10 @@ class PolicyEngine:
         self.scores.zero_()
         self.counters.zero_()
         self.arrived.zero_()
+        self.lru_state.zero_()
         self.n_records = 0
+        if self.prefetch_kind == "random":
+            self._rng = np.random.default_rng(self.seed)
         return self.on_gpu.cpu().numpy().astype(bool)
 
     # -- stepping --------------------------------------------------------------
@@ -128,32 +174,81 @@ class PolicyEngine:
     def layer_step(self, step: int, layer: int, token_index: int, is_eos: bool,
                    workloads: torch.Tensor, hidden: torch.Tensor | None,
                    gate_next: torch.Tensor | None, stream=None,
-                   predicted: torch.Tensor | None = None) -> int:
+                   predicted: torch.Tensor | None = None,
+                   gate_this: torch.Tensor | None = None) -> int:
         """Queue the decision of (step, layer) on ``stream``; returns the
         record index (valid on the host once the stream reaches it).
         ``predicted`` supplies layer+1's predicted workloads directly (the
-        expert-parallel path all-reduces them across ranks first)."""
+        expert-parallel path all-reduces them across ranks first);
+        ``gate_this`` (this layer's gate) feeds the score cache policy."""
         if self.n_records >= self.max_records:
             raise SimulationError("decision log full")
         sp = _dev.stream_ptr(stream)
-        pred_p = None
-        if predicted is not None and self.prefetch_size > 0 and layer < self.L - 1:
-            pred_p = predicted.data_ptr()
-        elif self.prefetch_size > 0 and layer < self.L - 1:
-            if hidden is None or gate_next is None:
-                raise SimulationError("prefetching requires the layer's gate inputs")
-            _, _, wl = route_device(hidden, gate_next, self.k, residual=self.residuals[layer],
-                                    want_idx=False, want_weights=False, stream=stream,
-                                    out=(None, None, self.predicted))
-            self.predicted = wl
-            pred_p = wl.data_ptr()
         i = self.n_records
+        pred_p = self.predicted_ptr(layer, hidden, gate_next, stream, predicted, i)
+        probs_p, n_tok = self.gate_probs_ptr(hidden, gate_this, stream)
         _lib.call("dali_policy_layer", C.addressof(self.cfg), C.addressof(self.cm_c), step,
                   layer, token_index, int(bool(is_eos)), workloads.data_ptr(), pred_p,
                   self.on_gpu.data_ptr(), self.scores.data_ptr(), self.counters.data_ptr(),
-                  self.arrived.data_ptr(), self.slot_of.data_ptr(), self.record_ptr(i), sp)
+                  self.arrived.data_ptr(), self.slot_of.data_ptr(), self.lru_state.data_ptr(),
+                  probs_p, n_tok, self.record_ptr(i), sp)
         self.n_records += 1
         return i
+
+    def predicted_ptr(self, layer: int, hidden, gate_next, stream=None, predicted=None,
+                      rec_index: int = 0):
+        """Device pointer to layer+1's predicted workloads for the configured
+        predictor (None when nothing is prefetched after this layer):
+        residual / feature -> routing kernel on the (shifted) gate inputs;
+        statistical -> the calibration table row; random -> the next numpy
+        permutation, staged through pinned memory by a kernel copy."""
+        if self.prefetch_size <= 0 or layer >= self.L - 1:
+            return None
+        if predicted is not None:
+            return predicted.data_ptr()
+        if self.prefetch_kind == "statistical":
+            return self.freq[layer + 1].data_ptr()
+        if self.prefetch_kind == "random":
+            if self._rng is None:
+                self._rng = np.random.default_rng(self.seed)
+            row = self._perm_host[rec_index]
+            row.copy_(torch.from_numpy(self._rng.permutation(self.N).astype(np.int64)))
+            _lib.call("dali_copy_mapped", self._perm_dev.data_ptr(), row.data_ptr(), self.N * 8,
+                      _dev.stream_ptr(stream))
+            return self._perm_dev.data_ptr()
+        if hidden is None or gate_next is None:
+            raise SimulationError("prefetching requires the layer's gate inputs")
+        _, _, wl = route_device(hidden, gate_next, self.k, residual=self.residuals[layer],
+                                want_idx=False, want_weights=False, stream=stream,
+                                out=(None, None, self.predicted))
+        return wl.data_ptr()
+
+    def gate_probs_ptr(self, hidden, gate_this, stream=None):
+        """(pointer, tokens) of this layer's fp64 gate scores for the score
+        cache policy (gate_scores, trace.py:242-250), else (None, 0)."""
+        if not (self.cache_enabled and self.cache_policy == "score"):
+            return None, 0
+        if hidden is None or gate_this is None:
+            raise CacheError("score policy requires per-expert gate scores")
+        T = hidden.shape[0]
+        if self._probs is None or self._probs.shape[0] < T:
+            self._probs = torch.empty((max(T, 1), self.N), dtype=torch.float64,
+                                      device=hidden.device)
+        fn = "dali_gate_probs_f64" if hidden.dtype == torch.float64 else "dali_gate_probs_bf16"
+        g = gate_this.to(hidden.dtype).contiguous()
+        _lib.call(fn, hidden.data_ptr(), g.data_ptr(), T, hidden.shape[1], self.N,
+                  self._probs.data_ptr(), _dev.stream_ptr(stream))
+        return self._probs.data_ptr(), T
+
+    def check_errors(self) -> None:
+        """Raise what the reference raises for refused instances (the exact
+        solver's activated-expert limit, assignment.py:284-288)."""
+        for i in range(self.n_records):
+            r = self.record(i)
+            if r.err:
+                raise AssignmentError(
+                    f"exact solver limited to {self.cfg.exact_solver_limit} activated experts, "
+                    f"instance has {r.n_act}; use greedy_assign instead")
 
     # -- reporting -------------------------------------------------------------
     def build_report(self, step_tokens: list[int], true_workloads: dict, spec: dict) -> dict:
@@ -268,6 +363,9 @@ class PolicyEngine:
                           if r.ev_valid else None),
                 "cpu_busy": r.cpu_busy, "gpu_makespan": r.gpu_makespan,
                 "latency": r.latency, "demand_end": r.demand_end,
+                "inserts": [(r.layer + (1 if r.ins_kind[j] == 2 else 0), int(r.ins_victim[j]),
+                             int(r.ins_expert[j]), ("lru", "demand", "prefetch")[r.ins_kind[j]])
+                            for j in range(r.n_ins)],
             })
         return out
 

@@ -5,14 +5,15 @@ calibrated residual and applies the next layer's gate on device (routing
 kernel with the residual fused into its shared-memory staging), then picks
 the prefetch set with the stable top-P kernel.  ``calibrate_residuals``
 (Eq. 11, prefetch.py:88-104) accumulates in fp64 on device.
-``prefetch_accuracy`` is a host metric.  Only the input-dependent kinds
-("residual", "feature") are on the B200 path; the statistical and random
-baselines are out of scope.
+``prefetch_accuracy`` is a host metric.  The reference's comparison
+predictors are here too: "statistical" ranks a calibration frequency table
+and "random" ranks a numpy PCG64 permutation (drawn on the host, the same
+stream as the reference), both through the device top-P kernel.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -21,7 +22,7 @@ from . import _dev, _lib
 from .errors import PrefetchError
 from .trace import ResidualVectors, Trace, route_device, topk_indices
 
-PREDICTOR_KINDS = ("residual", "feature")
+PREDICTOR_KINDS = ("residual", "feature", "statistical", "random")
 
 
 @dataclass
@@ -35,14 +36,39 @@ class PrefetchDecision:
 class Predictor:
     kind: str
     residuals: ResidualVectors | None = None
+    frequency_table: np.ndarray | None = None
+    seed: int = 0
+    n_experts: int | None = None
+    _rng: np.random.Generator | None = field(default=None, repr=False)
 
     def __post_init__(self):
         if self.kind not in PREDICTOR_KINDS:
             raise PrefetchError(f"unknown predictor kind {self.kind!r}; choose from "
-                                f"{PREDICTOR_KINDS} (statistical/random baselines are not on "
-                                f"the B200 path)")
+                                f"{PREDICTOR_KINDS}")
         if self.kind == "residual" and self.residuals is None:
             raise PrefetchError("residual predictor requires calibrated residual vectors")
+        if self.kind == "statistical" and self.frequency_table is None:
+            raise PrefetchError("statistical predictor requires a calibration frequency table")
+        if self.kind == "random":
+            self._rng = np.random.default_rng(self.seed)
+
+
+def statistical_predictor(calibration_trace: Trace) -> Predictor:
+    """Rank experts by per-layer activation counts (prefetch.py:63-66)."""
+    return Predictor(kind="statistical",
+                     frequency_table=activation_frequency_table(calibration_trace))
+
+
+def random_predictor(seed: int = 0, n_experts: int | None = None) -> Predictor:
+    return Predictor(kind="random", seed=seed, n_experts=n_experts)
+
+
+def activation_frequency_table(trace: Trace) -> np.ndarray:
+    """Per-layer summed workloads over all steps, (L, N) (prefetch.py:76-85)."""
+    if not trace.steps:
+        raise PrefetchError("calibration trace has no steps")
+    return np.sum(np.stack([np.asarray(s.workloads, dtype=np.int64) for s in trace.steps]),
+                  axis=0)
 
 
 def residual_predictor(residuals: ResidualVectors) -> Predictor:
@@ -88,6 +114,24 @@ def predict_next_layer(predictor: Predictor, hidden_states, gate_next, k: int,
                        prefetch_size: int, current_layer: int) -> PrefetchDecision:
     if prefetch_size < 0:
         raise PrefetchError("prefetch_size must be >= 0")
+    if predictor.kind in ("statistical", "random"):
+        if predictor.kind == "statistical":
+            table = predictor.frequency_table
+            if not (0 <= current_layer + 1 < table.shape[0]):
+                raise PrefetchError(f"layer {current_layer + 1} outside calibration table with "
+                                    f"{table.shape[0]} layers")
+            predicted = np.asarray(table[current_layer + 1], dtype=np.int64).copy()
+        else:
+            n = predictor.n_experts
+            if n is None and gate_next is not None:
+                n = np.asarray(gate_next).shape[1]
+            if n is None:
+                raise PrefetchError("random predictor needs n_experts or gate_next to size its "
+                                    "score vector")
+            predicted = predictor._rng.permutation(n).astype(np.int64)
+        pset = select_prefetch_set(_dev.to_dev(predicted, torch.int64), prefetch_size)
+        return PrefetchDecision(layer=current_layer + 1, predicted_workloads=predicted,
+                                prefetch_set=pset.cpu().numpy().astype(np.int64))
     if hidden_states is None or gate_next is None:
         raise PrefetchError(f"{predictor.kind} predictor requires hidden states and the next "
                             f"layer's gate")

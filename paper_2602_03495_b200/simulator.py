@@ -7,9 +7,11 @@ runs on the routing kernel and every assignment / lookup / prefetch-window /
 cache decision is made by the fused single-CTA policy kernel.  The report is
 assembled from the device decision log with the reference's accumulation
 order, so on identical inputs it equals ``moesim.simulate_run(...).to_dict()``
-(minus the ``timelines`` detail).  Only the hot-path policy set is
-supported: greedy / all-cpu assignment, residual (or feature = zero
-residual) prefetch, workload cache.
+(minus the ``timelines`` detail).  Every reference policy runs on the
+device: greedy / beam / branch-and-bound optimal / static-threshold /
+all-cpu / all-gpu assignment, residual / feature / statistical / random
+predictors (the random predictor's numpy PCG64 draws are made on the host),
+workload / LRU / score caches and the insert toggles.
 """
 
 from __future__ import annotations
@@ -25,7 +27,7 @@ from .errors import SimulationError
 from .policy_engine import PolicyEngine, default_u_size  # noqa: F401  (re-export)
 from .trace import ResidualVectors, Trace
 
-ASSIGNMENT_POLICIES = ("greedy", "all-cpu", "all-gpu")
+ASSIGNMENT_POLICIES = ("greedy", "optimal", "beam", "all-cpu", "all-gpu", "static-threshold")
 
 
 @dataclass
@@ -104,34 +106,43 @@ class RunReport:
 
 
 def _check(trace: Trace, config: SimConfig) -> None:
+    """Configuration checks with the reference's messages
+    (_validate_run_config / _build_predictor, simulator.py:266-315)."""
     cfg = trace.model_config
     if config.assignment_policy not in ASSIGNMENT_POLICIES:
-        raise SimulationError(f"assignment policy {config.assignment_policy!r} is not on the "
-                              f"B200 path; choose from {ASSIGNMENT_POLICIES}")
+        raise SimulationError(f"unknown assignment policy {config.assignment_policy!r}; "
+                              f"choose from {ASSIGNMENT_POLICIES}")
     if config.prefetch_enabled:
-        if config.prefetch_kind not in ("residual", "feature"):
-            raise SimulationError(f"prefetch kind {config.prefetch_kind!r} is not on the B200 "
-                                  f"path (residual | feature)")
         if not trace.has_features:
             raise SimulationError("prefetching requires a trace with hidden states")
-        if trace.gate_params is None:
+        if config.prefetch_kind in ("residual", "feature") and trace.gate_params is None:
             raise SimulationError("feature-based prefetching requires the trace's gate "
                                   "parameters (sidecar file)")
         if config.prefetch_size > cfg.num_routed_experts:
             raise SimulationError("prefetch_size cannot exceed the expert count")
-        if config.prefetch_kind == "residual":
+    if config.cache_enabled:
+        if not (0 < config.cache_capacity < cfg.num_routed_experts):
+            raise SimulationError(f"cache capacity must be in (0, {cfg.num_routed_experts}), "
+                                  f"got {config.cache_capacity}")
+        if config.cache_policy == "score" and not (trace.has_features
+                                                   and trace.gate_params is not None):
+            raise SimulationError("score cache policy requires a featureful trace with gate "
+                                  "parameters")
+    if config.threshold is not None and config.threshold < 0:
+        raise SimulationError("static threshold must be >= 0")
+    if config.prefetch_enabled:
+        kind = config.prefetch_kind
+        if kind == "residual":
             if config.residuals is None:
                 raise SimulationError("residual prefetching requires calibrated residual "
                                       "vectors; run the calibrate step first")
             config.residuals.check_shape(cfg)
-    if config.cache_enabled:
-        if config.cache_policy != "workload":
-            raise SimulationError(f"cache policy {config.cache_policy!r} is not on the B200 path")
-        if not (0 < config.cache_capacity < cfg.num_routed_experts):
-            raise SimulationError(f"cache capacity must be in (0, {cfg.num_routed_experts}), "
-                                  f"got {config.cache_capacity}")
-    if config.insert_demand_fetched or config.insert_prefetched:
-        raise SimulationError("insert toggles are baselines outside the B200 path")
+        elif kind == "statistical":
+            if config.frequency_table is None:
+                raise SimulationError("statistical prefetching requires a calibration "
+                                      "frequency table")
+        elif kind not in ("feature", "random"):
+            raise SimulationError(f"unknown prefetch kind {kind!r}")
 
 
 def simulate_run(trace: Trace, config: SimConfig) -> RunReport:
@@ -140,13 +151,15 @@ def simulate_run(trace: Trace, config: SimConfig) -> RunReport:
     L, N, k, d = cfg.num_layers, cfg.num_routed_experts, cfg.top_k, cfg.hidden_dim
     dev = _dev.require_cuda()
     pre = config.prefetch_enabled
+    feat = pre and config.prefetch_kind in ("residual", "feature")
+    score = config.cache_enabled and config.cache_policy == "score"
     res_dev = None
-    if pre:
+    if feat:
         res = (config.residuals.values if config.prefetch_kind == "residual"
                else np.zeros((L - 1, d)))
         res_dev = torch.from_numpy(np.ascontiguousarray(res)).to(dev)
     gates = None
-    if pre:
+    if feat or score:
         gates = torch.from_numpy(np.ascontiguousarray(trace.gate_params.weights)).to(dev)
     n_steps = len(trace.steps)
     eng = PolicyEngine(L, N, k, config.cost_model, assignment=config.assignment_policy,
@@ -159,22 +172,34 @@ def simulate_run(trace: Trace, config: SimConfig) -> RunReport:
                        solver_node_cost_ms=config.solver_node_cost_ms,
                        prefetch_compute_ms=config.prefetch_compute_ms,
                        non_moe_override=config.non_moe_override,
-                       max_records=max(1, n_steps * L))
+                       max_records=max(1, n_steps * L), beam_width=config.beam_width,
+                       threshold=config.threshold,
+                       exact_solver_limit=config.exact_solver_limit,
+                       cache_policy=config.cache_policy or "workload",
+                       insert_demand_fetched=config.insert_demand_fetched,
+                       insert_prefetched=config.insert_prefetched,
+                       prefetch_kind=config.prefetch_kind or "residual",
+                       frequency_table=(np.asarray(config.frequency_table)
+                                        if pre and config.prefetch_kind == "statistical"
+                                        else None))
+    eng.new_run()
     true_wl = {}
     tokens = []
     for si, st in enumerate(trace.steps):
         wl = torch.from_numpy(np.ascontiguousarray(st.workloads, dtype=np.int64)).to(dev)
         hid = (torch.from_numpy(np.ascontiguousarray(st.hidden)).to(dev)
-               if pre and st.hidden is not None else None)
+               if (feat or score) and st.hidden is not None else None)
         for l in range(L):
             true_wl[(si, l)] = st.workloads[l]
             eng.layer_step(si, l, st.token_index, st.eos, wl[l],
                            hid[l] if hid is not None else None,
-                           gates[l + 1] if (pre and l < L - 1) else None)
+                           gates[l + 1] if (feat and l < L - 1) else None,
+                           gate_this=gates[l] if score else None)
         tokens.append(st.tokens)
         if st.eos:
             break
     torch.cuda.synchronize()
+    eng.check_errors()
     rep = eng.build_report(tokens, true_wl, config.to_dict())
     rep["_decisions"] = eng.decision_log()
     return RunReport(rep)

@@ -32,8 +32,9 @@ def test_library_exports_every_declared_symbol():
 def test_struct_layouts_match_header():
     from paper_2602_03495_b200 import _lib
     assert ctypes.sizeof(_lib.CostModelC) == 8 + 4 * 32 * 8 + 3 * 8
-    assert ctypes.sizeof(_lib.LayerRecordC) == 16 * 4 + 8 * 8 + 4 * 256 + 5 * 256 * 2 + 4 * 256
-    assert ctypes.sizeof(_lib.PolicyConfigC) == 12 * 4 + 4 * 8
+    assert ctypes.sizeof(_lib.LayerRecordC) == (16 * 4 + 8 * 8 + 4 * 256 + 5 * 256 * 2 + 4 * 256
+                                                + 2 * 256 * 2 + 256)
+    assert ctypes.sizeof(_lib.PolicyConfigC) == 18 * 4 + 5 * 8
 
 
 def test_version_and_error_string():

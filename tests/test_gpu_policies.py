@@ -307,3 +307,135 @@ def test_decision_log_matches_oracle(dali, traces):
             assert rep[k] == orep[k], k
         if nm == 40.0:
             assert n_arrived > 0   # the arrival rule is exercised
+
+
+# --- alternative policies ---------------------------------
+
+def test_simulate_run_baselines_match_reference_reports(dali, golden, traces):
+    """Beam / optimal / static solvers, LRU + score caches, insert toggles,
+    feature / statistical / random predictors: whole reports equal the
+    frozen moesim reports; the exact solver refuses the same instances."""
+    import sys
+    sys.path.insert(0, __file__.rsplit("/", 1)[0] + "/golden")
+    from make_golden_cfgs import baseline_cfgs
+    _, meta = golden
+    for key, want in meta["runs_baseline"].items():
+        tname, rname = key.split("/")
+        tr, info = traces[tname], meta["traces"][tname]
+        over = dict(baseline_cfgs(info["N"]))[rname]
+        res = P.calibrate([s.hidden for s in tr.steps])
+        cfg = dali.ModelConfig(info["L"], info["N"], 0, info["k"], info["d"])
+        t = dali.Trace(cfg, info["B"], info["phase"],
+                       [dali.TokenStep(s.token_index, s.tokens, s.workloads, s.hidden, s.eos)
+                        for s in tr.steps], gate_params=dali.GateParams(tr.gates))
+        sc = _sim_config(dali, rname, over, res)
+        if over.get("prefetch_kind") == "statistical":
+            sc.frequency_table = P.frequency_table([s.workloads for s in tr.steps])
+        if "error" in want:
+            with pytest.raises(dali.AssignmentError, match="exact solver limited"):
+                dali.simulate_run(t, sc)
+            continue
+        rep = dali.simulate_run(t, sc).to_dict()
+        rep.pop("spec")
+        rep.pop("timelines")
+        assert rep == want, key
+
+
+def test_baseline_decision_logs_match_oracle(dali, traces):
+    """Entry by entry incl. the LRU / toggle insertions the engine executes."""
+    tr = traces["headline"]
+    res = P.calibrate([s.hidden for s in tr.steps])
+    steps = [D.StepInput(s.token_index, s.tokens, s.workloads, s.hidden, s.eos)
+             for s in tr.steps]
+    cfg = dali.ModelConfig(tr.L, tr.N, 0, tr.k, tr.d)
+    t = dali.Trace(cfg, 32, "decode", [dali.TokenStep(s.token_index, s.tokens, s.workloads,
+                                                      s.hidden, s.eos) for s in tr.steps],
+                   gate_params=dali.GateParams(tr.gates))
+    for pol, ins_d, ins_p in [("lru", False, True), ("workload", True, True),
+                              ("score", True, False)]:
+        dcfg = D.DriverConfig(tables=P.default_tables(non_moe_layer_time=3.0), prefetch_size=2,
+                              residuals=res, cache_capacity=4, cache_policy=pol, w_size=4,
+                              u_size=1, seed=3, insert_demand_fetched=ins_d,
+                              insert_prefetched=ins_p)
+        _, recs = D.run(steps, tr.gates, dcfg, tr.L, tr.N, tr.k)
+        sc = dali.SimConfig(cost_model=dali.default_cost_model(non_moe_layer_time=3.0),
+                            prefetch_kind="residual", prefetch_size=2,
+                            residuals=dali.ResidualVectors(res), cache_policy=pol,
+                            cache_capacity=4, w_size=4, u_size=1, seed=3,
+                            insert_demand_fetched=ins_d, insert_prefetched=ins_p)
+        got = dali.simulate_run(t, sc).decisions
+        assert len(got) == len(recs)
+        n_ins = 0
+        for g, o in zip(got, recs):
+            assert g["hits"] == o.lookups, (pol, o.step, o.layer)
+            assert g["inserts"] == o.inserts, (pol, o.step, o.layer)
+            assert g["event"] == o.event
+            n_ins += len(o.inserts)
+        assert n_ins > 0, pol
+
+
+def test_single_instance_solvers_vs_oracle(dali):
+    """beam_assign / optimal_assign / static_threshold_assign on random
+    dyadic-time instances (reference conftest.py:36-58 style) == oracle."""
+    rng = np.random.default_rng(41)
+    for it in range(120):
+        n = int(rng.integers(1, 14))
+        w = rng.integers(0, 6, size=n).astype(np.int64)
+        res = rng.random(n) < 0.3
+        ct = rng.integers(1, 64, size=n) / 64.0
+        gt = rng.integers(1, 64, size=n) / 64.0
+        ct[w == 0] = 0.0
+        gt[w == 0] = 0.0
+        cap = None if rng.random() < 0.5 else int(rng.integers(0, 4))
+        inst = dali.AssignmentInstance.from_times(ct, gt, resident=res, workloads=w,
+                                                  gpu_capacity=cap)
+        bw = int(rng.integers(1, 5))
+        C, G = P.beam(w, res, ct, gt, cap, bw)
+        a = dali.beam_assign(inst, bw)
+        assert a.C.tolist() == C.tolist() and a.G.tolist() == G.tolist(), ("beam", it)
+        C, G, nodes = P.optimal(w, res, ct, gt, cap)
+        a, mk, nd = dali.optimal_assign_with_stats(inst)
+        assert a.C.tolist() == C.tolist() and a.G.tolist() == G.tolist(), ("opt", it)
+        assert nd == nodes, ("nodes", it)
+        thr = None if it % 2 else float(rng.integers(0, 5))
+        C, G = P.static_threshold(w, res, cap, thr)
+        a = dali.static_threshold_assign(inst, thr)
+        assert a.C.tolist() == C.tolist() and a.G.tolist() == G.tolist(), ("static", it)
+
+
+def test_lru_lookup_and_force_insert(dali):
+    st = dali.init_cache(0, 6, 2, 4, 1, policy="lru", seed=0)
+    oc = P.new_cache(0, 6, 2, 4, 1, 0, policy="lru")
+    for e in [0, 1, 2, 0, 3, 3, 4, 1, 0, 5]:
+        assert dali.lookup(st, e) == P.lookup(oc, e)[0]
+        assert st.on_gpu.tolist() == oc.on_gpu.tolist()
+    for e in [2, 4, 5]:
+        assert dali.force_insert(st, e) == P.force_insert(oc, e)
+        assert st.on_gpu.tolist() == oc.on_gpu.tolist()
+    ws = dali.init_cache(1, 8, 3, 2, 1, policy="workload", seed=2)
+    ow = P.new_cache(1, 8, 3, 2, 1, 2)
+    ws.scores = np.array([3.0, 1.0, 1.0, 0.0, 2.0, 5.0, 0.0, 4.0])
+    ow.scores = ws.scores.copy()
+    for e in range(8):
+        assert dali.force_insert(ws, e) == P.force_insert(ow, e)
+        assert ws.on_gpu.tolist() == ow.on_gpu.tolist()
+
+
+def test_statistical_and_random_predictors(dali, traces):
+    tr = traces["tiny_decode"]
+    cfg = dali.ModelConfig(tr.L, tr.N, 0, tr.k, tr.d)
+    t = dali.Trace(cfg, 1, "decode", [dali.TokenStep(s.token_index, s.tokens, s.workloads,
+                                                     s.hidden, s.eos) for s in tr.steps])
+    sp = dali.statistical_predictor(t)
+    table = P.frequency_table([s.workloads for s in tr.steps])
+    assert np.array_equal(sp.frequency_table, table)
+    for l in range(tr.L - 1):
+        d = dali.predict_next_layer(sp, None, None, tr.k, 3, l)
+        assert d.prefetch_set.tolist() == P.stable_topk(table[l + 1].astype(float), 3).tolist()
+    rp = dali.random_predictor(seed=9, n_experts=tr.N)
+    rng = np.random.default_rng(9)
+    for l in range(5):
+        d = dali.predict_next_layer(rp, None, None, tr.k, 2, 0)
+        perm = rng.permutation(tr.N)
+        assert d.predicted_workloads.tolist() == perm.tolist()
+        assert d.prefetch_set.tolist() == P.stable_topk(perm.astype(float), 2).tolist()
