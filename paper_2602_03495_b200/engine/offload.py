@@ -54,8 +54,17 @@ class EngineConfig:
     w_size: int = 4
     u_size: int | None = None
     seed: int = 0
-    assignment: str = "greedy"
+    assignment: str = "greedy"              # or a reference baseline solver: beam | optimal |
+    #                                         static-threshold | all-cpu | all-gpu
     gpu_capacity: int | None = None
+    beam_width: int = 2
+    threshold: float | None = None
+    exact_solver_limit: int = 24
+    cache_policy: str = "workload"          # or the lru / score baselines
+    insert_demand_fetched: bool = False     # reference insert toggles (cache.py:13-15)
+    insert_prefetched: bool = False
+    prefetch_kind: str = "residual"         # or feature | statistical | random
+    frequency_table: np.ndarray | None = None   # statistical predictor (L, N)
     cpu_threads: int | None = None
     staging_slots: int | None = None
     capture: bool = False                   # keep gate inputs for oracle replay
@@ -77,6 +86,7 @@ class RunStats:
     demand_copies: int = 0
     prefetch_copies: int = 0
     replace_copies: int = 0
+    insert_copies: int = 0                 # D2D staging -> slot (baseline cache policies)
     cpu_expert_calls: int = 0
     gpu_expert_calls: int = 0
     dali_launches: int = 0
@@ -145,7 +155,11 @@ class OffloadEngine:
             prefetch_size=cfg.prefetch_size if not self.resident_mode else 0,
             residuals=res_dev, cache_capacity=slots, w_size=cfg.w_size, u_size=cfg.u_size,
             seed=cfg.seed, max_records=cfg.max_records, all_resident=self.resident_mode,
-            num_shared_experts=a.num_shared_experts)
+            num_shared_experts=a.num_shared_experts, beam_width=cfg.beam_width,
+            threshold=cfg.threshold, exact_solver_limit=cfg.exact_solver_limit,
+            cache_policy=cfg.cache_policy, insert_demand_fetched=cfg.insert_demand_fetched,
+            insert_prefetched=cfg.insert_prefetched, prefetch_kind=cfg.prefetch_kind,
+            frequency_table=cfg.frequency_table)
         self.copy_stream = torch.cuda.Stream()       # demand + prefetch expert copies
         self.repl_stream = torch.cuda.Stream()       # cache replacement copies (off the
         #                                              demand path: never delays a demand copy)
@@ -363,6 +377,7 @@ class OffloadEngine:
         waits = []
         used_staging = []
         n_hit = n_pf = n_dem = 0
+        stage_of = {}                      # expert -> staging slot holding its weights
         t0_ev = None
         for e in G:
             if self.resident_mode:
@@ -388,6 +403,7 @@ class OffloadEngine:
             maps[e] = self._map_addr(self.n_cache_slots + i)
             waits.append(ev)
             used_staging.append(i)
+            stage_of[e] = i
         ph = self.ptr_host[l]
         ph[:NL * 8].view(torch.int64).copy_(torch.from_numpy(ptrs.view(np.int64)))
         ph[NL * 8:NL * 16].view(torch.int64).copy_(torch.from_numpy(maps.view(np.int64)))
@@ -430,8 +446,12 @@ class OffloadEngine:
             self.stats.gpu_expert_calls += len(G)
         ffn_done = torch.cuda.Event()
         ffn_done.record(cs)
+        if rec.err:
+            self.policy.check_errors()
+        kept = self._apply_inserts(l, rec, stage_of, ffn_done, now=True)
         for i in used_staging:
-            self.staging.release(i, ffn_done)
+            if i not in kept:
+                self.staging.release(i, ffn_done)
         for key in [kk for kk in self.prefetched if kk[0] == l]:   # granted but unused
             i, ev = self.prefetched.pop(key)
             self.staging.release(i, ev)
@@ -442,6 +462,7 @@ class OffloadEngine:
                 i, ev = self._copy_into_staging(l + 1, e)
                 self.prefetched[(l + 1, e)] = (i, ev)
                 self.stats.prefetch_copies += 1
+            self._apply_inserts(l, rec, None, None, now=False)
             # replacement: admitted experts into the victims' slots once read
             if rec.ev_valid and rec.ev_n:
                 with torch.cuda.stream(self.repl_stream):
@@ -460,6 +481,58 @@ class OffloadEngine:
                                rep=int(rec.ev_n) if (rec.ev_valid and not self.resident_mode) else 0,
                                done=int(rec.n_done) if not self.resident_mode else 0)
         return yp, splits, pd.data_ptr() + NL * 16
+
+    def _apply_inserts(self, l: int, rec, stage_of, ffn_done, now: bool) -> set:
+        """Execute the cache insertions the policy kernel made outside the
+        window (LRU miss inserts, insert toggles; simulator.py:372-379,
+        421-423): the inserted expert's weights already sit in a staging slot
+        (demand copy or prefetch), so they move into the victim's HBM slot by
+        a device-to-device copy once the layer's FFN stopped reading the
+        victim.  now=True handles this layer's inserts (returns the staging
+        slots it keeps alive), now=False the prefetch inserts into layer+1."""
+        kept = set()
+        if self.resident_mode or not rec.n_ins:
+            return kept
+        if now:
+            # An LRU lookup can evict an expert this layer used from its slot and
+            # re-insert it later in the same lookup pass.  Such an expert's
+            # weights live in a cache slot that an earlier insert of this pass
+            # overwrites, so they are saved to staging before any insert copy.
+            with torch.cuda.stream(self.repl_stream):
+                self.repl_stream.wait_event(ffn_done)
+                for j in range(rec.n_ins):
+                    x = int(rec.ins_expert[j])
+                    if int(rec.ins_kind[j]) == 2 or x in stage_of:
+                        continue
+                    i = self.staging.get()
+                    if self.staging.free_after[i] is not None:
+                        self.repl_stream.wait_event(self.staging.free_after[i])
+                    self.staging.buf[i].copy_(self.cache_buf[int(self.host_slot[l, x])],
+                                              non_blocking=True)
+                    stage_of[x] = i
+        for j in range(rec.n_ins):
+            kind = int(rec.ins_kind[j])
+            if (kind == 2) == now:
+                continue
+            ll = l + 1 if kind == 2 else l
+            v, x = int(rec.ins_victim[j]), int(rec.ins_expert[j])
+            s = int(self.host_slot[ll, v])
+            with torch.cuda.stream(self.repl_stream):
+                if kind == 2:
+                    i, ev_src = self.prefetched.pop((ll, x))
+                    self.repl_stream.wait_event(ev_src)
+                else:
+                    i = stage_of.pop(x)
+                    self.repl_stream.wait_event(ffn_done)
+                self.cache_buf[s].copy_(self.staging.buf[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.repl_stream)
+            self.slot_ready[s] = ev
+            self.staging.release(i, ev)
+            kept.add(i)
+            self.host_slot[ll, x], self.host_slot[ll, v] = s, -1
+            self.stats.insert_copies += 1
+        return kept
 
     def _cpu_rows(self, l: int, rows_host: torch.Tensor, offs_np: np.ndarray, rec,
                   R: int) -> torch.Tensor | None:

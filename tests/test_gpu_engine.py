@@ -439,3 +439,87 @@ def test_offload_decode_graphs_match_eager(name):
                 assert a_[k_] == b_[k_], (rep, k_, a_["step"], a_["layer"])
             assert np.array_equal(a_["C"], b_["C"]) and np.array_equal(a_["G"], b_["G"])
         assert engs[0].policy_report() == engs[1].policy_report()
+
+
+BASELINE_ENGINE_CFGS = [
+    ("tiny", dict(cache_policy="lru", insert_prefetched=True, prefetch_size=2)),
+    ("tiny", dict(insert_demand_fetched=True, insert_prefetched=True, prefetch_size=2)),
+    ("tiny-shared", dict(cache_policy="score", prefetch_size=1)),
+    ("tiny", dict(assignment="beam", beam_width=3, prefetch_size=1)),
+    ("tiny", dict(assignment="optimal", prefetch_size=1)),
+    ("tiny", dict(assignment="static-threshold", gpu_capacity=1)),
+    ("tiny", dict(prefetch_kind="statistical", prefetch_size=2)),
+    ("tiny", dict(prefetch_kind="random", prefetch_size=2)),
+]
+
+
+@pytest.mark.parametrize("name,over", BASELINE_ENGINE_CFGS,
+                         ids=[f"{n}-{'-'.join(f'{k}={v}' for k, v in o.items())}"
+                              for n, o in BASELINE_ENGINE_CFGS])
+def test_engine_baseline_policies(name, over):
+    """The real engine under the reference's comparison policies: every
+    decision (incl. LRU / toggle insertions executed as staging->slot copies)
+    equals the oracle replaying the engine's gate inputs, and logits stay
+    within tolerance of the fp32 CPU model (so the moved weights are right)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    arch = preset(name)
+    L, N, k = arch.num_layers, arch.num_experts, arch.top_k
+    w = ModelWeights(arch, seed=21)
+    cm = default_cost_model(shared_expert_gpu_time=SHARED_MS[name], non_moe_layer_time=3.0)
+    rng = np.random.default_rng(2)
+    res = rng.standard_normal((L - 1, arch.hidden_dim)) * 0.05
+    freq = rng.integers(0, 50, size=(L, N)).astype(np.int64)
+    kw = dict(cache_slots_per_layer=2 if name == "tiny" else 6, seed=3, capture=True)
+    kw.update(over)
+    if kw.get("prefetch_kind") == "statistical":
+        kw["frequency_table"] = freq
+    eng = OffloadEngine(arch, w, cm, EngineConfig(**kw), residuals=res, max_seq=64)
+    g = torch.Generator().manual_seed(8)
+    for rep in range(2):
+        prompt = torch.randint(0, arch.vocab_size, (1, 12), generator=g)
+        toks, st = eng.generate(prompt, 8)
+        by_step = {}
+        for (s, l, h) in st.captured:
+            by_step.setdefault(s, {})[l] = h.double().numpy()
+        steps = [D.StepInput(ti, ntok, np.stack([st.workloads[(s, l)] for l in range(L)]),
+                             np.stack([by_step[s][l] for l in range(L)]), eos)
+                 for s, (ti, ntok, eos) in enumerate(st.steps_meta)]
+        gates = np.stack([w.router[l].double().cpu().numpy() for l in range(L)])
+        dkw = {key: val for key, val in kw.items() if key in (
+            "assignment", "gpu_capacity", "beam_width", "threshold", "exact_solver_limit",
+            "cache_policy", "insert_demand_fetched", "insert_prefetched", "prefetch_size",
+            "prefetch_kind", "frequency_table", "seed")}
+        if "assignment" in dkw:
+            dkw["assignment_policy"] = dkw.pop("assignment")
+        dcfg = D.DriverConfig(tables=P.default_tables(SHARED_MS[name], non_moe_layer_time=3.0),
+                              residuals=res, cache_capacity=eng.slots_per_layer,
+                              w_size=eng.cfg.w_size, u_size=eng.cfg.u_size,
+                              initial_on_gpu=st.initial_on_gpu,
+                              num_shared_experts=arch.num_shared_experts, **dkw)
+        orep, recs = D.run(steps, gates, dcfg, L, N, k)
+        got = eng.policy.decision_log()
+        assert len(got) == len(recs)
+        for a_, o in zip(got, recs):
+            assert np.array_equal(a_["C"], o.C) and np.array_equal(a_["G"], o.G), \
+                (rep, o.step, o.layer)
+            assert a_["hits"] == o.lookups and a_["inserts"] == o.inserts, (rep, o.step, o.layer)
+            assert a_["event"] == o.event
+            if o.prefetch_set is not None:
+                assert a_["pset"] == o.prefetch_set.tolist() and a_["done"] == o.completed
+        rep_ = eng.policy_report()
+        for key in ("cache_hit_rate", "prefetch_accuracy_top1", "replacement_events",
+                    "total_time_ms", "pcie_busy_fraction"):
+            assert rep_[key] == orep[key], key
+        # physical correctness: logits vs the fp32 CPU model on the same routing
+        seq = torch.cat([prompt, toks[:, :-1]], dim=1)
+        overs = {l: torch.cat([torch.from_numpy(st.topk[(s, l)])
+                               for s in range(len(st.steps_meta))], 0) for l in range(L)}
+        dense = M.dense_from_weights(w)
+        logits, _ = M.forward(arch, dense, lambda l_, e_: w.expert_host(l_, e_), seq, overs)
+        S0 = prompt.shape[1]
+        for s_, lg in enumerate(st.logits):
+            ref = logits[0, S0 - 1 + s_]
+            torch.testing.assert_close(lg[0], ref, rtol=RTOL, atol=RTOL * ref.abs().max().item())
