@@ -101,6 +101,19 @@ class RunStats:
     layer_trace: list = field(default_factory=list)  # per-layer timeline (cfg.trace_layers)
 
 
+def ffn_splits(max_rows: int, tiles: int, kb: int, n_sm: int) -> int:
+    """Split-K planes of the down projection for dali_expert_ffn_tc: the
+    smallest factor dividing f/64 that gives >= 2 CTAs per SM (``max_rows``
+    is kept for the signature: every token-tile width uses the same rule)."""
+    best = 1
+    for s in range(1, 17):
+        if kb % s == 0:
+            best = s
+            if tiles * s >= 2 * n_sm:
+                break
+    return best
+
+
 class _Staging:
     """Ring of HBM staging slots for demand / prefetch copies."""
 
@@ -242,12 +255,7 @@ class OffloadEngine:
         bn = 16 if T <= 16 else 32 if T <= 32 else 64 if T <= 64 else 128 if T <= 128 else 256
         kb = fs // 64
         tiles = ((T + bn - 1) // bn) * (d // 128)
-        sp = 1
-        for s in range(1, 17):
-            if kb % s == 0:
-                sp = s
-                if tiles * s >= 2 * self.n_sm:
-                    break
+        sp = ffn_splits(T, tiles, kb, self.n_sm)
         hs = self._ws("sh_h", (T, fs), torch.bfloat16)
         ys = self._ws("sh_y", (sp, T, d), torch.float32)
         cs = torch.cuda.current_stream()
@@ -274,16 +282,8 @@ class OffloadEngine:
     def _map_addr(self, phys: int) -> int:
         return self.maps_dev.data_ptr() + int(phys) * 256
 
-    def _splits_for(self, tiles: int) -> int:
-        """Split-K factor of the down projection so decode fills the SMs."""
-        kb = self.arch.ffn_dim // 64
-        best = 1
-        for s in range(1, 17):
-            if kb % s == 0:
-                best = s
-                if tiles * s >= 2 * self.n_sm:
-                    break
-        return best
+    def _splits_for(self, tiles: int, max_rows: int, ffn_dim: int | None = None) -> int:
+        return ffn_splits(max_rows, tiles, (ffn_dim or self.arch.ffn_dim) // 64, self.n_sm)
 
     def _load_initial_cache(self):
         if not self.slots_per_layer:
@@ -419,7 +419,7 @@ class OffloadEngine:
             bn = 16 if max_rows <= 16 else 32 if max_rows <= 32 else 64 if max_rows <= 64 \
                 else 128 if max_rows <= 128 else 256
             tiles = sum((int(wl_np[e]) + bn - 1) // bn for e in G) * (d // 128)
-            splits = self._splits_for(tiles)
+            splits = self._splits_for(tiles, max_rows)
         yp = self._ws("yp", (splits, max(R, 1), d), torch.float32)
         if G and R > 0:
             for ev in waits:
@@ -693,7 +693,7 @@ class OffloadEngine:
         mr = min(T, R)                 # an expert sees each token at most once
         bn = 16 if mr <= 16 else 32 if mr <= 32 else 64 if mr <= 64 else 128 if mr <= 128 else 256
         tiles = min(N, R) * ((mr + bn - 1) // bn) * (d // 128)
-        splits = self._splits_for(tiles)
+        splits = self._splits_for(tiles, mr)
         yp = self._ws("yp", (splits, R, d), torch.float32)
         hbuf = self._ws("hbuf", (R, f), torch.bfloat16)
         if self.cfg.time_ffn:

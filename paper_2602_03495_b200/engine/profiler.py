@@ -21,6 +21,7 @@ from .. import _lib
 from ..cost_model import CostModel, fit_cost_model, quantize_ms
 from .arch import MoEArch
 from .cpu_worker import cpu_expert_rows
+from .offload import ffn_splits
 
 
 def _cpu_expert(h: torch.Tensor, blk: torch.Tensor, d: int, f: int, threads: int):
@@ -82,13 +83,8 @@ def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
         offs = torch.tensor([0] + [w] * N, dtype=torch.int32, device=dev)
         hbuf = torch.empty((w, f), dtype=torch.bfloat16, device=dev)
         tiles = ((w + 15) // 16 if w <= 16 else 1) * (d // 128)
-        splits = 1
-        kb = f // 64
-        for s_ in range(1, 17):
-            if kb % s_ == 0:
-                splits = s_
-                if tiles * s_ >= 2 * torch.cuda.get_device_properties(dev).multi_processor_count:
-                    break
+        splits = ffn_splits(w, tiles, f // 64,
+                            torch.cuda.get_device_properties(dev).multi_processor_count)
         yp = torch.empty((splits, w, d), dtype=torch.float32, device=dev)
 
         def run():

@@ -15,6 +15,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_03495_b200 import _lib  # noqa: E402
+from paper_2602_03495_b200.engine.offload import ffn_splits  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--mode", default="both")
@@ -50,12 +51,7 @@ def run(counts, label):
     mr = max(counts)
     bn = 16 if mr <= 16 else 32 if mr <= 32 else 64 if mr <= 64 else 128 if mr <= 128 else 256
     tiles = sum((c + bn - 1) // bn for c in counts if c) * (d // 128)
-    splits = 1
-    for s in range(1, 17):
-        if (f // 64) % s == 0:
-            splits = s
-            if tiles * s >= 2 * nsm:
-                break
+    splits = ffn_splits(mr, tiles, f // 64, nsm)
     y = torch.empty(splits, rows, d, dtype=torch.float32, device=dev)
     cs = torch.cuda.current_stream().cuda_stream
 
