@@ -14,7 +14,8 @@
 
 namespace dali {
 
-constexpr int kRouteThreads = 256;
+// threads per CTA are a template parameter: 256 for token batches, up to
+// 1024 when one CTA carries a single decode token (more d-slices in flight)
 // tokens per CTA (TB <= warps per CTA) is a template parameter: 8 for long
 // prompts, fewer when T is small so the grid still covers the SMs.
 // hidden chunk staged per iteration: as much of the CTA's rows as fits the
@@ -25,7 +26,7 @@ constexpr int kRouteThreads = 256;
 constexpr int kRouteStageBytes = 64 * 1024;
 template <int TB> constexpr int route_ch() { return kRouteStageBytes / (8 * TB); }
 
-template <typename TH, typename TW, int kRouteTB>
+template <typename TH, typename TW, int kRouteTB, int kRouteThreads>
 __global__ void __launch_bounds__(kRouteThreads)
 route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
              const TW* __restrict__ gate, int64_t T, int d, int N, int k,
@@ -56,14 +57,27 @@ route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
   for (int c0 = 0; c0 < d; c0 += kRouteCH) {
     const int cn = min(kRouteCH, d - c0);
     __syncthreads();
-    for (int idx = tid; idx < kRouteTB * kRouteCH; idx += kRouteThreads) {
-      const int tb = idx / kRouteCH, i = idx % kRouteCH;
-      double v = 0.0;
-      if (tb < tb_n && i < cn) {
-        v = to_f64(hidden[(t0 + tb) * (int64_t)d + c0 + i]);
-        if (residual) v = __dadd_rn(v, residual[c0 + i]);
+    // stage the chunk: batches of 8 independent loads per thread so the
+    // global-load latency is paid once per batch, not once per element
+    constexpr int kBatch = 8;
+    const int n_el = kRouteTB * kRouteCH;
+    for (int base = tid; base < n_el; base += kRouteThreads * kBatch) {
+      double v[kBatch];
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) {
+        const int idx = base + q * kRouteThreads;
+        const int tb = idx / kRouteCH, i = idx % kRouteCH;
+        v[q] = 0.0;
+        if (idx < n_el && tb < tb_n && i < cn) {
+          v[q] = to_f64(hidden[(t0 + tb) * (int64_t)d + c0 + i]);
+          if (residual) v[q] = __dadd_rn(v[q], residual[c0 + i]);
+        }
       }
-      sh_h[tb][i] = v;
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q) {
+        const int idx = base + q * kRouteThreads;
+        if (idx < n_el) sh_h[idx / kRouteCH][idx % kRouteCH] = v[q];
+      }
     }
     __syncthreads();
     if (active) {
@@ -162,31 +176,40 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
     DALI_LAUNCH_CHECK("zero_i64");
   }
   if (T == 0) return DALI_OK;
-  const int S = kRouteThreads / N;
   DALI_REQUIRE((T + 1) / 2 < (1ll << 31), DALI_ETRACE, "too many tokens");
   // dynamic smem = staged hidden rows (64 KB) + partial logits (TB*N*S doubles)
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(route_kernel<TH, TW, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRouteStageBytes + 8 * 8 * kRouteThreads);
-    cudaFuncSetAttribute(route_kernel<TH, TW, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRouteStageBytes + 8 * 4 * kRouteThreads);
-    cudaFuncSetAttribute(route_kernel<TH, TW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRouteStageBytes + 8 * 2 * kRouteThreads);
+    cudaFuncSetAttribute(route_kernel<TH, TW, 8, 256>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRouteStageBytes + 8 * 8 * 256);
+    cudaFuncSetAttribute(route_kernel<TH, TW, 4, 256>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRouteStageBytes + 8 * 4 * 256);
+    cudaFuncSetAttribute(route_kernel<TH, TW, 2, 512>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRouteStageBytes + 8 * 2 * 512);
+    cudaFuncSetAttribute(route_kernel<TH, TW, 1, 1024>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRouteStageBytes + 8 * 1 * 1024);
     attr_set = true;
   }
   auto* ul = reinterpret_cast<unsigned long long*>(workloads);
   if (T >= 8 * 148) {
-    route_kernel<TH, TW, 8><<<(unsigned)((T + 7) / 8), kRouteThreads,
-                              kRouteStageBytes + sizeof(double) * 8 * N * S, st>>>(
+    route_kernel<TH, TW, 8, 256><<<(unsigned)((T + 7) / 8), 256,
+                                   kRouteStageBytes + sizeof(double) * 8 * N * (256 / N), st>>>(
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   } else if (T >= 4 * 148) {
-    route_kernel<TH, TW, 4><<<(unsigned)((T + 3) / 4), kRouteThreads,
-                              kRouteStageBytes + sizeof(double) * 4 * N * S, st>>>(
+    route_kernel<TH, TW, 4, 256><<<(unsigned)((T + 3) / 4), 256,
+                                   kRouteStageBytes + sizeof(double) * 4 * N * (256 / N), st>>>(
+        hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
+  } else if (T > 1) {
+    route_kernel<TH, TW, 2, 512><<<(unsigned)((T + 1) / 2), 512,
+                                   kRouteStageBytes + sizeof(double) * 2 * N * (512 / N), st>>>(
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   } else {
-    route_kernel<TH, TW, 2><<<(unsigned)((T + 1) / 2), kRouteThreads,
-                              kRouteStageBytes + sizeof(double) * 2 * N * S, st>>>(
+    route_kernel<TH, TW, 1, 1024><<<1u, 1024,
+                                    kRouteStageBytes + sizeof(double) * N * (1024 / N), st>>>(
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   }
   DALI_LAUNCH_CHECK("route_kernel");

@@ -1,0 +1,41 @@
+"""Time the routing kernel at decode / prefill shapes (diagnostic, ncu target).
+
+    python tools/prof_route.py [--d 4096] [--N 8] [--k 2]
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_03495_b200.trace import route_device  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--d", type=int, default=4096)
+ap.add_argument("--N", type=int, default=8)
+ap.add_argument("--k", type=int, default=2)
+ap.add_argument("--iters", type=int, default=50)
+args = ap.parse_args()
+g = (torch.randn(args.d, args.N, device="cuda") * 0.02).to(torch.bfloat16)
+for T in (1, 4, 16, 128, 512, 4096):
+    h = torch.randn(T, args.d, device="cuda").to(torch.bfloat16)
+    for _ in range(3):
+        route_device(h, g, args.k)
+    torch.cuda.synchronize()
+    out = (torch.empty((T, args.k), dtype=torch.int32, device="cuda"),
+           torch.empty((T, args.k), dtype=torch.float32, device="cuda"),
+           torch.empty((args.N,), dtype=torch.int64, device="cuda"))
+    graph = torch.cuda.CUDAGraph()            # device time without host launch cost
+    with torch.cuda.graph(graph):
+        for _ in range(args.iters):
+            route_device(h, g, args.k, out=out)
+    graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    graph.replay()
+    e1.record()
+    e1.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / args.iters
+    print(f"T={T}: {us:.1f} us per call ({T * args.d * 2 / us / 1e3:.1f} GB/s hidden)")
