@@ -277,6 +277,10 @@ def run_dali(args, ws, rank, local):
                 toks, st = eng.generate(p, args.decode, host_io=host_io)
                 stats.append(st)
                 reps.append(eng.policy_report())
+                log(f"{'e2e' if host_io else 'value'} request: decode "
+                    f"{st.decode_tokens / max(st.decode_ms, 1e-9) * 1e3:.2f} tok/s, "
+                    f"{st.cpu_expert_calls} CPU / {st.gpu_expert_calls} GPU expert calls, "
+                    f"{st.demand_copies} demand copies, hit {reps[-1]['cache_hit_rate']}")
             e1.record(cs)
             torch.cuda.synchronize()
             torch.cuda.nvtx.range_pop()
