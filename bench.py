@@ -41,6 +41,19 @@ def log(*a):
     print("[bench]", *a, file=sys.stderr, flush=True)
 
 
+def ffn_traffic_ratio():
+    """DRAM bytes / algorithmic bytes of the expert FFN at the decode shapes
+    that dominate the launch list (1-2 GPU experts x 1 token), from the
+    committed ncu --set full capture (profiles/r01_ncu_ffn_traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_ffn_traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    r = [c["traffic_over_algorithmic"] for c in d["calls"] if c["shape"].startswith("1 token")]
+    return (float(np.mean(r)) if r else None), "profiles/r01_ncu_ffn_traffic.json"
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -320,6 +333,7 @@ def run_dali(args, ws, rank, local):
     avg_b = float(np.mean(byts)) if byts else None
     achieved = (avg_b / (avg_ms / 1e3) / 1e9) if durs else None
     total_ffn_ms = float(np.sum(durs)) if durs else 0.0
+    t_ratio, t_src = ffn_traffic_ratio()
     h2d_step = int(np.mean([args.batch * args.prefill * 8 for _ in st_e]))
     d2h_step = int(args.batch * 8 * args.decode)
 
@@ -360,7 +374,11 @@ def run_dali(args, ws, rank, local):
                          "achieved": round(achieved, 2) if achieved else None,
                          "peak": peak, "peak_kind": pk_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
-                         "traffic": None, "launches": len(durs),
+                         "traffic": (round(avg_b * t_ratio) if (avg_b and t_ratio) else None),
+                         "traffic_note": (f"algorithmic bytes x ncu-measured DRAM/algorithmic "
+                                          f"ratio {t_ratio:.4f} of the decode shapes ({t_src})"
+                                          if t_ratio else None),
+                         "launches": len(durs),
                          "avg_launch_ms": avg_ms, "algorithmic_bytes_per_launch": avg_b,
                          "share_of_step": round(total_ffn_ms / ms_v, 4) if ms_v else None},
             "clocks": clocks,
