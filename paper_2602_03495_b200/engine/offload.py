@@ -299,6 +299,28 @@ class OffloadEngine:
                             non_blocking=True)
         self.copy_stream.synchronize()
 
+    def reset_cache(self) -> None:
+        """Return the HBM expert cache to its seeded initial residency (the
+        state after construction): policy residency + slot table, host slot
+        mirror and slot contents.  Used to start measurement passes from the
+        same state so their decision sequences are identical."""
+        torch.cuda.synchronize()
+        pol = self.policy
+        L, N, cap = self.arch.num_layers, self.NL, self.slots_per_layer
+        on = pol.initial_on_gpu.astype(np.uint8)
+        slot = np.full((L, N), -1, np.int32)
+        if cap:
+            for l in range(L):
+                slot[l, np.flatnonzero(on[l])] = np.arange(cap) + l * cap
+        pol.on_gpu.copy_(torch.from_numpy(on))
+        pol.slot_of.copy_(torch.from_numpy(slot))
+        self.host_slot = slot.copy()
+        self.slot_ready = [None] * (L * cap)
+        for key in list(self.prefetched):
+            i, ev = self.prefetched.pop(key)
+            self.staging.release(i, ev)
+        self._load_initial_cache()
+
     def _host_block(self, l: int, e: int) -> torch.Tensor:
         off = self.w.expert_index(l, e) * self.w.expert_bytes
         return self.w.host.bytes[off:off + self.w.expert_bytes]

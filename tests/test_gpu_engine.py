@@ -523,3 +523,30 @@ def test_engine_baseline_policies(name, over):
         for s_, lg in enumerate(st.logits):
             ref = logits[0, S0 - 1 + s_]
             torch.testing.assert_close(lg[0], ref, rtol=RTOL, atol=RTOL * ref.abs().max().item())
+
+
+def test_reset_cache_reproduces_first_request():
+    """reset_cache() returns residency, slots and slot contents to the seeded
+    state: the same prompt then yields the same decisions and tokens."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    arch = preset("tiny")
+    w = ModelWeights(arch, seed=4)
+    res = np.random.default_rng(1).standard_normal((arch.num_layers - 1, arch.hidden_dim)) * 0.05
+    eng = OffloadEngine(arch, w, default_cost_model(non_moe_layer_time=3.0),
+                        EngineConfig(cache_slots_per_layer=2, prefetch_size=2, seed=3),
+                        residuals=res, max_seq=64)
+    prompt = torch.randint(0, arch.vocab_size, (1, 10), generator=torch.Generator().manual_seed(3))
+    t1, _ = eng.generate(prompt, 8)
+    d1 = eng.policy.decision_log()
+    eng.generate(torch.randint(0, arch.vocab_size, (1, 10)), 8)     # moves the cache
+    eng.reset_cache()
+    t2, _ = eng.generate(prompt, 8)
+    d2 = eng.policy.decision_log()
+    assert torch.equal(t1, t2)
+    assert len(d1) == len(d2)
+    for a_, b_ in zip(d1, d2):
+        assert np.array_equal(a_["G"], b_["G"]) and a_["hits"] == b_["hits"]
+        assert a_["event"] == b_["event"]
