@@ -382,6 +382,16 @@ int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
 int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f,
                     const uint16_t* x, int32_t R, float* y, int32_t nthreads);
 
+/* Asynchronous form for the engine: run experts i < n (block[i], rows x[i]
+ * (rows[i], d) bf16 -> y[i] (rows[i], d) f32, [host] pointers as uint64) on
+ * the worker pool from a dispatcher thread and return immediately, so the
+ * caller can dispatch the GPU side of the same layer; dali_cpu_expert_wait
+ * joins (returns the first failing status).  One submission in flight. */
+int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const uint64_t* xs,
+                           const int32_t* rows, const uint64_t* ys, int32_t d,
+                           int32_t f, int32_t nthreads);
+int dali_cpu_expert_wait(void);
+
 /* Deterministic counter-hash weight init (uniform, given std):
  * out[i] = bf16(std * sqrt(3) * (2*u(seed, offset+i) - 1)). */
 int dali_init_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed,

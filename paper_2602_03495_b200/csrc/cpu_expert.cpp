@@ -200,3 +200,102 @@ extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, cons
   });
   return DALI_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Asynchronous submission: one dispatcher thread runs a list of experts on the
+// pool while the caller (the engine's Python thread) dispatches the GPU side
+// of the same layer; dali_cpu_expert_wait joins.  One job in flight at a time.
+// ---------------------------------------------------------------------------
+namespace {
+struct CpuJob {
+  std::vector<const uint16_t*> blocks;
+  std::vector<const uint16_t*> xs;
+  std::vector<int32_t> rows;
+  std::vector<float*> ys;
+  int32_t d = 0, f = 0, nthreads = 1;
+};
+
+class Dispatcher {
+ public:
+  Dispatcher() : th_([this] { loop(); }) {}
+  ~Dispatcher() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    th_.join();
+  }
+  int submit(CpuJob&& job) {
+    std::unique_lock<std::mutex> lk(m_);
+    if (busy_) return DALI_ESIM;            // previous job not joined
+    job_ = std::move(job);
+    busy_ = true;
+    rc_ = DALI_OK;
+    lk.unlock();
+    cv_.notify_all();
+    return DALI_OK;
+  }
+  int wait() {
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [this] { return !busy_; });
+    return rc_;
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      CpuJob job;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [this] { return stop_ || (busy_ && !running_); });
+        if (stop_) return;
+        running_ = true;
+        job = std::move(job_);
+      }
+      int rc = DALI_OK;
+      for (size_t i = 0; i < job.blocks.size() && rc == DALI_OK; ++i)
+        rc = dali_cpu_expert(job.blocks[i], job.d, job.f, job.xs[i], job.rows[i], job.ys[i],
+                             job.nthreads);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        rc_ = rc;
+        running_ = false;
+        busy_ = false;
+      }
+      done_.notify_all();
+    }
+  }
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  CpuJob job_;
+  bool busy_ = false, running_ = false, stop_ = false;
+  int rc_ = DALI_OK;
+  std::thread th_;
+};
+
+Dispatcher& dispatcher() {
+  static Dispatcher d;
+  return d;
+}
+}  // namespace
+
+extern "C" int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const uint64_t* xs,
+                                      const int32_t* rows, const uint64_t* ys, int32_t d,
+                                      int32_t f, int32_t nthreads) {
+  if (n < 0 || (n > 0 && (!blocks || !xs || !rows || !ys)) || d % 32 || f % 64)
+    return DALI_ETRACE;
+  CpuJob job;
+  job.d = d;
+  job.f = f;
+  job.nthreads = nthreads;
+  for (int i = 0; i < n; ++i) {
+    job.blocks.push_back(reinterpret_cast<const uint16_t*>(blocks[i]));
+    job.xs.push_back(reinterpret_cast<const uint16_t*>(xs[i]));
+    job.rows.push_back(rows[i]);
+    job.ys.push_back(reinterpret_cast<float*>(ys[i]));
+  }
+  return dispatcher().submit(std::move(job));
+}
+
+extern "C" int dali_cpu_expert_wait(void) { return dispatcher().wait(); }

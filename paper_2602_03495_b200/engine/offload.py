@@ -41,7 +41,7 @@ from ..errors import SimulationError
 from ..policy_engine import PolicyEngine
 from ..trace import route_device
 from .arch import MoEArch
-from .cpu_worker import cpu_expert_rows
+from .cpu_worker import NATIVE_MAX_ROWS, cpu_expert_rows
 from .layers import KVCache, Rope, attention, rms_norm
 from .weights import ModelWeights
 
@@ -186,6 +186,11 @@ class OffloadEngine:
         self.staging = _Staging(n_stage, weights.expert_bytes, self.dev) if n_stage else None
         self.prefetched: dict = {}          # (layer, expert) -> (staging idx, event)
         self.cpu_threads = cfg.cpu_threads or len(os.sched_getaffinity(0))
+        # asynchronous CPU experts (dispatcher thread) measured ~12% slower per
+        # decode token on the 16-vCPU boxes: the Python thread's GPU dispatch
+        # preempts a pool thread and the pool's phase barrier waits for it.
+        # Off by default; DALI_CPU_ASYNC=1 enables it.
+        self._cpu_async = os.environ.get("DALI_CPU_ASYNC", "0") == "1"
         torch.set_num_threads(self.cpu_threads)
         # per-layer pinned scratch for pointer table + G mask
         row = (N * 17 + 63) // 64 * 64        # ptrs | maps | G mask, 64-B aligned rows
@@ -556,31 +561,67 @@ class OffloadEngine:
             self.stats.insert_copies += 1
         return kept
 
-    def _cpu_rows(self, l: int, rows_host: torch.Tensor, offs_np: np.ndarray, rec,
-                  R: int) -> torch.Tensor | None:
-        """CPU-assigned experts on the host worker: SwiGLU of each expert's
-        contiguous rows over the pinned store -> (R, d) f32 on the device
-        (rows of GPU experts are left unused)."""
-        a = self.arch
-        d, f = a.hidden_dim, a.ffn_dim
+    def _cpu_submit(self, l: int, rows_host: torch.Tensor, offs_np: np.ndarray, rec, R: int):
+        """Start the CPU-assigned experts on the host worker: decode-sized
+        experts (<= NATIVE_MAX_ROWS rows) go to the native pool asynchronously
+        (``dali_cpu_expert_submit``) so the caller dispatches the GPU side of
+        the layer meanwhile; prefill-sized ones are returned for the oneDNN
+        path.  Returns the job description for ``_cpu_finish``."""
         Cx = [e for e in range(self.NL) if rec.C[e]]
         if not Cx or R == 0:
             return None
+        d = self.arch.hidden_dim
         out = self._ws("cpu_rows_h", (R, d), torch.float32, pinned=True)
+        native, big = [], []
         lo, hi = R, 0
         for e in Cx:
             r0, r1 = int(offs_np[e]), int(offs_np[e + 1])
             if r1 <= r0:
                 continue
-            cpu_expert_rows(self._host_block(l, e).view(torch.bfloat16), rows_host[r0:r1], d,
-                            f, self.cpu_threads, out=out[r0:r1])
+            (native if r1 - r0 <= NATIVE_MAX_ROWS else big).append((e, r0, r1))
             self.stats.cpu_expert_calls += 1
             lo, hi = min(lo, r0), max(hi, r1)
+        if native and not self._cpu_async:          # synchronous (A/B switch)
+            for e, r0, r1 in native:
+                cpu_expert_rows(self._host_block(l, e).view(torch.bfloat16),
+                                rows_host[r0:r1], d, self.arch.ffn_dim, self.cpu_threads,
+                                out=out[r0:r1])
+            native = []
+        if native:
+            n = len(native)
+            blocks = np.array([self.w.expert_host_ptr(l, e) for e, _, _ in native], np.uint64)
+            xs = np.array([rows_host[r0].data_ptr() for _, r0, _ in native], np.uint64)
+            rows = np.array([r1 - r0 for _, r0, r1 in native], np.int32)
+            ys = np.array([out[r0].data_ptr() for _, r0, _ in native], np.uint64)
+            _lib.call("dali_cpu_expert_submit", n, blocks.ctypes.data, xs.ctypes.data,
+                      rows.ctypes.data, ys.ctypes.data, d, self.arch.ffn_dim, self.cpu_threads)
+        return dict(out=out, native=bool(native), big=big, lo=lo, hi=hi, l=l, rows=rows_host)
+
+    def _cpu_finish(self, job, R: int) -> torch.Tensor | None:
+        """Run the prefill-sized CPU experts, join the asynchronous ones and
+        move the CPU rows to the device (kernel copy: no copy-engine queueing)."""
+        if job is None:
+            return None
+        a = self.arch
+        d, f = a.hidden_dim, a.ffn_dim
+        out = job["out"]
+        for e, r0, r1 in job["big"]:
+            cpu_expert_rows(self._host_block(job["l"], e).view(torch.bfloat16),
+                            job["rows"][r0:r1], d, f, self.cpu_threads, out=out[r0:r1])
+        if job["native"]:
+            _lib.call("dali_cpu_expert_wait")
         dev_rows = self._ws("cpu_rows_d", (R, d), torch.float32)
-        if hi > lo:      # only the CPU experts' rows; kernel copy (no copy-engine queueing)
+        lo, hi = job["lo"], job["hi"]
+        if hi > lo:
             _lib.call("dali_copy_mapped", dev_rows[lo].data_ptr(), out[lo].data_ptr(),
                       (hi - lo) * d * 4, torch.cuda.current_stream().cuda_stream)
         return dev_rows
+
+    def _cpu_rows(self, l: int, rows_host: torch.Tensor, offs_np: np.ndarray, rec,
+                  R: int) -> torch.Tensor | None:
+        """CPU-assigned experts on the host worker, synchronously -> (R, d)
+        f32 on the device (rows of GPU experts are left unused)."""
+        return self._cpu_finish(self._cpu_submit(l, rows_host, offs_np, rec, R), R)
 
     def _moe(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, token_index: int,
              is_eos: bool) -> torch.Tensor:
@@ -656,11 +697,18 @@ class OffloadEngine:
         if self.cfg.capture:
             self.stats.captured.append((step, l, views["h_host"].clone()))
             self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
-        yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
-        # shared expert(s): queued before the host starts the CPU experts
-        y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+        # CPU experts are submitted first; with DALI_CPU_ASYNC=1 they run while
+        # this thread dispatches the GPU experts and copies of the same layer
+        job = self._cpu_submit(l, xp_host, hv["offsets"].numpy(), rec, R)
+        try:
+            yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
+            y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+        except BaseException:
+            if job is not None and job["native"]:
+                _lib.load().dali_cpu_expert_wait()     # never leave a job in flight
+            raise
         tp3 = time.perf_counter()
-        cpu_rows = self._cpu_rows(l, xp_host, hv["offsets"].numpy(), rec, R)
+        cpu_rows = self._cpu_finish(job, R)
         tp4 = time.perf_counter()
         self._acct(tp0, tp1, tp2, tp3, tp4)
         _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
