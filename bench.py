@@ -77,13 +77,35 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        # in-process NVML (same counters as nvidia-smi) so sampling does not fork
+        # a process every 250 ms and preempt the CPU-expert worker threads
+        nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            hdl = nv.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            nv = None
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                if nv is not None:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(hdl)
+                    act = lambda bit: "Active" if r & bit else "Not Active"  # noqa: E731
+                    self.rows.append([
+                        str(nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)),
+                        str(nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM)),
+                        act(nv.nvmlClocksEventReasonHwSlowdown),
+                        act(nv.nvmlClocksEventReasonHwThermalSlowdown),
+                        act(nv.nvmlClocksEventReasonSwThermalSlowdown),
+                        act(nv.nvmlClocksEventReasonSwPowerCap),
+                        str(nv.nvmlDeviceGetUtilizationRates(hdl).gpu)])
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([c.strip() for c in out.split(",")])
             except Exception:
                 pass
             self._stop.wait(0.25)

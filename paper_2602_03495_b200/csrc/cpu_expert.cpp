@@ -47,52 +47,58 @@ class Pool {
   ~Pool() {
     {
       std::lock_guard<std::mutex> g(m_);
-      stop_ = true;
-      ++gen_;
+      stop_.store(true, std::memory_order_release);
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     for (auto& t : th_) t.join();
   }
   int size() const { return n_; }
-  // run fn(tid) on every thread (caller is tid 0), return when all finished
+  // run fn(tid) on every thread (caller is tid 0), return when all finished.
+  // Workers spin briefly on the generation counter before sleeping, so the
+  // two phases of an expert and back-to-back experts of a layer start without
+  // a futex wake-up; the caller spins on the completion count.
   void run(const std::function<void(int)>& fn) {
+    fn_ = &fn;
+    pending_.store(n_ - 1, std::memory_order_relaxed);
     {
       std::lock_guard<std::mutex> g(m_);
-      fn_ = &fn;
-      pending_ = n_ - 1;
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     fn(0);
-    std::unique_lock<std::mutex> lk(m_);
-    done_.wait(lk, [this] { return pending_ == 0; });
+    while (pending_.load(std::memory_order_acquire) != 0) _mm_pause();
   }
 
  private:
   void loop(int tid) {
-    uint64_t seen = 0;
+    uint64_t seen = 0;           // generation at construction (a run may precede this thread)
     for (;;) {
-      const std::function<void(int)>* fn;
-      {
-        std::unique_lock<std::mutex> lk(m_);
-        cv_.wait(lk, [&] { return gen_ != seen; });
-        seen = gen_;
-        if (stop_) return;
-        fn = fn_;
+      uint64_t g = gen_.load(std::memory_order_acquire);
+      for (int spin = 0; g == seen && spin < kSpin; ++spin) {
+        _mm_pause();
+        g = gen_.load(std::memory_order_acquire);
       }
-      (*fn)(tid);
-      std::lock_guard<std::mutex> g(m_);
-      if (--pending_ == 0) done_.notify_one();
+      if (g == seen) {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+        g = gen_.load(std::memory_order_acquire);
+      }
+      seen = g;
+      if (stop_.load(std::memory_order_acquire)) return;
+      (*fn_)(tid);
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
+  static constexpr int kSpin = 20000;      // ~50-100 us of pause loops
   int n_;
   std::vector<std::thread> th_;
   std::mutex m_;
-  std::condition_variable cv_, done_;
+  std::condition_variable cv_;
   const std::function<void(int)>* fn_ = nullptr;
-  uint64_t gen_ = 0;
-  int pending_ = 0;
-  bool stop_ = false;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> pending_{0};
+  std::atomic<bool> stop_{false};
 };
 
 Pool* pool_for(int n) {

@@ -700,6 +700,7 @@ class OffloadEngine:
         # CPU experts are submitted first; with DALI_CPU_ASYNC=1 they run while
         # this thread dispatches the GPU experts and copies of the same layer
         job = self._cpu_submit(l, xp_host, hv["offsets"].numpy(), rec, R)
+        tp_sub = time.perf_counter()
         try:
             yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
             y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
@@ -710,7 +711,10 @@ class OffloadEngine:
         tp3 = time.perf_counter()
         cpu_rows = self._cpu_finish(job, R)
         tp4 = time.perf_counter()
-        self._acct(tp0, tp1, tp2, tp3, tp4)
+        # synchronous CPU experts run inside _cpu_submit: account them as CPU time
+        t_disp = tp3 - tp_sub
+        t_cpu = (tp_sub - tp2) + (tp4 - tp3)
+        self._acct(tp0, tp1, tp2, tp2 + t_disp, tp2 + t_disp + t_cpu)
         _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
                   v["pos"].data_ptr(), v["wts"].data_ptr(), gmask_p,
                   cpu_rows.data_ptr() if cpu_rows is not None else None,
