@@ -14,6 +14,7 @@
 #include <condition_variable>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -90,7 +91,11 @@ class Pool {
       pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
-  static constexpr int kSpin = 20000;      // ~50-100 us of pause loops
+  // pause iterations before a worker sleeps (DALI_POOL_SPIN, default 20000)
+  const int kSpin = [] {
+    const char* v = getenv("DALI_POOL_SPIN");
+    return v ? atoi(v) : 20000;
+  }();
   int n_;
   std::vector<std::thread> th_;
   std::mutex m_;
