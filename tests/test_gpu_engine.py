@@ -550,3 +550,61 @@ def test_reset_cache_reproduces_first_request():
     for a_, b_ in zip(d1, d2):
         assert np.array_equal(a_["G"], b_["G"]) and a_["hits"] == b_["hits"]
         assert a_["event"] == b_["event"]
+
+
+def test_full_width_mixtral_layers_decisions_and_logits():
+    """BASELINE configs[1] widths (d 4096, f 14336, 8 experts top-2, GQA 32/8)
+    on 2 layers: fp64 gating of the bf16 gate inputs, every DALI decision
+    bit-exact against the oracle replay, logits within the bf16 tolerance of
+    the fp32 CPU model -- at the full expert size, offloaded with a 2-slot
+    cache, residual prefetch and the per-layer CUDA-graph decode."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import dataclasses
+
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    arch = dataclasses.replace(preset("mixtral-8x7b"), name="mixtral-2l", num_layers=2,
+                               vocab_size=2048)
+    L, N, k = arch.num_layers, arch.num_experts, arch.top_k
+    w = ModelWeights(arch, seed=12)
+    res = np.random.default_rng(5).standard_normal((L - 1, arch.hidden_dim)) * 0.01
+    cm = default_cost_model(non_moe_layer_time=3.0)
+    eng = OffloadEngine(arch, w, cm, EngineConfig(cache_slots_per_layer=2, prefetch_size=1,
+                                                  seed=3, capture=True),
+                        residuals=res, max_seq=128)
+    prompt = torch.randint(0, arch.vocab_size, (1, 48), generator=torch.Generator().manual_seed(2))
+    toks, st = eng.generate(prompt, 8)
+    by_step = {}
+    for (s, l, h) in st.captured:
+        by_step.setdefault(s, {})[l] = h.double().numpy()
+    steps = [D.StepInput(ti, ntok, np.stack([st.workloads[(s, l)] for l in range(L)]),
+                         np.stack([by_step[s][l] for l in range(L)]), eos)
+             for s, (ti, ntok, eos) in enumerate(st.steps_meta)]
+    gates = np.stack([w.router[l].double().cpu().numpy() for l in range(L)])
+    for s, step in enumerate(steps):
+        for l in range(L):
+            o_idx, _, o_wl = P.route(step.hidden[l], gates[l], k)
+            assert np.array_equal(o_wl, st.workloads[(s, l)]), (s, l)
+            assert np.array_equal(o_idx, st.topk[(s, l)]), (s, l)
+    dcfg = D.DriverConfig(tables=P.default_tables(non_moe_layer_time=3.0), prefetch_size=1,
+                          residuals=res, cache_capacity=2, w_size=4, u_size=1, seed=3,
+                          initial_on_gpu=st.initial_on_gpu)
+    _, recs = D.run(steps, gates, dcfg, L, N, k)
+    got = eng.policy.decision_log()
+    assert len(got) == len(recs)
+    for a_, o in zip(got, recs):
+        assert np.array_equal(a_["C"], o.C) and np.array_equal(a_["G"], o.G), (o.step, o.layer)
+        assert a_["hits"] == o.lookups and a_["event"] == o.event
+        if o.prefetch_set is not None:
+            assert a_["pset"] == o.prefetch_set.tolist() and a_["done"] == o.completed
+    assert st.cpu_expert_calls > 0 and st.gpu_expert_calls > 0
+    seq = torch.cat([prompt, toks[:, :-1]], dim=1)
+    overs = {l: torch.cat([torch.from_numpy(st.topk[(s, l)])
+                           for s in range(len(st.steps_meta))], 0) for l in range(L)}
+    logits, _ = M.forward(arch, M.dense_from_weights(w), lambda l_, e_: w.expert_host(l_, e_),
+                          seq, overs)
+    S0 = prompt.shape[1]
+    for s_, lg in enumerate(st.logits):
+        ref = logits[0, S0 - 1 + s_]
+        torch.testing.assert_close(lg[0], ref, rtol=RTOL, atol=RTOL * ref.abs().max().item())
