@@ -13,6 +13,7 @@ __global__ void rope_append_kernel(const uint16_t* __restrict__ qkv, const float
                                    const float* __restrict__ sin_t, const int32_t* __restrict__ pos_p,
                                    int H, int KV, int hd, int max_len, uint16_t* __restrict__ q_out,
                                    uint16_t* __restrict__ kc, uint16_t* __restrict__ vc) {
+  DALI_PDL_ENTRY();
   const int b = blockIdx.y;
   const int head = blockIdx.x;                 // 0..H+2KV-1
   const int pos = *pos_p;
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 decode_attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ kc,
                    const uint16_t* __restrict__ vc, const int32_t* __restrict__ len_p, int H,
                    int KV, int max_len, float scale, float* __restrict__ ws) {
+  DALI_PDL_ENTRY();
   constexpr int EL = HD / 32;
   const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int kvh = h / (H / KV);
@@ -126,6 +128,7 @@ decode_attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ 
 template <int HD>
 __global__ void attn_merge_kernel(const float* __restrict__ ws, int nsplit,
                                   uint16_t* __restrict__ o) {
+  DALI_PDL_ENTRY();
   const int bh = blockIdx.x;
   const float* in = ws + (int64_t)bh * nsplit * (HD + 2);
   float M = -INFINITY;
@@ -149,7 +152,7 @@ extern "C" int dali_rope_append(const uint16_t* qkv, const float* cos_t, const f
                                 int32_t max_len, uint16_t* q_out, uint16_t* k_cache,
                                 uint16_t* v_cache, void* stream) {
   DALI_REQUIRE(hd % 2 == 0 && H % KV == 0, DALI_ETRACE, "bad attention geometry");
-  dali::rope_append_kernel<<<dim3(H + 2 * KV, B), 64, 0, dali::as_stream(stream)>>>(
+  dali::launch_pdl(dali::rope_append_kernel, dim3(dim3(H + 2 * KV, B)), dim3(64), 0, dali::as_stream(stream), 
       qkv, cos_t, sin_t, pos, H, KV, hd, max_len, q_out, k_cache, v_cache);
   DALI_LAUNCH_CHECK("rope_append_kernel");
   return DALI_OK;
@@ -165,15 +168,15 @@ extern "C" int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
   DALI_REQUIRE(H % KV == 0 && splits >= 1, DALI_ETRACE, "bad attention geometry");
   cudaStream_t st = dali::as_stream(stream);
   if (hd == 128) {
-    dali::decode_attn_kernel<128><<<dim3(B * H, splits), dali::kAttnWarps * 32, 0, st>>>(
+    dali::launch_pdl(dali::decode_attn_kernel<128>, dim3(dim3(B * H, splits)), dim3(dali::kAttnWarps * 32), 0, st, 
         q, k_cache, v_cache, len, H, KV, max_len, scale, workspace);
     DALI_LAUNCH_CHECK("decode_attn_kernel");
-    dali::attn_merge_kernel<128><<<B * H, 128, 0, st>>>(workspace, splits, out);
+    dali::launch_pdl(dali::attn_merge_kernel<128>, dim3(B * H), dim3(128), 0, st, workspace, splits, out);
   } else {
-    dali::decode_attn_kernel<64><<<dim3(B * H, splits), dali::kAttnWarps * 32, 0, st>>>(
+    dali::launch_pdl(dali::decode_attn_kernel<64>, dim3(dim3(B * H, splits)), dim3(dali::kAttnWarps * 32), 0, st, 
         q, k_cache, v_cache, len, H, KV, max_len, scale, workspace);
     DALI_LAUNCH_CHECK("decode_attn_kernel");
-    dali::attn_merge_kernel<64><<<B * H, 64, 0, st>>>(workspace, splits, out);
+    dali::launch_pdl(dali::attn_merge_kernel<64>, dim3(B * H), dim3(64), 0, st, workspace, splits, out);
   }
   DALI_LAUNCH_CHECK("attn_merge_kernel");
   return DALI_OK;

@@ -36,6 +36,33 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
     }                                                                        \
   } while (0)
 
+// Programmatic dependent launch (PDL).  Decode-path kernels are launched
+// with programmatic stream serialisation (launch_pdl): the next kernel's CTAs
+// are scheduled while this one runs and block in griddepcontrol.wait until it
+// has completed and flushed, which hides the kernel-to-kernel launch gap
+// inside the per-step CUDA graphs.  Every such kernel starts with
+// DALI_PDL_ENTRY(): wait for the predecessor (no-op without PDL), then allow
+// the successor to launch.  Nothing is read or written before the wait.
+#define DALI_PDL_ENTRY()                                                     \
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" :: \
+                   : "memory")
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ double bf16_bits_to_f64(uint16_t b) {
   return (double)__uint_as_float(((uint32_t)b) << 16);
 }

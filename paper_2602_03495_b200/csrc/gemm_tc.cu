@@ -144,6 +144,9 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap b_map, const int32_t* __restri
               const uint64_t* __restrict__ a_maps, int N, int K, int m_tiles, int splits,
               int out_ld, uint16_t* __restrict__ H, float* __restrict__ Y, int64_t y_plane) {
   using S = Smem<BN>;
+  // the up projection is PDL-launched behind the routing / plan kernels: its
+  // tile list (offsets, expert maps) is only valid after the wait
+  if (MODE == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
   Tile t;
   if (!find_tile<BN>(offs, a_maps, N, m_tiles, splits, t, blockIdx.x)) return;
   const void* a_map = reinterpret_cast<const void*>(a_maps[t.e] + (MODE == 0 ? 0 : 128));
@@ -498,8 +501,8 @@ static int launch_bn(const int32_t* offs, const uint64_t* maps, int N, int d, in
   const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;   // sum_e ceil(n_e / BN) <= this
   const int m_up = (2 * f) / BM, m_dn = d / BM;
   const int64_t g_up = ntile_bound * m_up;
-  ffn_tc_kernel<BN, 0><<<(unsigned)g_up, kThreads, S::BYTES, st>>>(
-      xmap, offs, maps, N, d, m_up, 1, f, hbuf, nullptr, 0);
+  launch_pdl(ffn_tc_kernel<BN, 0>, dim3((unsigned)g_up), dim3(kThreads), S::BYTES, st, xmap, offs,
+             maps, N, d, m_up, 1, f, hbuf, (float*)nullptr, (int64_t)0);
   DALI_LAUNCH_CHECK("ffn_tc_kernel<up>");
   const int64_t g_dn = ntile_bound * m_dn * splits;
   cudaLaunchAttribute pdl[1];

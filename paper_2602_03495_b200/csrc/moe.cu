@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(kPlanWarps * 32)
 plan_kernel(const int32_t* __restrict__ topk_idx, int64_t pairs, int k, int N,
             int32_t* __restrict__ offsets, int32_t* __restrict__ perm_token,
             int32_t* __restrict__ pos) {
+  DALI_PDL_ENTRY();
   __shared__ int cnt[kPlanWarps][DALI_MAX_EXPERTS];
   __shared__ int tot[DALI_MAX_EXPERTS + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -79,6 +80,7 @@ plan_kernel(const int32_t* __restrict__ topk_idx, int64_t pairs, int k, int N,
 // ---------------------------------------------------------------------------
 __global__ void permute_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ perm,
                                int64_t rows, int d8, uint4* __restrict__ out) {
+  DALI_PDL_ENTRY();
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -202,6 +204,7 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
                                const float* __restrict__ cpu_rows,
                                const float* __restrict__ extra, int64_t T, int k, int d,
                                int splits, int64_t plane, uint16_t* __restrict__ out) {
+  DALI_PDL_ENTRY();
   // one thread per (token, 8-column chunk): all of a row's chunks load their
   // k x splits partial rows concurrently (decode: T=1 is latency-bound)
   const int d8 = d >> 3;
@@ -300,7 +303,7 @@ extern "C" int dali_moe_plan(const int32_t* topk_idx, int64_t T, int32_t k, int3
                              int32_t* offsets, int32_t* perm_token, int32_t* pos, void* stream) {
   DALI_REQUIRE(N >= 1 && N <= DALI_MAX_EXPERTS, DALI_ETRACE, "expert count %d", N);
   DALI_REQUIRE(T >= 0 && k >= 1 && T * k < (1ll << 31), DALI_ETRACE, "bad plan shape");
-  plan_kernel<<<1, kPlanWarps * 32, 0, as_stream(stream)>>>(topk_idx, T * k, k, N, offsets,
+  launch_pdl(plan_kernel, dim3(1), dim3(kPlanWarps * 32), 0, as_stream(stream), topk_idx, T * k, k, N, offsets,
                                                             perm_token, pos);
   DALI_LAUNCH_CHECK("plan_kernel");
   return DALI_OK;
@@ -311,7 +314,7 @@ extern "C" int dali_permute(const uint16_t* x, const int32_t* perm_token, int64_
   DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
   if (rows <= 0) return DALI_OK;
   const int64_t blocks = std::min<int64_t>((rows + 7) / 8, (int64_t)sm_count() * 8);
-  permute_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+  launch_pdl(permute_kernel, dim3((unsigned)blocks), dim3(256), 0, as_stream(stream), 
       reinterpret_cast<const uint4*>(x), perm_token, rows, d / 8, reinterpret_cast<uint4*>(out));
   DALI_LAUNCH_CHECK("permute_kernel");
   return DALI_OK;
@@ -338,7 +341,7 @@ extern "C" int dali_unpermute_combine(const uint16_t* x, const float* yp, const 
   DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
   if (T <= 0) return DALI_OK;
   const int64_t blocks = std::min<int64_t>((T * (d / 8) + 255) / 256, (int64_t)sm_count() * 8);
-  combine_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(x, yp, topk_idx, pos, topk_w,
+  launch_pdl(combine_kernel, dim3((unsigned)blocks), dim3(256), 0, as_stream(stream), x, yp, topk_idx, pos, topk_w,
                                                                   gpu_mask, cpu_rows, extra, T, k,
                                                                   d,
                                                                   splits < 1 ? 1 : splits,
@@ -357,6 +360,7 @@ namespace dali {
 __global__ void copy_mapped_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
                                    int64_t n16, uint8_t* __restrict__ dst_tail,
                                    const uint8_t* __restrict__ src_tail, int tail) {
+  DALI_PDL_ENTRY();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
     dst[i] = src[i];
@@ -385,7 +389,7 @@ extern "C" int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void
   const int tail = (int)(nbytes & 15);
   const int64_t blocks =
       std::max<int64_t>(1, std::min<int64_t>((n16 + 255) / 256, (int64_t)sm_count() * 4));
-  copy_mapped_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+  launch_pdl(copy_mapped_kernel, dim3((unsigned)blocks), dim3(256), 0, as_stream(stream), 
       reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), n16,
       reinterpret_cast<uint8_t*>(dst) + n16 * 16, reinterpret_cast<const uint8_t*>(src) + n16 * 16,
       tail);
@@ -421,6 +425,7 @@ namespace dali {
 __global__ void add_rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ a,
                                    const uint16_t* __restrict__ w, float eps, int d,
                                    uint16_t* __restrict__ x_out, uint16_t* __restrict__ h) {
+  DALI_PDL_ENTRY();
   const int64_t row = blockIdx.x;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * d);
   const uint4* ar = a ? reinterpret_cast<const uint4*>(a + row * d) : nullptr;
@@ -496,7 +501,7 @@ extern "C" int dali_add_rmsnorm(const uint16_t* x, const uint16_t* a, const uint
                                 void* stream) {
   DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
   if (T <= 0) return DALI_OK;
-  dali::add_rmsnorm_kernel<<<(unsigned)T, 256, 0, dali::as_stream(stream)>>>(x, a, w, eps, d, x_out,
+  launch_pdl(dali::add_rmsnorm_kernel, dim3((unsigned)T), dim3(256), 0, dali::as_stream(stream), x, a, w, eps, d, x_out,
                                                                              h);
   DALI_LAUNCH_CHECK("add_rmsnorm_kernel");
   return DALI_OK;

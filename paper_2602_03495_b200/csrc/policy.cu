@@ -559,6 +559,7 @@ policy_layer_kernel(dali_policy_config cfg, dali_cost_model cm, int step, int la
                     int32_t* slot_of_all, int64_t* lru_all,
                     const double* __restrict__ gate_probs, int n_tokens,
                     dali_layer_record* rec, const int32_t* __restrict__ desc) {
+  DALI_PDL_ENTRY();
   __shared__ PolShared s;
   __shared__ SolverScratch scratch;
   __shared__ int sh_nins;
@@ -918,7 +919,7 @@ extern "C" int dali_policy_layer(const dali_policy_config* cfg, const dali_cost_
   DALI_REQUIRE(cfg->N >= 1 && cfg->N <= DALI_MAX_EXPERTS, DALI_ESIM, "expert count %d", cfg->N);
   DALI_REQUIRE(layer >= 0 && layer < cfg->L, DALI_ESIM, "layer %d out of range", layer);
   DALI_REQUIRE(!cfg->cache_enabled || cfg->u_size <= DALI_MAX_EXPERTS, DALI_ESIM, "u_size");
-  dali::policy_layer_kernel<<<1, dali::kPolThreads, 0, dali::as_stream(stream)>>>(
+  dali::launch_pdl(dali::policy_layer_kernel, dim3(1), dim3(dali::kPolThreads), 0, dali::as_stream(stream), 
       *cfg, *cm, step, layer, token_index, is_eos, workloads, predicted, on_gpu, scores,
       counters, arrived, slot_of, lru_state, gate_probs, n_tokens, rec, nullptr);
   DALI_LAUNCH_CHECK("policy_layer_kernel");
@@ -937,7 +938,7 @@ extern "C" int dali_policy_layer_desc(const dali_policy_config* cfg, const dali_
   DALI_REQUIRE(dali::valid_baselines(cfg, lru_state, gate_probs), DALI_ESIM,
                "baseline policy configuration needs its state");
   DALI_REQUIRE(layer >= 0 && layer < cfg->L, DALI_ESIM, "layer %d out of range", layer);
-  dali::policy_layer_kernel<<<1, dali::kPolThreads, 0, dali::as_stream(stream)>>>(
+  dali::launch_pdl(dali::policy_layer_kernel, dim3(1), dim3(dali::kPolThreads), 0, dali::as_stream(stream), 
       *cfg, *cm, 0, layer, 0, 0, workloads, predicted, on_gpu, scores, counters, arrived,
       slot_of, lru_state, gate_probs, n_tokens, rec_base, desc);
   DALI_LAUNCH_CHECK("policy_layer_kernel(desc)");
@@ -946,6 +947,7 @@ extern "C" int dali_policy_layer_desc(const dali_policy_config* cfg, const dali_
 
 namespace dali {
 __global__ void step_advance_kernel(int32_t* desc) {
+  DALI_PDL_ENTRY();
   desc[0] += 1;            // step
   desc[1] += 1;            // token_index
   desc[3] += desc[6];      // record_index += L
@@ -955,7 +957,7 @@ __global__ void step_advance_kernel(int32_t* desc) {
 }  // namespace dali
 
 extern "C" int dali_step_advance(int32_t* desc, void* stream) {
-  dali::step_advance_kernel<<<1, 1, 0, dali::as_stream(stream)>>>(desc);
+  dali::launch_pdl(dali::step_advance_kernel, dim3(1), dim3(1), 0, dali::as_stream(stream), desc);
   DALI_LAUNCH_CHECK("step_advance_kernel");
   return DALI_OK;
 }

@@ -32,6 +32,7 @@ route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
              const TW* __restrict__ gate, int64_t T, int d, int N, int k,
              int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
              unsigned long long* __restrict__ workloads, double* __restrict__ probs) {
+  DALI_PDL_ENTRY();
   constexpr int kRouteCH = route_ch<kRouteTB>();
   __shared__ double sh_red[kRouteTB * DALI_MAX_EXPERTS];   // logits, then probs
   __shared__ int sh_hist[DALI_MAX_EXPERTS];
@@ -154,6 +155,7 @@ route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
 }
 
 __global__ void zero_i64(int64_t* p, int n) {
+  DALI_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = 0;
 }
@@ -172,7 +174,7 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
                "workloads output required");
   cudaStream_t st = as_stream(stream);
   if (workloads) {
-    zero_i64<<<(N + 255) / 256, 256, 0, st>>>(workloads, N);
+    launch_pdl(zero_i64, dim3((N + 255) / 256), dim3(256), 0, st, workloads, N);
     DALI_LAUNCH_CHECK("zero_i64");
   }
   if (T == 0) return DALI_OK;
@@ -196,20 +198,16 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
   }
   auto* ul = reinterpret_cast<unsigned long long*>(workloads);
   if (T >= 8 * 148) {
-    route_kernel<TH, TW, 8, 256><<<(unsigned)((T + 7) / 8), 256,
-                                   kRouteStageBytes + sizeof(double) * 8 * N * (256 / N), st>>>(
+    launch_pdl(route_kernel<TH, TW, 8, 256>, dim3((unsigned)((T + 7) / 8)), dim3(256), kRouteStageBytes + sizeof(double) * 8 * N * (256 / N), st, 
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   } else if (T >= 4 * 148) {
-    route_kernel<TH, TW, 4, 256><<<(unsigned)((T + 3) / 4), 256,
-                                   kRouteStageBytes + sizeof(double) * 4 * N * (256 / N), st>>>(
+    launch_pdl(route_kernel<TH, TW, 4, 256>, dim3((unsigned)((T + 3) / 4)), dim3(256), kRouteStageBytes + sizeof(double) * 4 * N * (256 / N), st, 
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   } else if (T > 1) {
-    route_kernel<TH, TW, 2, 512><<<(unsigned)((T + 1) / 2), 512,
-                                   kRouteStageBytes + sizeof(double) * 2 * N * (512 / N), st>>>(
+    launch_pdl(route_kernel<TH, TW, 2, 512>, dim3((unsigned)((T + 1) / 2)), dim3(512), kRouteStageBytes + sizeof(double) * 2 * N * (512 / N), st, 
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   } else {
-    route_kernel<TH, TW, 1, 1024><<<1u, 1024,
-                                    kRouteStageBytes + sizeof(double) * N * (1024 / N), st>>>(
+    launch_pdl(route_kernel<TH, TW, 1, 1024>, dim3(1u), dim3(1024), kRouteStageBytes + sizeof(double) * N * (1024 / N), st, 
         hidden, residual, gate, T, d, N, k, renorm, topk_idx, topk_w, ul, probs);
   }
   DALI_LAUNCH_CHECK("route_kernel");
