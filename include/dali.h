@@ -288,6 +288,13 @@ int dali_moe_plan(const int32_t* topk_idx, int64_t T, int32_t k, int32_t N,
                   int32_t* offsets, int32_t* perm_token, int32_t* pos,
                   void* stream);
 
+/* dali_moe_plan followed by dali_permute; decode-sized batches (T*k <= 64)
+ * do both in one single-CTA launch.  x (T, d) bf16 [dev] -> xp (T*k, d). */
+int dali_moe_plan_permute(const int32_t* topk_idx, int64_t T, int32_t k, int32_t N,
+                          const uint16_t* x, int32_t d, int32_t* offsets,
+                          int32_t* perm_token, int32_t* pos, uint16_t* xp,
+                          void* stream);
+
 /* Coalesced 128-bit gather: out[r,:] = x[perm_token[r],:]  (bf16, d % 8 == 0) */
 int dali_permute(const uint16_t* x, const int32_t* perm_token, int64_t rows,
                  int32_t d, uint16_t* out, void* stream);

@@ -88,6 +88,7 @@ SIGNATURES = {
     "dali_gate_probs_bf16": [_P, _P, _I64, _I32, _I32, _P, _P],
     "dali_moe_plan": [_P, _I64, _I32, _I32, _P, _P, _P, _P],
     "dali_permute": [_P, _P, _I64, _I32, _P, _P],
+    "dali_moe_plan_permute": [_P, _I64, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P],
     "dali_expert_ffn": [_P, _P, _I32, _P, _I32, _I32, _I64, _I32, _P, _P, _P],
     "dali_expert_ffn_simt": [_P, _P, _I32, _P, _I32, _I32, _P, _P, _P],
     "dali_unpermute_combine": [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I64, _P,

@@ -21,11 +21,16 @@ namespace dali {
 // by expert.  One CTA of 32 warps; each warp owns a contiguous segment.
 // ---------------------------------------------------------------------------
 constexpr int kPlanWarps = 32;
+constexpr int kPlanGatherMax = 64;    // fused plan+gather up to 64 (token, slot) rows
 
+// GATHER: decode-sized batches also gather the permuted rows in the same CTA
+// (saves the permute launch): xp[r,:] = x[perm_token[r],:].
+template <bool GATHER>
 __global__ void __launch_bounds__(kPlanWarps * 32)
 plan_kernel(const int32_t* __restrict__ topk_idx, int64_t pairs, int k, int N,
             int32_t* __restrict__ offsets, int32_t* __restrict__ perm_token,
-            int32_t* __restrict__ pos) {
+            int32_t* __restrict__ pos, const uint4* __restrict__ x, int d8,
+            uint4* __restrict__ xp) {
   DALI_PDL_ENTRY();
   __shared__ int cnt[kPlanWarps][DALI_MAX_EXPERTS];
   __shared__ int tot[DALI_MAX_EXPERTS + 1];
@@ -72,6 +77,14 @@ plan_kernel(const int32_t* __restrict__ topk_idx, int64_t pairs, int k, int N,
       if (rank == 0) cnt[warp][e] += __popc(peers);
     }
     __syncwarp();
+  }
+  if (GATHER) {
+    __syncthreads();                       // perm_token written by this CTA
+    for (int64_t r = warp; r < pairs; r += kPlanWarps) {
+      const uint4* src = x + (int64_t)perm_token[r] * d8;
+      uint4* dst = xp + r * d8;
+      for (int c = lane; c < d8; c += 32) dst[c] = __ldg(src + c);
+    }
   }
 }
 
@@ -303,9 +316,27 @@ extern "C" int dali_moe_plan(const int32_t* topk_idx, int64_t T, int32_t k, int3
                              int32_t* offsets, int32_t* perm_token, int32_t* pos, void* stream) {
   DALI_REQUIRE(N >= 1 && N <= DALI_MAX_EXPERTS, DALI_ETRACE, "expert count %d", N);
   DALI_REQUIRE(T >= 0 && k >= 1 && T * k < (1ll << 31), DALI_ETRACE, "bad plan shape");
-  launch_pdl(plan_kernel, dim3(1), dim3(kPlanWarps * 32), 0, as_stream(stream), topk_idx, T * k, k, N, offsets,
-                                                            perm_token, pos);
+launch_pdl(plan_kernel<false>, dim3(1), dim3(kPlanWarps * 32), 0, as_stream(stream), topk_idx,
+             T * k, k, N, offsets, perm_token, pos, (const uint4*)nullptr, 0, (uint4*)nullptr);
   DALI_LAUNCH_CHECK("plan_kernel");
+  return DALI_OK;
+}
+
+extern "C" int dali_moe_plan_permute(const int32_t* topk_idx, int64_t T, int32_t k, int32_t N,
+                                     const uint16_t* x, int32_t d, int32_t* offsets,
+                                     int32_t* perm_token, int32_t* pos, uint16_t* xp,
+                                     void* stream) {
+  DALI_REQUIRE(N >= 1 && N <= DALI_MAX_EXPERTS, DALI_ETRACE, "expert count %d", N);
+  DALI_REQUIRE(T >= 0 && k >= 1 && T * k < (1ll << 31), DALI_ETRACE, "bad plan shape");
+  DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
+  if (T * k > kPlanGatherMax) {
+    int rc = dali_moe_plan(topk_idx, T, k, N, offsets, perm_token, pos, stream);
+    return rc ? rc : dali_permute(x, perm_token, T * k, d, xp, stream);
+  }
+  launch_pdl(plan_kernel<true>, dim3(1), dim3(kPlanWarps * 32), 0, as_stream(stream), topk_idx,
+             T * k, k, N, offsets, perm_token, pos, reinterpret_cast<const uint4*>(x), d / 8,
+             reinterpret_cast<uint4*>(xp));
+  DALI_LAUNCH_CHECK("plan_kernel<gather>");
   return DALI_OK;
 }
 

@@ -149,9 +149,15 @@ route_kernel(const TH* __restrict__ hidden, const double* __restrict__ residual,
     }
   }
   __syncthreads();
-  if (workloads)
-    for (int i = tid; i < N; i += kRouteThreads)
-      if (sh_hist[i]) atomicAdd(workloads + i, (unsigned long long)sh_hist[i]);
+  if (workloads) {
+    if (gridDim.x == 1) {          // single CTA: the histogram is the result (no zeroing pass)
+      for (int i = tid; i < N; i += kRouteThreads)
+        workloads[i] = (unsigned long long)sh_hist[i];
+    } else {
+      for (int i = tid; i < N; i += kRouteThreads)
+        if (sh_hist[i]) atomicAdd(workloads + i, (unsigned long long)sh_hist[i]);
+    }
+  }
 }
 
 __global__ void zero_i64(int64_t* p, int n) {
@@ -173,7 +179,7 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
   DALI_REQUIRE(workloads != nullptr || probs != nullptr, DALI_ETRACE,
                "workloads output required");
   cudaStream_t st = as_stream(stream);
-  if (workloads) {
+  if (workloads && (T > 2 || T == 0)) {   // 1 <= T <= 2: one CTA writes the histogram
     launch_pdl(zero_i64, dim3((N + 255) / 256), dim3(256), 0, st, workloads, N);
     DALI_LAUNCH_CHECK("zero_i64");
   }

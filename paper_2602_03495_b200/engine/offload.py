@@ -367,11 +367,10 @@ class OffloadEngine:
                      out=(v["idx"], v["wts"], v["wl"]))
         perm = self._ws("perm", (T * k,), torch.int32)
         v["pos"] = self._ws("pos", (T, k), torch.int32)
-        _lib.call("dali_moe_plan", v["idx"].data_ptr(), T, k, N, v["offsets"].data_ptr(),
-                  perm.data_ptr(), v["pos"].data_ptr(), cs.cuda_stream)
         v["xp"] = self._ws("xp", (T * k, d), torch.bfloat16)
-        _lib.call("dali_permute", h.data_ptr(), perm.data_ptr(), T * k, d, v["xp"].data_ptr(),
-                  cs.cuda_stream)
+        _lib.call("dali_moe_plan_permute", v["idx"].data_ptr(), T, k, N, h.data_ptr(), d,
+                  v["offsets"].data_ptr(), perm.data_ptr(), v["pos"].data_ptr(),
+                  v["xp"].data_ptr(), cs.cuda_stream)
         v["blk"], v["layout"] = rblk, (o_off, o_idx, o_w, nb)
         return v
 
