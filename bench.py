@@ -382,6 +382,14 @@ def run_dali(args, ws, rank, local):
             "policy_virtual_clock_tokens_per_s": float(np.mean([r["tokens_per_second"]
                                                                 for r in rep_v])),
             "pcie_h2d_bytes_per_step": int(np.mean([s.h2d_bytes for s in st_v])),
+            # expert transfers: one block H2D from the pinned store, timed by the
+            # warm-up profiler on this box (cost model trans_time), vs the link
+            "h2d_expert_copy": ({"gbs": round(eng.w.expert_bytes / (eng.cm.trans_time / 1e3)
+                                              / 1e9, 2),
+                                 "block_bytes": int(eng.w.expert_bytes),
+                                 "ms_per_block": eng.cm.trans_time,
+                                 "link": "PCIe Gen5 x16 (64 GB/s nominal per direction)"}
+                                if eng.cm.trans_time > 0 else None),
             "copies_per_step": {k: float(np.mean([getattr(s, k) for s in st_v])) for k in
                                 ("demand_copies", "prefetch_copies", "replace_copies")},
             "host_ms_per_step": {k: round(float(np.mean([s.host_ms.get(k, 0.0) for s in st_v])), 2)
