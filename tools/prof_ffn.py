@@ -23,6 +23,7 @@ ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--kernel", default="tc")
 ap.add_argument("--d", type=int, default=4096)
 ap.add_argument("--f", type=int, default=14336)
+ap.add_argument("--splits", type=int, default=0, help="override the split-K planes")
 args = ap.parse_args()
 d, f, N = args.d, args.f, 8
 dev = torch.device("cuda")
@@ -51,7 +52,7 @@ def run(counts, label):
     mr = max(counts)
     bn = 16 if mr <= 16 else 32 if mr <= 32 else 64 if mr <= 64 else 128 if mr <= 128 else 256
     tiles = sum((c + bn - 1) // bn for c in counts if c) * (d // 128)
-    splits = ffn_splits(mr, tiles, f // 64, nsm)
+    splits = args.splits or ffn_splits(mr, tiles, f // 64, nsm)
     y = torch.empty(splits, rows, d, dtype=torch.float32, device=dev)
     cs = torch.cuda.current_stream().cuda_stream
 
