@@ -552,26 +552,31 @@ def test_reset_cache_reproduces_first_request():
         assert a_["event"] == b_["event"]
 
 
-def test_full_width_mixtral_layers_decisions_and_logits():
-    """BASELINE configs[1] widths (d 4096, f 14336, 8 experts top-2, GQA 32/8)
-    on 2 layers: fp64 gating of the bf16 gate inputs, every DALI decision
-    bit-exact against the oracle replay, logits within the bf16 tolerance of
-    the fp32 CPU model -- at the full expert size, offloaded with a 2-slot
-    cache, residual prefetch and the per-layer CUDA-graph decode."""
+@pytest.mark.parametrize("name,slots,psize", [("mixtral-8x7b", 2, 1),
+                                              ("deepseek-v2-lite", 24, 4),
+                                              ("qwen1.5-moe-a2.7b", 24, 4)])
+def test_full_width_layers_decisions_and_logits(name, slots, psize):
+    """BASELINE configs widths on 2 layers -- Mixtral-8x7B (d 4096, f 14336,
+    8 experts top-2), DeepSeek-V2-Lite (64 routed top-6 + 2 shared) and
+    Qwen1.5-MoE (60 routed top-4 + gated shared): fp64 gating of the bf16
+    gate inputs, every DALI decision bit-exact against the oracle replay,
+    logits within the bf16 tolerance of the fp32 CPU model -- at the full
+    expert size, offloaded with a capped cache, residual prefetch and the
+    per-layer CUDA-graph decode."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import dataclasses
 
     from paper_2602_03495_b200.cost_model import default_cost_model
     from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
-    arch = dataclasses.replace(preset("mixtral-8x7b"), name="mixtral-2l", num_layers=2,
-                               vocab_size=2048)
+    arch = dataclasses.replace(preset(name), name=name + "-2l", num_layers=2, vocab_size=2048)
     L, N, k = arch.num_layers, arch.num_experts, arch.top_k
     w = ModelWeights(arch, seed=12)
     res = np.random.default_rng(5).standard_normal((L - 1, arch.hidden_dim)) * 0.01
-    cm = default_cost_model(non_moe_layer_time=3.0)
-    eng = OffloadEngine(arch, w, cm, EngineConfig(cache_slots_per_layer=2, prefetch_size=1,
-                                                  seed=3, capture=True),
+    shared = 0.5 if arch.num_shared_experts else 0.0
+    cm = default_cost_model(shared_expert_gpu_time=shared, non_moe_layer_time=3.0)
+    eng = OffloadEngine(arch, w, cm, EngineConfig(cache_slots_per_layer=slots,
+                                                  prefetch_size=psize, seed=3, capture=True),
                         residuals=res, max_seq=128)
     prompt = torch.randint(0, arch.vocab_size, (1, 48), generator=torch.Generator().manual_seed(2))
     toks, st = eng.generate(prompt, 8)
@@ -587,9 +592,10 @@ def test_full_width_mixtral_layers_decisions_and_logits():
             o_idx, _, o_wl = P.route(step.hidden[l], gates[l], k)
             assert np.array_equal(o_wl, st.workloads[(s, l)]), (s, l)
             assert np.array_equal(o_idx, st.topk[(s, l)]), (s, l)
-    dcfg = D.DriverConfig(tables=P.default_tables(non_moe_layer_time=3.0), prefetch_size=1,
-                          residuals=res, cache_capacity=2, w_size=4, u_size=1, seed=3,
-                          initial_on_gpu=st.initial_on_gpu)
+    dcfg = D.DriverConfig(tables=P.default_tables(shared, non_moe_layer_time=3.0),
+                          prefetch_size=psize, residuals=res, cache_capacity=slots, w_size=4,
+                          u_size=eng.cfg.u_size, seed=3, initial_on_gpu=st.initial_on_gpu,
+                          num_shared_experts=arch.num_shared_experts)
     _, recs = D.run(steps, gates, dcfg, L, N, k)
     got = eng.policy.decision_log()
     assert len(got) == len(recs)
