@@ -696,24 +696,29 @@ class OffloadEngine:
         if self.cfg.capture:
             self.stats.captured.append((step, l, views["h_host"].clone()))
             self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
-        # CPU experts are submitted first; with DALI_CPU_ASYNC=1 they run while
-        # this thread dispatches the GPU experts and copies of the same layer
-        job = self._cpu_submit(l, xp_host, hv["offsets"].numpy(), rec, R)
-        tp_sub = time.perf_counter()
-        try:
+        offs_np = hv["offsets"].numpy()
+        if self._cpu_async:
+            # the CPU experts start first and run on the pool while this thread
+            # dispatches the GPU experts and copies of the same layer
+            job = self._cpu_submit(l, xp_host, offs_np, rec, R)
+            try:
+                yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
+                y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+            except BaseException:
+                if job is not None and job["native"]:
+                    _lib.load().dali_cpu_expert_wait()     # never leave a job in flight
+                raise
+            tp3 = time.perf_counter()
+        else:
+            # GPU work is queued first (it runs during the CPU experts), then the
+            # CPU experts run on this thread's pool
             yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
             y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
-        except BaseException:
-            if job is not None and job["native"]:
-                _lib.load().dali_cpu_expert_wait()     # never leave a job in flight
-            raise
-        tp3 = time.perf_counter()
+            tp3 = time.perf_counter()
+            job = self._cpu_submit(l, xp_host, offs_np, rec, R)
         cpu_rows = self._cpu_finish(job, R)
         tp4 = time.perf_counter()
-        # synchronous CPU experts run inside _cpu_submit: account them as CPU time
-        t_disp = tp3 - tp_sub
-        t_cpu = (tp_sub - tp2) + (tp4 - tp3)
-        self._acct(tp0, tp1, tp2, tp2 + t_disp, tp2 + t_disp + t_cpu)
+        self._acct(tp0, tp1, tp2, tp3, tp4)
         _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
                   v["pos"].data_ptr(), v["wts"].data_ptr(), gmask_p,
                   cpu_rows.data_ptr() if cpu_rows is not None else None,
