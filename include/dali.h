@@ -357,6 +357,13 @@ int dali_unpermute_combine(const uint16_t* x, const float* yp,
  * path; unaligned copies are byte-wise and limited to 1 MiB. */
 int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream);
 
+/* Shared expert(s) finish (engine plumbing): out[t,:] = sum over `splits`
+ * planes of ys (splits, T, d) f32, times sigmoid(h[t,:] . gate_w) when
+ * gate_w (d,) bf16 is given (Qwen-style gated shared expert), else 1.
+ * h (T, d) bf16; out (T, d) f32 [dev]. */
+int dali_shared_finish(const float* ys, int32_t splits, int64_t T, int32_t d,
+                       const uint16_t* h, const uint16_t* gate_w, float* out, void* stream);
+
 /* Engine plumbing: fused residual add + RMSNorm over (T, d) bf16 rows:
  *   x_out = x + a (a may be NULL: x_out untouched, x used as is);
  *   h = bf16(bf16(x_out * rsqrt(mean(x_out^2) + eps)) * w). */

@@ -428,6 +428,54 @@ extern "C" int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void
   return DALI_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Shared-expert finish: out[t,:] = (sum_s ys[s,t,:]) * gate(t), gate(t) =
+// sigmoid(h[t,:] . g) for Qwen's gated shared expert (1 when g == NULL).
+// One CTA per token: replaces a plane sum + fp32 cast + GEMV + sigmoid + mul.
+// ---------------------------------------------------------------------------
+namespace dali {
+__global__ void shared_finish_kernel(const float* __restrict__ ys, int splits, int64_t plane,
+                                     const uint16_t* __restrict__ h,
+                                     const uint16_t* __restrict__ g, int d,
+                                     float* __restrict__ out) {
+  DALI_PDL_ENTRY();
+  const int64_t t = blockIdx.x;
+  __shared__ float red[32];
+  float gate = 1.0f;
+  if (g) {
+    float acc = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x)
+      acc += bf16_bits_to_f32(h[t * d + i]) * bf16_bits_to_f32(g[i]);
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) red[0] = 1.0f / (1.0f + __expf(-v));
+    }
+    __syncthreads();
+    gate = red[0];
+  }
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float v = ys[t * d + i];
+    for (int s = 1; s < splits; ++s) v += ys[s * plane + t * d + i];
+    out[t * d + i] = v * gate;
+  }
+}
+}  // namespace dali
+
+extern "C" int dali_shared_finish(const float* ys, int32_t splits, int64_t T, int32_t d,
+                                  const uint16_t* h, const uint16_t* gate_w, float* out,
+                                  void* stream) {
+  if (T <= 0) return DALI_OK;
+  DALI_REQUIRE(splits >= 1, DALI_ETRACE, "splits must be >= 1");
+  launch_pdl(shared_finish_kernel, dim3((unsigned)T), dim3(256), 0, as_stream(stream), ys,
+             splits, T * (int64_t)d, h, gate_w, d, out);
+  DALI_LAUNCH_CHECK("shared_finish_kernel");
+  return DALI_OK;
+}
+
 extern "C" int dali_init_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, uint64_t offset,
                                       float stdev, void* stream) {
   if (n <= 0) return DALI_OK;

@@ -225,6 +225,8 @@ class OffloadEngine:
         self._heads: dict = {}              # offloaded decode: layer -> (graph, h, views)
         self._heads_warm = False
         self._in_capture = False
+        self._capturing = False
+        self._cs_cached = None
         self._eos_at = -1
         self._pending_ffn, self._pending_cap = [], []
         self._used_fast = False
@@ -263,14 +265,23 @@ class OffloadEngine:
         sp = ffn_splits(T, tiles, kb, self.n_sm)
         hs = self._ws("sh_h", (T, fs), torch.bfloat16)
         ys = self._ws("sh_y", (sp, T, d), torch.float32)
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         _lib.call("dali_expert_ffn_tc", h.data_ptr(), offs.data_ptr(), 1,
                   self.shared_map_ptr.data_ptr() + 8 * l, d, fs, T, T, 1, hs.data_ptr(),
                   ys.data_ptr(), sp, cs.cuda_stream)
-        y = ys.sum(0) if sp > 1 else ys[0]
-        if a.shared_gate:
-            y = y * torch.sigmoid(h.float() @ self.w.shared_gate[l].float().t())
+        y = self._ws("sh_out", (T, d), torch.float32)
+        _lib.call("dali_shared_finish", ys.data_ptr(), sp, T, d, h.data_ptr(),
+                  self.w.shared_gate[l].data_ptr() if a.shared_gate else None, y.data_ptr(),
+                  cs.cuda_stream)
         return y
+
+    def _cur(self):
+        """The compute stream.  torch.cuda.current_stream() costs ~15 us of
+        Python per call, so it is looked up once per prefill / decode step and
+        cached; during graph capture the (capture) stream is read live."""
+        if self._capturing or self._cs_cached is None:
+            return torch.cuda.current_stream()
+        return self._cs_cached
 
     def _ws(self, name: str, shape: tuple, dtype, pinned: bool = False) -> torch.Tensor:
         """Per-engine workspace reused across layers/steps (stream-ordered on
@@ -351,7 +362,7 @@ class OffloadEngine:
         a = self.arch
         N, k, d = a.num_experts, a.top_k, a.hidden_dim
         T = h.shape[0]
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         o_off = N * 8
         o_idx = o_off + ((N + 1) * 4 + 7) // 8 * 8
         o_w = o_idx + T * k * 4
@@ -396,7 +407,7 @@ class OffloadEngine:
         (yp planes, splits, G mask device pointer)."""
         a = self.arch
         NL, d, f = self.NL, a.hidden_dim, a.ffn_dim
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         G = [e for e in range(NL) if rec.G[e]]
         ptrs = np.zeros(NL, dtype=np.uint64)
         maps = np.zeros(NL, dtype=np.uint64)
@@ -613,7 +624,7 @@ class OffloadEngine:
         lo, hi = job["lo"], job["hi"]
         if hi > lo:
             _lib.call("dali_copy_mapped", dev_rows[lo].data_ptr(), out[lo].data_ptr(),
-                      (hi - lo) * d * 4, torch.cuda.current_stream().cuda_stream)
+                      (hi - lo) * d * 4, self._cur().cuda_stream)
         return dev_rows
 
     def _cpu_rows(self, l: int, rows_host: torch.Tensor, offs_np: np.ndarray, rec,
@@ -628,7 +639,7 @@ class OffloadEngine:
             return self._moe_ep(l, x, h, step, token_index, is_eos)
         if self.resident_mode and self.use_tc and self.cfg.resident_fast:
             return self._moe_resident(l, x, h, step, token_index, is_eos)
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         ev_r = None
         if self.cfg.trace_layers:
             ev_r = torch.cuda.Event(enable_timing=True)
@@ -648,7 +659,7 @@ class OffloadEngine:
         d, k = a.hidden_dim, a.top_k
         T = h.shape[0]
         R = T * k
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         v = self._route(l, h)
         gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
         if use_desc:
@@ -682,7 +693,7 @@ class OffloadEngine:
         N, k, d = a.num_experts, a.top_k, a.hidden_dim
         v, hv, xp_host, T = views["v"], views["hv"], views["xp_host"], views["T"]
         R = T * k
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         tr = self.cfg.trace_layers
         ri = views["ri"] if views["ri"] is not None else self.policy.n_records + l
         ev_dec = torch.cuda.Event(enable_timing=tr)
@@ -747,7 +758,7 @@ class OffloadEngine:
         N, k, d, f = a.num_experts, a.top_k, a.hidden_dim, a.ffn_dim
         T = h.shape[0]
         R = T * k
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         tp0 = time.perf_counter()
         v = self._route(l, h)
         if T == self.kv.k.shape[1] and self.stats.steps_meta:     # decode: device descriptor
@@ -840,7 +851,7 @@ class OffloadEngine:
         a, ep = self.arch, self.ep
         N, k, d, NL = a.num_experts, a.top_k, a.hidden_dim, self.NL
         T = h.shape[0]
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         tp0 = time.perf_counter()
         v = self._route(l, h)
         recv_counts = ep.exchange_counts(v["wl"])                  # (G*NL,) int64
@@ -918,7 +929,7 @@ class OffloadEngine:
         descriptor (graph-capturable), o-proj GEMM."""
         a, W = self.arch, self.w
         H, KV, hd = a.num_heads, a.num_kv_heads, a.head_dim
-        sp = torch.cuda.current_stream().cuda_stream
+        sp = self._cur().cuda_stream
         qkv = hn @ W.wqkv[l].t()
         q = self._ws("q_dec", (B, H, hd), torch.bfloat16)
         kc, vc = self.kv.k[l], self.kv.v[l]
@@ -938,7 +949,7 @@ class OffloadEngine:
         a, W = self.arch, self.w
         x = W.embed[tokens_dev.reshape(-1)]
         T, d = x.shape
-        sp = torch.cuda.current_stream().cuda_stream
+        sp = self._cur().cuda_stream
         hn = self._ws("hn", (T, d), torch.bfloat16)
         h = self._ws("h", (T, d), torch.bfloat16)
         dev_attn = S == 1 and a.head_dim in (64, 128)
@@ -969,7 +980,7 @@ class OffloadEngine:
         so the same launch sequence is valid for every step (graph body)."""
         a, W = self.arch, self.w
         d = a.hidden_dim
-        sp = torch.cuda.current_stream().cuda_stream
+        sp = self._cur().cuda_stream
         hn = self._ws("hn", (B, d), torch.bfloat16)
         h = self._ws("h", (B, d), torch.bfloat16)
         _lib.call("dali_add_rmsnorm", X.data_ptr(), None, W.attn_norm[l].data_ptr(), a.rms_eps,
@@ -987,7 +998,7 @@ class OffloadEngine:
         pinned memory by a kernel copy before the layers run."""
         a, W = self.arch, self.w
         L, d = a.num_layers, a.hidden_dim
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         step, pos = self._step, self.kv.len
         base = self.policy.n_records
         if base + L > self.policy.max_records:
@@ -1012,8 +1023,12 @@ class OffloadEngine:
                 g.replay()
             elif capture:
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    h, views = self._decode_head(l, X, X2, B)
+                self._capturing = True
+                try:
+                    with torch.cuda.graph(g):
+                        h, views = self._decode_head(l, X, X2, B)
+                finally:
+                    self._capturing = False
                 g.replay()
                 heads[l] = (g, h, views)
             else:
@@ -1030,7 +1045,7 @@ class OffloadEngine:
         dh.copy_(torch.tensor([step, token_index, eos_at, rec_index, pos, pos + 1,
                                self.arch.num_layers, 0], dtype=torch.int32))
         _lib.call("dali_copy_mapped", self.desc_dev.data_ptr(), dh.data_ptr(), 32,
-                  torch.cuda.current_stream().cuda_stream)
+                  self._cur().cuda_stream)
 
     def start_request(self, batch: int) -> np.ndarray:
         """New policy run for one request; cache residency carries over."""
@@ -1049,6 +1064,7 @@ class OffloadEngine:
         return init
 
     def prefill(self, prompt_dev: torch.Tensor, is_eos: bool = False) -> torch.Tensor:
+        self._cs_cached = torch.cuda.current_stream()
         B, S = prompt_dev.shape
         logits = self._forward(prompt_dev, B, S, 0, self._step, 0, is_eos)
         self.stats.steps_meta.append((0, B * S, is_eos))
@@ -1064,6 +1080,7 @@ class OffloadEngine:
                 not self.cfg.capture)
 
     def decode(self, tok_dev: torch.Tensor, is_eos: bool = False) -> torch.Tensor:
+        self._cs_cached = torch.cuda.current_stream()
         B = tok_dev.shape[0]
         pos = self.kv.len
         ti = self._step
@@ -1074,7 +1091,7 @@ class OffloadEngine:
         else:
             logits = self._forward(tok_dev.view(B, 1), B, 1, pos, self._step, ti, is_eos)
             _lib.call("dali_step_advance", self.desc_dev.data_ptr(),
-                      torch.cuda.current_stream().cuda_stream)
+                      self._cur().cuda_stream)
         self.stats.steps_meta.append((ti, B, is_eos))
         self._step += 1
         self.kv.len = pos + 1
@@ -1097,7 +1114,7 @@ class OffloadEngine:
             logits = self._forward(tok_dev.view(B, 1), B, 1, self.kv.len, self._step, self._step,
                                    False)
             _lib.call("dali_step_advance", self.desc_dev.data_ptr(),
-                      torch.cuda.current_stream().cuda_stream)
+                      self._cur().cuda_stream)
             self._graph_warm = True
             return logits
         self._graph_in = torch.zeros((B,), dtype=torch.int64, device=self.dev)
@@ -1108,11 +1125,13 @@ class OffloadEngine:
         self.cfg.time_ffn = False                 # no timing events inside the graph
         self._in_capture = True
         n0 = self.policy.n_records
+        self._capturing = True
         with torch.cuda.graph(g):
             out = self._forward(self._graph_in.view(B, 1), B, 1, 0, 0, 0, False)
             _lib.call("dali_step_advance", self.desc_dev.data_ptr(),
-                      torch.cuda.current_stream().cuda_stream)
+                      self._cur().cuda_stream)
         self._in_capture = False
+        self._capturing = False
         self.cfg.time_ffn = saved
         self.policy.n_records = n0
         self._graph, self._graph_logits = g, out
@@ -1129,9 +1148,10 @@ class OffloadEngine:
         host_io=False: ``prompt`` already in HBM and tokens stay on device.
         Returns (tokens (B, n) int64, stats)."""
         B, S = prompt.shape
+        self._cs_cached = torch.cuda.current_stream()
         self.start_request(B)
         l0 = _lib.launch_count()
-        cs = torch.cuda.current_stream()
+        cs = self._cur()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(cs)
         if host_io:
@@ -1147,7 +1167,7 @@ class OffloadEngine:
 
             def fetch(t, i):
                 _lib.call("dali_copy_mapped", toks_h[i].data_ptr(), t.data_ptr(), B * 8,
-                          torch.cuda.current_stream().cuda_stream)
+                          self._cur().cuda_stream)
                 ev = torch.cuda.Event()
                 ev.record()
                 ev.synchronize()
