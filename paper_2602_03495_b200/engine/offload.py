@@ -195,6 +195,7 @@ class OffloadEngine:
         # per-layer pinned scratch for pointer table + G mask
         row = (N * 17 + 63) // 64 * 64        # ptrs | maps | G mask, 64-B aligned rows
         self.ptr_host = torch.zeros((L, row), dtype=torch.uint8, pin_memory=True)
+        self._ptr_host_np = self.ptr_host.numpy()    # same pinned memory
         self.ptr_dev = torch.zeros((L, row), dtype=torch.uint8, device=self.dev)
         self.rope = Rope(a, max_seq, self.dev)
         self.max_batch, self.max_seq = max_batch, max_seq
@@ -408,9 +409,16 @@ class OffloadEngine:
         a = self.arch
         NL, d, f = self.NL, a.hidden_dim, a.ffn_dim
         cs = self._cur()
-        G = [e for e in range(NL) if rec.G[e]]
-        ptrs = np.zeros(NL, dtype=np.uint64)
-        maps = np.zeros(NL, dtype=np.uint64)
+        g_np = np.frombuffer(rec.G, dtype=np.int8, count=NL)
+        G = np.flatnonzero(g_np).tolist()
+        # numpy views of this layer's pinned row: ptrs | maps | G mask
+        ph = self.ptr_host[l]
+        row = self._ptr_host_np[l]
+        ptrs = row[:NL * 8].view(np.uint64)
+        maps = row[NL * 8:NL * 16].view(np.uint64)
+        ptrs[:] = 0
+        maps[:] = 0
+        row[NL * 16:NL * 17] = g_np.view(np.uint8)
         waits = []
         used_staging = []
         n_hit = n_pf = n_dem = 0
@@ -441,21 +449,17 @@ class OffloadEngine:
             waits.append(ev)
             used_staging.append(i)
             stage_of[e] = i
-        ph = self.ptr_host[l]
-        ph[:NL * 8].view(torch.int64).copy_(torch.from_numpy(ptrs.view(np.int64)))
-        ph[NL * 8:NL * 16].view(torch.int64).copy_(torch.from_numpy(maps.view(np.int64)))
-        gm = np.array(rec.G[:NL], dtype=np.int8)
-        ph[NL * 16:NL * 17].copy_(torch.from_numpy(gm.view(np.uint8)))
         pd = self.ptr_dev[l]
         # kernel copy from mapped pinned memory: never queues behind expert DMA
         _lib.call("dali_copy_mapped", pd.data_ptr(), ph.data_ptr(), ph.numel(), cs.cuda_stream)
         splits = 1
         max_rows = 0
         if G and self.use_tc:
-            max_rows = int(max(wl_np[e] for e in G))
+            wg = wl_np[G]
+            max_rows = int(wg.max())
             bn = 16 if max_rows <= 16 else 32 if max_rows <= 32 else 64 if max_rows <= 64 \
                 else 128 if max_rows <= 128 else 256
-            tiles = sum((int(wl_np[e]) + bn - 1) // bn for e in G) * (d // 128)
+            tiles = int(((wg + bn - 1) // bn).sum()) * (d // 128)
             splits = self._splits_for(tiles, max_rows)
         yp = self._ws("yp", (splits, max(R, 1), d), torch.float32)
         if G and R > 0:
@@ -577,7 +581,7 @@ class OffloadEngine:
         (``dali_cpu_expert_submit``) so the caller dispatches the GPU side of
         the layer meanwhile; prefill-sized ones are returned for the oneDNN
         path.  Returns the job description for ``_cpu_finish``."""
-        Cx = [e for e in range(self.NL) if rec.C[e]]
+        Cx = np.flatnonzero(np.frombuffer(rec.C, dtype=np.int8, count=self.NL)).tolist()
         if not Cx or R == 0:
             return None
         d = self.arch.hidden_dim
