@@ -423,7 +423,7 @@ def run_dali(args, ws, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dali", choices=["dali", "reference"])
     ap.add_argument("--model", default="mixtral-8x7b")
