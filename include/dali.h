@@ -364,6 +364,12 @@ int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream);
 int dali_shared_finish(const float* ys, int32_t splits, int64_t T, int32_t d,
                        const uint16_t* h, const uint16_t* gate_w, float* out, void* stream);
 
+/* Decode GEMV (engine plumbing, attention projections): y (B, M) bf16 =
+ * x (B, K) bf16 . W^T with W (M, K) bf16 row-major, 1 <= B <= 8, K % 8 == 0;
+ * fp32 accumulation, weight-streaming (one warp per output row). */
+int dali_gemv_bf16(const uint16_t* x, const uint16_t* w, int32_t B, int32_t M, int32_t K,
+                   uint16_t* y, void* stream);
+
 /* Engine plumbing: fused residual add + RMSNorm over (T, d) bf16 rows:
  *   x_out = x + a (a may be NULL: x_out untouched, x used as is);
  *   h = bf16(bf16(x_out * rsqrt(mean(x_out^2) + eps)) * w). */

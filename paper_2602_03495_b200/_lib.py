@@ -110,6 +110,7 @@ SIGNATURES = {
     "dali_add_rmsnorm": [_P, _P, _P, C.c_float, _I64, _I32, _P, _P, _P],
     "dali_copy_mapped": [_P, _P, _I64, _P],
     "dali_shared_finish": [_P, _I32, _I64, _I32, _P, _P, _P, _P],
+    "dali_gemv_bf16": [_P, _P, _I32, _I32, _I32, _P, _P],
     "dali_host_alloc_shared": [C.c_size_t, _I32, _I32, C.POINTER(C.c_int32), _I32,
                                C.POINTER(C.c_void_p)],
 }

@@ -476,6 +476,88 @@ extern "C" int dali_shared_finish(const float* ys, int32_t splits, int64_t T, in
   return DALI_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Decode GEMV: y (B, M) bf16 = x (B, K) bf16 . W (M, K)^T, B <= 8 tokens.
+// Weight streaming: one warp per output row, 16-byte loads (8 bf16 per lane
+// per step, 8 steps in flight), x staged in shared memory, fp32 accumulation.
+// ---------------------------------------------------------------------------
+namespace dali {
+constexpr int kGemvWarps = 8;
+constexpr int kGemvMaxB = 8;
+
+template <int B>
+__global__ void __launch_bounds__(kGemvWarps * 32)
+gemv_bf16_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int M, int K,
+                 uint16_t* __restrict__ y) {
+  DALI_PDL_ENTRY();
+  extern __shared__ uint4 sx[];                       // B x K bf16
+  const int k8 = K >> 3;
+  for (int i = threadIdx.x; i < B * k8; i += blockDim.x) sx[i] = reinterpret_cast<const uint4*>(x)[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.x * kGemvWarps + warp;
+  if (m >= M) return;
+  const uint4* wr = reinterpret_cast<const uint4*>(w + (int64_t)m * K);
+  float acc[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) acc[b] = 0.f;
+#pragma unroll 4
+  for (int c = lane; c < k8; c += 32) {
+    const uint4 wv = __ldg(wr + c);
+    const uint32_t* ww = reinterpret_cast<const uint32_t*>(&wv);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const uint4 xv = sx[b * k8 + c];
+      const uint32_t* xx = reinterpret_cast<const uint32_t*>(&xv);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[b] = fmaf(__uint_as_float(ww[q] << 16), __uint_as_float(xx[q] << 16), acc[b]);
+        acc[b] = fmaf(__uint_as_float(ww[q] & 0xffff0000u), __uint_as_float(xx[q] & 0xffff0000u),
+                      acc[b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    float v = acc[b];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) y[(int64_t)b * M + m] = f32_to_bf16_bits(v);
+  }
+}
+}  // namespace dali
+
+extern "C" int dali_gemv_bf16(const uint16_t* x, const uint16_t* w, int32_t Bt, int32_t M,
+                              int32_t K, uint16_t* y, void* stream) {
+  DALI_REQUIRE(Bt >= 1 && Bt <= dali::kGemvMaxB, DALI_ETRACE, "gemv batch %d outside [1, %d]",
+               Bt, dali::kGemvMaxB);
+  DALI_REQUIRE(K % 8 == 0 && M >= 1, DALI_ETRACE, "gemv needs K %% 8 == 0 (K=%d)", K);
+  const size_t smem = (size_t)Bt * K * 2;
+  DALI_REQUIRE(smem <= 200 * 1024, DALI_ETRACE, "gemv activations exceed shared memory");
+  const dim3 grid((unsigned)((M + dali::kGemvWarps - 1) / dali::kGemvWarps));
+  const dim3 block(dali::kGemvWarps * 32);
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaSuccess;
+  switch (Bt) {
+#define DALI_GEMV_CASE(BB)                                                                  \
+  case BB: {                                                                                \
+    static bool attr = false;                                                              \
+    if (!attr) {                                                                           \
+      cudaFuncSetAttribute(dali::gemv_bf16_kernel<BB>,                                     \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);       \
+      attr = true;                                                                         \
+    }                                                                                      \
+    e = launch_pdl(dali::gemv_bf16_kernel<BB>, grid, block, smem, st, x, w, M, K, y);      \
+    break;                                                                                 \
+  }
+    DALI_GEMV_CASE(1) DALI_GEMV_CASE(2) DALI_GEMV_CASE(3) DALI_GEMV_CASE(4)
+    DALI_GEMV_CASE(5) DALI_GEMV_CASE(6) DALI_GEMV_CASE(7) DALI_GEMV_CASE(8)
+#undef DALI_GEMV_CASE
+  }
+  (void)e;
+  DALI_LAUNCH_CHECK("gemv_bf16_kernel");
+  return DALI_OK;
+}
+
 extern "C" int dali_init_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, uint64_t offset,
                                       float stdev, void* stream) {
   if (n <= 0) return DALI_OK;

@@ -934,7 +934,13 @@ class OffloadEngine:
         a, W = self.arch, self.w
         H, KV, hd = a.num_heads, a.num_kv_heads, a.head_dim
         sp = self._cur().cuda_stream
-        qkv = hn @ W.wqkv[l].t()
+        nqkv = (H + 2 * KV) * hd
+        if B <= 8:          # weight-streaming GEMV kernel (decode batches)
+            qkv = self._ws("qkv_dec", (B, nqkv), torch.bfloat16)
+            _lib.call("dali_gemv_bf16", hn.data_ptr(), W.wqkv[l].data_ptr(), B, nqkv,
+                      a.hidden_dim, qkv.data_ptr(), sp)
+        else:
+            qkv = hn @ W.wqkv[l].t()
         q = self._ws("q_dec", (B, H, hd), torch.bfloat16)
         kc, vc = self.kv.k[l], self.kv.v[l]
         _lib.call("dali_rope_append", qkv.data_ptr(), self.rope.cos.data_ptr(),
@@ -946,6 +952,11 @@ class OffloadEngine:
         _lib.call("dali_decode_attention", q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
                   self.desc_dev.data_ptr() + 20, B, H, KV, hd, self.max_seq, splits,
                   1.0 / math.sqrt(hd), ws.data_ptr(), o.data_ptr(), sp)
+        if B <= 8:
+            att = self._ws("att_dec", (B, a.hidden_dim), torch.bfloat16)
+            _lib.call("dali_gemv_bf16", o.data_ptr(), W.wo[l].data_ptr(), B, a.hidden_dim,
+                      H * hd, att.data_ptr(), sp)
+            return att
         return o @ W.wo[l].t()
 
     def _forward(self, tokens_dev: torch.Tensor, B: int, S: int, pos0: int, step: int,

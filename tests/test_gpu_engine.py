@@ -614,3 +614,19 @@ def test_full_width_layers_decisions_and_logits(name, slots, psize):
     for s_, lg in enumerate(st.logits):
         ref = logits[0, S0 - 1 + s_]
         torch.testing.assert_close(lg[0], ref, rtol=RTOL, atol=RTOL * ref.abs().max().item())
+
+
+@pytest.mark.parametrize("B,M,K", [(1, 6144, 4096), (2, 4096, 4096), (8, 512, 256), (3, 96, 64)])
+def test_decode_gemv_vs_torch(B, M, K):
+    """dali_gemv_bf16 (attention projections at decode) vs fp32 torch."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(B * 7 + M)
+    x = torch.randn(B, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(M, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    y = torch.empty(B, M, dtype=torch.bfloat16, device="cuda")
+    _lib.call("dali_gemv_bf16", x.data_ptr(), w.data_ptr(), B, M, K, y.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    ref = x.float() @ w.float().t()
+    torch.testing.assert_close(y.float(), ref, rtol=1e-2, atol=1e-2 * ref.abs().max().item())
