@@ -26,8 +26,13 @@ same code runs on NCCL (GPU tensors) and gloo (CPU tensors, tests).
 
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import torch
+
+from .. import _lib
+from ..trace import route_device
 import torch.distributed as dist
 
 
@@ -95,3 +100,89 @@ def plan_regroup(recv_counts: np.ndarray):
     per_expert = rc.sum(axis=0)
     offsets = np.concatenate([[0], np.cumsum(per_expert)]).astype(np.int32)
     return (np.asarray(perm, dtype=np.int32), offsets, [int(x) for x in recv_sz])
+
+
+class EPMoEMixin:
+    """Expert-parallel MoE layer of ``OffloadEngine`` (dispatch / combine
+    exchange around the 1-GPU execution path)."""
+
+    def _moe_ep(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, token_index: int,
+                is_eos: bool) -> torch.Tensor:
+        """Expert-parallel MoE layer (see ep.py): dispatch all-to-all, DALI
+        policy + execution on this rank's NL experts with global workloads,
+        return all-to-all, Eq. (2) combine on the source rank."""
+        a, ep = self.arch, self.ep
+        N, k, d, NL = a.num_experts, a.top_k, a.hidden_dim, self.NL
+        T = h.shape[0]
+        cs = self._cur()
+        tp0 = time.perf_counter()
+        v = self._route(l, h)
+        recv_counts = ep.exchange_counts(v["wl"])                  # (G*NL,) int64
+        wl_glob = recv_counts.view(ep.world, NL).sum(0)
+        pred = None
+        if self.policy.prefetch_size > 0 and l + 1 < a.num_layers:
+            _, _, pw = route_device(h, self.w.router[l + 1], k, residual=self.policy.residuals[l],
+                                    want_idx=False, want_weights=False)
+            pred = ep.all_reduce_sum_(pw)[ep.rank * NL:(ep.rank + 1) * NL].contiguous()
+        ri = self.policy.layer_step(step, l, token_index, is_eos, wl_glob, None, None,
+                                    predicted=pred)
+        hv = self._host_view(v, T)
+        rc_host = self._ws("rc_h", (ep.world * NL,), torch.int64, pinned=True)
+        rc_host.copy_(recv_counts, non_blocking=True)
+        if self.cfg.capture:
+            h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
+            h_host.copy_(h, non_blocking=True)
+        ev_dec = torch.cuda.Event()
+        ev_dec.record(cs)
+        tp1 = time.perf_counter()
+        ev_dec.synchronize()
+        tp2 = time.perf_counter()
+        rec = self.policy.record(ri)
+        rc = rc_host.numpy().reshape(ep.world, NL).copy()
+        wl_np = rc.sum(axis=0)
+        self.stats.workloads[(step, l)] = wl_np
+        if self.cfg.capture:
+            self.stats.captured.append((step, l, h_host.clone()))
+            self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
+        perm2, offs_l, recv_sz = plan_regroup(rc)
+        snd_sz = send_sizes(hv["wl"].numpy(), ep.world)
+        recv_x = ep.exchange_rows(v["xp"], snd_sz, recv_sz)        # (R, d) bf16
+        R = int(recv_x.shape[0])
+        perm2_d = torch.from_numpy(perm2).to(self.dev, non_blocking=True)
+        offs_d = torch.from_numpy(offs_l).to(self.dev, non_blocking=True)
+        xl = self._ws("xl", (max(R, 1), d), torch.bfloat16)
+        if R:
+            _lib.call("dali_permute", recv_x.data_ptr(), perm2_d.data_ptr(), R, d, xl.data_ptr(),
+                      cs.cuda_stream)
+        yp, splits, _ = self._exec_local(l, xl, offs_d, wl_np, rec, R)
+        y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+        tp3 = time.perf_counter()
+        cpu_rows = None
+        if any(rec.C[e] for e in range(NL)) and R:
+            xl_host = self._ws("xl_h", (R, d), torch.bfloat16, pinned=True)
+            xl_host.copy_(xl[:R])
+            cpu_rows = self._cpu_rows(l, xl_host, offs_l, rec, R)
+        tp4 = time.perf_counter()
+        self._acct(tp0, tp1, tp2, tp3, tp4)
+        # per-row expert outputs in grouped order -> received order -> sources
+        # split-K planes summed in plane order, exactly as the combine kernel
+        # does (fp32 adds in the same order: bit-identical to the 1-GPU engine)
+        y_l = yp[0, :R].clone()
+        for s_ in range(1, splits):
+            y_l += yp[s_, :R]
+        if cpu_rows is not None:
+            for e in range(NL):
+                if rec.C[e] and offs_l[e + 1] > offs_l[e]:
+                    y_l[offs_l[e]:offs_l[e + 1]] = cpu_rows[offs_l[e]:offs_l[e + 1]]
+        y_recv = torch.empty_like(y_l)
+        if R:
+            y_recv.index_copy_(0, perm2_d.long(), y_l)
+        y_back = ep.exchange_rows(y_recv, recv_sz, snd_sz)          # (T*k, d) f32
+        out = torch.empty_like(x)
+        _lib.call("dali_unpermute_combine", x.data_ptr(), y_back.data_ptr(), v["idx"].data_ptr(),
+                  v["pos"].data_ptr(), v["wts"].data_ptr(), None, None,
+                  y_shared.data_ptr() if y_shared is not None else None, T, k, d, 1, T * k,
+                  out.data_ptr(), cs.cuda_stream)
+        return out
+
+    # ------------------------------------------------------------- forward
