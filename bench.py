@@ -29,9 +29,19 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: keep NCCL's version banner off it
-if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
-    os.environ["NCCL_DEBUG"] = "WARN"
+# stdout carries exactly one JSON line.  Native libraries (NCCL's version
+# banner, CUDA/driver messages) write to file descriptor 1 directly, so the
+# real stdout is kept on a private descriptor for the result line and fd 1 is
+# pointed at stderr for everything else.
+_RESULT_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+sys.stdout = sys.stderr
+
+
+def emit(line: dict) -> None:
+    _RESULT_OUT.write(json.dumps(line) + "\n")
+    _RESULT_OUT.flush()
+
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -228,7 +238,7 @@ def run_reference(args, ws, rank):
         "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 METRIC = "decode tokens/s, Mixtral-8x7B shape, 24 GB HBM expert cache (prefill tokens/s + hit rate reported)"
@@ -417,7 +427,7 @@ def run_dali(args, ws, rank, local):
             "clocks": clocks,
             "cpu_baseline": cpu_base,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def main():
