@@ -394,6 +394,51 @@ int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
                           int32_t splits, float scale, float* workspace,
                           uint16_t* out, void* stream);
 
+/* ---- expert-parallel exchange over peer memory ---------------------------
+ * The EP MoE layer's dispatch and return all-to-alls, fused with the permute
+ * / unpermute around them: ranks store rows straight into each other's
+ * receive buffers (CUDA IPC mappings over NVLink/NVSwitch) and bump a
+ * system-scope arrival counter (one per rank and direction) instead of
+ * calling a collective.  Per-rank buffer (dali_ep_layout, out[5] =
+ * {recv, ret, cnt, flags, total} byte offsets):
+ *   recv [G][cap][d] bf16, ret [G][cap][d] f32, cnt [G][NL] i32, flags u64[2].
+ * Source block s of a receiver's recv / ret is written only by rank s.
+ *   dali_ipc_alloc / open / close / free: cudaMalloc + IPC handles (64 B).
+ *   dali_ep_dispatch: row r of this rank's permuted rows (grouped by global
+ *     expert by dali_moe_plan; offsets (N+1) [dev]) -> owner q = e / NL at
+ *     recv_q[rank][r - offsets[q*NL]] (gathered from x via perm_token),
+ *     counts -> cnt_q[rank][:]; then every peer's flags[0] += 1.
+ *   dali_ep_wait: spin until *flag >= target (bounded; *err = 1 on timeout).
+ *   dali_ep_recv: cnt (G, NL) -> grouped order (local expert, source):
+ *     offs_l (NL+1), workloads (NL) i64, meta[0] = rows, and the regrouped
+ *     rows out (rows, d) bf16.
+ *   dali_ep_return: grouped result rows (sum of `splits` planes of yp, or
+ *     cpu_rows where gmask[j] == 0) -> ret_s[rank][idx] of their source s;
+ *     then every peer's flags[1] += 1.
+ *   dali_ep_gather_back: ret (G, cap, d) -> back (rows, d) f32 in this
+ *     rank's permuted order (for dali_unpermute_combine with splits 1).
+ * peer_* are [dev] (G,) u64 tables of the ranks' buffer addresses. */
+int dali_ipc_alloc(size_t bytes, void** ptr, void* handle);
+int dali_ipc_open(const void* handle, void** ptr);
+int dali_ipc_close(void* ptr);
+int dali_ipc_free(void* ptr);
+int dali_ep_layout(int32_t G, int32_t NL, int64_t cap, int32_t d, int64_t* out);
+int dali_ep_dispatch(const uint16_t* x, const int32_t* perm_token, const int32_t* offsets,
+                     int32_t N, int32_t NL, int32_t G, int32_t rank, int64_t cap, int32_t d,
+                     int64_t max_rows, const uint64_t* peer_recv, const uint64_t* peer_cnt,
+                     const uint64_t* peer_flag, void* stream);
+int dali_ep_wait(const uint64_t* flag, uint64_t target, int64_t max_spins, int32_t* err,
+                 void* stream);
+int dali_ep_recv(const int32_t* cnt, int32_t G, int32_t NL, int64_t cap, const uint16_t* recv,
+                 int32_t d, int64_t max_rows, int32_t* perm2, int32_t* offs_l,
+                 int64_t* workloads, int32_t* meta, uint16_t* out, void* stream);
+int dali_ep_return(const float* yp, int32_t splits, int64_t plane, const float* cpu_rows,
+                   const int8_t* gmask, const int32_t* offs_l, const int32_t* cnt, int32_t G,
+                   int32_t NL, int32_t rank, int64_t cap, int32_t d, int64_t max_rows,
+                   const uint64_t* peer_ret, const uint64_t* peer_flag, void* stream);
+int dali_ep_gather_back(const float* ret, const int32_t* offsets, int32_t N, int32_t NL,
+                        int64_t cap, int32_t d, int64_t max_rows, float* back, void* stream);
+
 /* ---- CPU expert worker (host; DALI hybrid execution) ---------------------
  * SwiGLU of R token rows x (R, d) bf16 [host] with one expert block [host]
  * (the engine's W13/W2 layout), y (R, d) f32 [host]; AVX-512 BF16

@@ -111,6 +111,17 @@ SIGNATURES = {
     "dali_copy_mapped": [_P, _P, _I64, _P],
     "dali_shared_finish": [_P, _I32, _I64, _I32, _P, _P, _P, _P],
     "dali_gemv_bf16": [_P, _P, _I32, _I32, _I32, _P, _P],
+    "dali_ipc_alloc": [C.c_size_t, C.POINTER(C.c_void_p), _P],
+    "dali_ipc_open": [_P, C.POINTER(C.c_void_p)],
+    "dali_ipc_close": [_P],
+    "dali_ipc_free": [_P],
+    "dali_ep_layout": [_I32, _I32, _I64, _I32, _P],
+    "dali_ep_dispatch": [_P, _P, _P, _I32, _I32, _I32, _I32, _I64, _I32, _I64, _P, _P, _P, _P],
+    "dali_ep_wait": [_P, C.c_uint64, _I64, _P, _P],
+    "dali_ep_recv": [_P, _I32, _I32, _I64, _P, _I32, _I64, _P, _P, _P, _P, _P, _P],
+    "dali_ep_return": [_P, _I32, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I64, _I32, _I64, _P,
+                       _P, _P],
+    "dali_ep_gather_back": [_P, _P, _I32, _I32, _I64, _I32, _I64, _P, _P],
     "dali_host_alloc_shared": [C.c_size_t, _I32, _I32, C.POINTER(C.c_int32), _I32,
                                C.POINTER(C.c_void_p)],
 }

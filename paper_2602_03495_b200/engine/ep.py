@@ -32,6 +32,7 @@ import numpy as np
 import torch
 
 from .. import _lib
+from ..errors import SimulationError
 from ..trace import route_device
 import torch.distributed as dist
 
@@ -45,6 +46,7 @@ class EPGroup:
             raise ValueError(f"{num_experts} experts do not split over {self.world} ranks")
         self.N = num_experts
         self.NL = num_experts // self.world
+        self.peer = None                 # PeerExchange, built by the engine on first use
 
     @property
     def local_experts(self) -> list[int]:
@@ -67,6 +69,70 @@ class EPGroup:
         dist.all_to_all_single(out, send.contiguous(), output_split_sizes=recv_sizes,
                                input_split_sizes=send_sizes, group=self.group)
         return out
+
+
+# ---------------------------------------------------------------------------
+# peer-memory exchange (the product path on one node; NCCL stays as baseline)
+# ---------------------------------------------------------------------------
+
+class PeerExchange:
+    """Per-rank IPC buffers of the fused EP exchange (csrc/ep.cu): recv /
+    ret / cnt / flags of every rank mapped into this process, with device
+    pointer tables for the dispatch and return kernels.  ``cap`` = the most
+    rows one rank can send another in one layer (tokens x top_k)."""
+
+    MAX_SPINS = 200_000_000            # ~20 s of 64 ns sleeps: a lost peer errors out
+
+    def __init__(self, ep: "EPGroup", cap: int, d: int, device):
+        import ctypes as C
+        self.ep, self.cap, self.d = ep, int(cap), int(d)
+        G, NL = ep.world, ep.NL
+        lay = (C.c_int64 * 5)()
+        _lib.call("dali_ep_layout", G, NL, self.cap, self.d, lay)
+        self.off = list(lay)
+        ptr = C.c_void_p()
+        handle = (C.c_uint8 * 64)()
+        _lib.call("dali_ipc_alloc", self.off[4], C.byref(ptr), handle)
+        self.base = int(ptr.value)
+        handles = [None] * G
+        dist.all_gather_object(handles, bytes(handle), group=ep.group)
+        self.opened = []
+        bases = []
+        for g in range(G):
+            if g == ep.rank:
+                bases.append(self.base)
+                continue
+            hp = (C.c_uint8 * 64).from_buffer_copy(handles[g])
+            pp = C.c_void_p()
+            _lib.call("dali_ipc_open", hp, C.byref(pp))
+            self.opened.append(int(pp.value))
+            bases.append(int(pp.value))
+
+        def table(off):
+            return torch.tensor([b + off for b in bases], dtype=torch.int64, device=device)
+        self.peer_recv = table(self.off[0])
+        self.peer_ret = table(self.off[1])
+        self.peer_cnt = table(self.off[2])
+        self.peer_flag_d = table(self.off[3])
+        self.peer_flag_r = table(self.off[3] + 8)
+        self.recv = self.base + self.off[0]
+        self.ret = self.base + self.off[1]
+        self.cnt = self.base + self.off[2]
+        self.flag_d = self.base + self.off[3]
+        self.flag_r = self.base + self.off[3] + 8
+        self.epoch = 0
+        # timeout flag in mapped pinned memory: the host checks it with no copy
+        self.err = torch.zeros((1,), dtype=torch.int32, pin_memory=True)
+        dist.barrier(group=ep.group)
+
+    def check(self):
+        if int(self.err[0]):
+            raise RuntimeError("expert-parallel peer exchange timed out (a rank stopped)")
+
+    def close(self):
+        for p in self.opened:
+            _lib.load().dali_ipc_close(p)
+        self.opened = []
 
 
 # ---------------------------------------------------------------------------
@@ -108,9 +174,104 @@ class EPMoEMixin:
 
     def _moe_ep(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, token_index: int,
                 is_eos: bool) -> torch.Tensor:
-        """Expert-parallel MoE layer (see ep.py): dispatch all-to-all, DALI
-        policy + execution on this rank's NL experts with global workloads,
-        return all-to-all, Eq. (2) combine on the source rank."""
+        if self.cfg.ep_transport == "p2p":
+            return self._moe_ep_p2p(l, x, h, step, token_index, is_eos)
+        return self._moe_ep_nccl(l, x, h, step, token_index, is_eos)
+
+    def _moe_ep_p2p(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int,
+                    token_index: int, is_eos: bool) -> torch.Tensor:
+        """Expert-parallel MoE layer over peer memory (csrc/ep.cu): the
+        dispatch kernel gathers this rank's permuted rows straight into the
+        owners' receive buffers; owners regroup, decide (DALI policy on the
+        GLOBAL workloads) and execute, then the return kernel sums split-K
+        planes / takes CPU rows and stores each result into its source's
+        return buffer; the source gathers and combines (Eq. 2)."""
+        a, ep = self.arch, self.ep
+        N, k, d, NL, G = a.num_experts, a.top_k, a.hidden_dim, self.NL, ep.world
+        T = h.shape[0]
+        cs = self._cur()
+        sp = cs.cuda_stream
+        tp0 = time.perf_counter()
+        if ep.peer is None:
+            ep.peer = PeerExchange(ep, self.max_batch * self.max_seq * k, d, self.dev)
+        ex = ep.peer
+        if T * k > ex.cap:
+            raise SimulationError(f"{T * k} rows exceed the EP exchange capacity {ex.cap}")
+        ex.epoch += 1
+        v = self._route(l, h)
+        _lib.call("dali_ep_dispatch", h.data_ptr(), v["perm"].data_ptr(),
+                  v["offsets"].data_ptr(), N, NL, G, ep.rank, ex.cap, d, T * k,
+                  ex.peer_recv.data_ptr(), ex.peer_cnt.data_ptr(), ex.peer_flag_d.data_ptr(), sp)
+        _lib.call("dali_ep_wait", ex.flag_d, ex.epoch * G, PeerExchange.MAX_SPINS,
+                  ex.err.data_ptr(), sp)
+        perm2 = self._ws("ep_perm2", (G * ex.cap,), torch.int32)
+        offs_l = self._ws("ep_offs", (NL + 1,), torch.int32)
+        wl_glob = self._ws("ep_wl", (NL,), torch.int64)
+        meta = self._ws("ep_meta", (4,), torch.int32)
+        xl = self._ws("ep_xl", (G * ex.cap, d), torch.bfloat16)
+        _lib.call("dali_ep_recv", ex.cnt, G, NL, ex.cap, ex.recv, d, G * ex.cap,
+                  perm2.data_ptr(), offs_l.data_ptr(), wl_glob.data_ptr(), meta.data_ptr(),
+                  xl.data_ptr(), sp)
+        pred = None
+        if self.policy.prefetch_size > 0 and l + 1 < a.num_layers:
+            _, _, pw = route_device(h, self.w.router[l + 1], k, residual=self.policy.residuals[l],
+                                    want_idx=False, want_weights=False)
+            pred = ep.all_reduce_sum_(pw)[ep.rank * NL:(ep.rank + 1) * NL].contiguous()
+        ri = self.policy.layer_step(step, l, token_index, is_eos, wl_glob, None, None,
+                                    predicted=pred)
+        hv = self._host_view(v, T)
+        cnt_host = self._ws("ep_cnt_h", (G * NL,), torch.int32, pinned=True)
+        _lib.call("dali_copy_mapped", cnt_host.data_ptr(), ex.cnt, G * NL * 4, sp)
+        if self.cfg.capture:
+            h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
+            h_host.copy_(h, non_blocking=True)
+        ev_dec = torch.cuda.Event()
+        ev_dec.record(cs)
+        tp1 = time.perf_counter()
+        ev_dec.synchronize()
+        tp2 = time.perf_counter()
+        ex.check()
+        rec = self.policy.record(ri)
+        rc = cnt_host.numpy().astype(np.int64).reshape(G, NL)
+        wl_np = rc.sum(axis=0)
+        R = int(wl_np.sum())
+        offs_np = np.concatenate([[0], np.cumsum(wl_np)]).astype(np.int32)
+        self.stats.workloads[(step, l)] = wl_np
+        if self.cfg.capture:
+            self.stats.captured.append((step, l, h_host.clone()))
+            self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
+        yp, splits, gmask_p = self._exec_local(l, xl, offs_l, wl_np, rec, R)
+        y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+        tp3 = time.perf_counter()
+        cpu_rows = None
+        if R and np.frombuffer(rec.C, dtype=np.int8, count=NL).any():
+            xl_host = self._ws("xl_h", (R, d), torch.bfloat16, pinned=True)
+            xl_host.copy_(xl[:R])
+            cpu_rows = self._cpu_rows(l, xl_host, offs_np, rec, R)
+        tp4 = time.perf_counter()
+        self._acct(tp0, tp1, tp2, tp3, tp4)
+        _lib.call("dali_ep_return", yp.data_ptr(), splits, yp.shape[1] * d,
+                  cpu_rows.data_ptr() if cpu_rows is not None else None, gmask_p,
+                  offs_l.data_ptr(), ex.cnt, G, NL, ep.rank, ex.cap, d, G * ex.cap,
+                  ex.peer_ret.data_ptr(), ex.peer_flag_r.data_ptr(), sp)
+        _lib.call("dali_ep_wait", ex.flag_r, ex.epoch * G, PeerExchange.MAX_SPINS,
+                  ex.err.data_ptr(), sp)
+        back = self._ws("ep_back", (T * k, d), torch.float32)
+        _lib.call("dali_ep_gather_back", ex.ret, v["offsets"].data_ptr(), N, NL, ex.cap, d, T * k,
+                  back.data_ptr(), sp)
+        out = torch.empty_like(x)
+        _lib.call("dali_unpermute_combine", x.data_ptr(), back.data_ptr(), v["idx"].data_ptr(),
+                  v["pos"].data_ptr(), v["wts"].data_ptr(), None, None,
+                  y_shared.data_ptr() if y_shared is not None else None, T, k, d, 1, T * k,
+                  out.data_ptr(), sp)
+        return out
+
+    def _moe_ep_nccl(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int,
+                     token_index: int, is_eos: bool) -> torch.Tensor:
+        """Expert-parallel MoE layer over NCCL (the baseline transport):
+        dispatch all-to-all, DALI policy + execution on this rank's NL experts
+        with global workloads, return all-to-all, Eq. (2) combine on the
+        source rank."""
         a, ep = self.arch, self.ep
         N, k, d, NL = a.num_experts, a.top_k, a.hidden_dim, self.NL
         T = h.shape[0]

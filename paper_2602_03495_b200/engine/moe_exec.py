@@ -108,7 +108,7 @@ class MoEExecMixin:
         _lib.call("dali_moe_plan_permute", v["idx"].data_ptr(), T, k, N, h.data_ptr(), d,
                   v["offsets"].data_ptr(), perm.data_ptr(), v["pos"].data_ptr(),
                   v["xp"].data_ptr(), cs.cuda_stream)
-        v["blk"], v["layout"] = rblk, (o_off, o_idx, o_w, nb)
+        v["blk"], v["layout"], v["perm"] = rblk, (o_off, o_idx, o_w, nb), perm
         return v
 
     def _host_view(self, v, T: int):

@@ -75,6 +75,8 @@ class EngineConfig:
     ffn_kernel: str = "tc"                  # "tc" (tcgen05 + TMA) | "simt" (weight streaming)
     resident_fast: bool = True              # all-resident: no per-layer host wait
     use_graph: bool = True                  # all-resident decode steps replay one CUDA graph
+    ep_transport: str = "p2p"               # expert parallelism: "p2p" (peer-memory kernels,
+    #                                         csrc/ep.cu) or "nccl" (all_to_all baseline)
     trace_layers: bool = False              # per-layer host/device timeline (tools/decode_timeline.py)
 
 

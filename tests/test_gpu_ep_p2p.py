@@ -1,0 +1,120 @@
+"""Peer-memory expert-parallel exchange (csrc/ep.cu) across two processes.
+
+This pool gives one GPU per call, so both ranks share cuda:0: the CUDA IPC
+mappings, system-scope arrival counters, dispatch / regroup / return /
+gather-back kernels run exactly as between two GPUs on an NVSwitch node
+(gloo only bootstraps the IPC handles).  Each owner applies a per-expert
+scale as its "FFN", so every returned row checks routing and placement."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+G, N, K, D, T = 2, 8, 2, 256, 37
+
+
+def _worker(rank, port, out_q):
+    import torch.distributed as dist
+
+    from paper_2602_03495_b200 import _lib
+    from paper_2602_03495_b200.engine.ep import EPGroup, PeerExchange
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=G)
+    try:
+        ep = EPGroup(N)
+        NL = ep.NL
+        ex = PeerExchange(ep, T * K, D, torch.device("cuda", 0))
+        sp = torch.cuda.current_stream().cuda_stream
+        ok = True
+        for epoch_seed in range(3):                  # three layers: flags are monotonic
+            g = torch.Generator().manual_seed(100 * rank + epoch_seed)
+            x = torch.randn(T, D, generator=g).to(torch.bfloat16).cuda()
+            idx = torch.stack([torch.randperm(N, generator=g)[:K] for _ in range(T)]).to(
+                torch.int32).cuda()
+            offsets = torch.empty(N + 1, dtype=torch.int32, device="cuda")
+            perm = torch.empty(T * K, dtype=torch.int32, device="cuda")
+            pos = torch.empty(T, K, dtype=torch.int32, device="cuda")
+            _lib.call("dali_moe_plan", idx.data_ptr(), T, K, N, offsets.data_ptr(),
+                      perm.data_ptr(), pos.data_ptr(), sp)
+            ex.epoch += 1
+            _lib.call("dali_ep_dispatch", x.data_ptr(), perm.data_ptr(), offsets.data_ptr(), N,
+                      NL, G, rank, ex.cap, D, T * K, ex.peer_recv.data_ptr(),
+                      ex.peer_cnt.data_ptr(), ex.peer_flag_d.data_ptr(), sp)
+            _lib.call("dali_ep_wait", ex.flag_d, ex.epoch * G, PeerExchange.MAX_SPINS,
+                      ex.err.data_ptr(), sp)
+            perm2 = torch.empty(G * ex.cap, dtype=torch.int32, device="cuda")
+            offs_l = torch.empty(NL + 1, dtype=torch.int32, device="cuda")
+            wl = torch.empty(NL, dtype=torch.int64, device="cuda")
+            meta = torch.zeros(4, dtype=torch.int32, device="cuda")
+            xl = torch.zeros(G * ex.cap, D, dtype=torch.bfloat16, device="cuda")
+            _lib.call("dali_ep_recv", ex.cnt, G, NL, ex.cap, ex.recv, D, G * ex.cap,
+                      perm2.data_ptr(), offs_l.data_ptr(), wl.data_ptr(), meta.data_ptr(),
+                      xl.data_ptr(), sp)
+            torch.cuda.synchronize()
+            R = int(meta[0])
+            ol = offs_l.cpu().numpy()
+            # owner "FFN": row of local expert j scaled by (global expert + 1); odd
+            # local experts go through the CPU-rows path of the return kernel
+            yp = torch.zeros(2, max(R, 1), D, dtype=torch.float32, device="cuda")
+            cpu_rows = torch.zeros(max(R, 1), D, dtype=torch.float32, device="cuda")
+            gmask = torch.tensor([1 if j % 2 == 0 else 0 for j in range(NL)], dtype=torch.int8,
+                                 device="cuda")
+            for j in range(NL):
+                sc = float(rank * NL + j + 1)
+                rows = xl[ol[j]:ol[j + 1]].float() * sc
+                if j % 2 == 0:                       # two split-K planes summing to rows
+                    yp[0, ol[j]:ol[j + 1]] = rows * 0.25
+                    yp[1, ol[j]:ol[j + 1]] = rows * 0.75
+                else:
+                    cpu_rows[ol[j]:ol[j + 1]] = rows
+            _lib.call("dali_ep_return", yp.data_ptr(), 2, yp.shape[1] * D, cpu_rows.data_ptr(),
+                      gmask.data_ptr(), offs_l.data_ptr(), ex.cnt, G, NL, rank, ex.cap, D,
+                      G * ex.cap, ex.peer_ret.data_ptr(), ex.peer_flag_r.data_ptr(), sp)
+            _lib.call("dali_ep_wait", ex.flag_r, ex.epoch * G, PeerExchange.MAX_SPINS,
+                      ex.err.data_ptr(), sp)
+            back = torch.empty(T * K, D, dtype=torch.float32, device="cuda")
+            _lib.call("dali_ep_gather_back", ex.ret, offsets.data_ptr(), N, NL, ex.cap, D, T * K,
+                      back.data_ptr(), sp)
+            torch.cuda.synchronize()
+            ex.check()
+            # expected: permuted row r = x[perm[r]] * (expert(r) + 1)
+            off = offsets.cpu().numpy()
+            pm = perm.cpu().numpy()
+            exp_rows = torch.empty(T * K, D)
+            for e in range(N):
+                for r in range(off[e], off[e + 1]):
+                    exp_rows[r] = x[pm[r]].float().cpu() * (e + 1)
+            ok &= bool(torch.allclose(back.cpu(), exp_rows, rtol=1e-6, atol=1e-5))
+            ok &= int(wl.sum()) == R
+        dist.barrier()
+        ex.close()
+        out_q.put((rank, ok))
+    except Exception as exc:                         # surface the error in the parent
+        out_q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_two_processes_one_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(G)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(G))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
