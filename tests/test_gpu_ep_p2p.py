@@ -118,3 +118,75 @@ def test_peer_exchange_two_processes_one_gpu():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+def _engine_worker(rank, port, out_q):
+    import torch.distributed as dist
+
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    from paper_2602_03495_b200.engine.ep import EPGroup
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=G)
+    try:
+        arch = preset("tiny")
+        cm = default_cost_model(non_moe_layer_time=3.0)
+        res = np.random.default_rng(0).standard_normal((arch.num_layers - 1,
+                                                        arch.hidden_dim)) * 0.05
+        cfg = dict(cache_slots_per_layer=1, prefetch_size=1, capture=True, seed=3)
+        ep = EPGroup(arch.num_experts)
+        w_sh = ModelWeights(arch, seed=9, experts=ep.local_experts)
+        eng = OffloadEngine(arch, w_sh, cm, EngineConfig(**cfg), residuals=res, max_seq=64,
+                            ep=ep)
+        g = torch.Generator().manual_seed(40 + rank)
+        prompt = torch.randint(0, arch.vocab_size, (1, 10), generator=g)
+        toks, st = eng.generate(prompt, 6)
+        # reference: the single-process engine on this rank's prompt
+        base = OffloadEngine(arch, ModelWeights(arch, seed=9), cm, EngineConfig(**cfg),
+                             residuals=res, max_seq=64)
+        tb, sb = base.generate(prompt, 6)
+        ok = True
+        for la, lb in zip(st.logits, sb.logits):
+            ok &= bool(torch.allclose(la, lb, rtol=2e-2, atol=2e-2 * lb.abs().max().item()))
+        # the owner's workloads are the GLOBAL histogram of its experts
+        mine = {key: st.topk[key] for key in st.topk}
+        both = [None] * G
+        dist.all_gather_object(both, mine)
+        NL = ep.NL
+        for key, wl in st.workloads.items():
+            hist = np.zeros(arch.num_experts, np.int64)
+            for r in range(G):
+                np.add.at(hist, both[r][key].reshape(-1), 1)
+            ok &= bool(np.array_equal(wl, hist[rank * NL:(rank + 1) * NL]))
+        ok &= st.cpu_expert_calls + st.gpu_expert_calls > 0
+        dist.barrier()
+        ep.peer.close()
+        out_q.put((rank, ok))
+    except Exception as exc:
+        import traceback
+        out_q.put((rank, repr(exc) + traceback.format_exc()[-1500:]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_engine_two_ranks_one_gpu():
+    """The EP engine at world 2 over the peer-memory transport (both ranks on
+    the pool's one GPU): each rank's logits match the single-process engine
+    on its own prompt, and every owner decides on the global workloads."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_engine_worker, args=(r, port, q)) for r in range(G)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(G))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
