@@ -149,8 +149,15 @@ def dist_setup(need_group: bool = False):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # DALI_BENCH_SHARED_GPU=1 (testing on a one-GPU pool): every rank on
+        # cuda:0 and a gloo group (NCCL refuses two ranks on one device)
+        shared = os.environ.get("DALI_BENCH_SHARED_GPU") == "1"
+        dev = 0 if shared else local
+        torch.cuda.set_device(dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
         if need_group:                       # EP at one GPU: a world-1 NCCL group
@@ -318,7 +325,7 @@ def run_dali(args, ws, rank, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = _lib.launch_count()
         stats, reps = [], []
-        with ClockSampler(local) as clk:
+        with ClockSampler(torch.cuda.current_device()) as clk:
             torch.cuda.nvtx.range_push("timed")
             e0.record(cs)
             for p in dev_prompts:
