@@ -150,6 +150,12 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap b_map, const int32_t* __restri
   Tile t;
   if (!find_tile<BN>(offs, a_maps, N, m_tiles, splits, t, blockIdx.x)) return;
   const void* a_map = reinterpret_cast<const void*>(a_maps[t.e] + (MODE == 0 ? 0 : 128));
+  // Early PDL trigger: the tile list is final once the wait above returned, so
+  // the down projection may launch now; its CTAs take the SM slots this
+  // grid's CTAs leave and start streaming W2 (which does not depend on H)
+  // while the last up tiles drain.  The down kernel's own griddepcontrol.wait
+  // still orders every read of H after this grid completes.
+  if (MODE == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -187,6 +193,15 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap b_map, const int32_t* __restri
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
+  // down: the first ring's worth of weight tiles (A) is independent of the up
+  // projection, so it is requested before the PDL wait
+  const int pre = MODE == 1 ? min(nk, S::STAGES) : 0;
+  if (MODE == 1 && warp == 0 && lane == 0) {
+    for (int i = 0; i < pre; ++i) {
+      mbar_expect_tx(full + i, S::A_BYTES + S::B_BYTES);
+      tma_load_2d(sA + i * S::A_BYTES, a_map, full + i, (kb0 + i) * BK, t.m_tile * BM);
+    }
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");     // PDL (no-op without it)
 
   if (warp == 0 && lane == 0) {
@@ -194,10 +209,12 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap b_map, const int32_t* __restri
     for (int i = 0; i < nk; ++i) {
       const int s = i % S::STAGES;
       const uint32_t ph = (i / S::STAGES) & 1;
-      mbar_wait(empty + s, ph ^ 1);
-      mbar_expect_tx(full + s, S::A_BYTES + S::B_BYTES);
       const int kx = (kb0 + i) * BK;
-      tma_load_2d(sA + s * S::A_BYTES, a_map, full + s, kx, t.m_tile * BM);
+      if (i >= pre) {
+        mbar_wait(empty + s, ph ^ 1);
+        mbar_expect_tx(full + s, S::A_BYTES + S::B_BYTES);
+        tma_load_2d(sA + s * S::A_BYTES, a_map, full + s, kx, t.m_tile * BM);
+      }
       tma_load_2d(sB + s * S::B_BYTES, &b_map, full + s, kx, t.row0);
     }
   } else if (warp == 1 && lane == 0) {

@@ -27,13 +27,16 @@ from .cpu_worker import NATIVE_MAX_ROWS, cpu_expert_rows
 
 def ffn_splits(max_rows: int, tiles: int, kb: int, n_sm: int) -> int:
     """Split-K planes of the down projection for dali_expert_ffn_tc: the
-    smallest factor dividing f/64 that gives >= 2 CTAs per SM (``max_rows``
-    is kept for the signature: every token-tile width uses the same rule)."""
+    smallest factor dividing f/64 that gives >= 1.5 CTAs per SM (``max_rows``
+    is kept for the signature: every token-tile width uses the same rule).
+    Measured at Mixtral shapes (tools/prof_ffn.py --splits): one expert runs
+    best at 7 planes (224 CTAs), two at 4 (256 CTAs); a full second wave of
+    short CTAs costs more in per-CTA prologue/epilogue than it hides."""
     best = 1
     for s in range(1, 17):
         if kb % s == 0:
             best = s
-            if tiles * s >= 2 * n_sm:
+            if 2 * tiles * s >= 3 * n_sm:
                 break
     return best
 

@@ -82,6 +82,8 @@ def run(counts, label):
           f"{flops / ms / 1e9:.1f} TFLOP/s, bytes {byts}")
 
 
+if args.mode == "one":
+    run([1, 0, 0, 0, 0, 0, 0, 0], "decode 1x1")
 if args.mode in ("decode", "both"):
     run([1, 0, 0, 1, 0, 0, 0, 0], "decode 2x1")
 if args.mode in ("prefill", "both"):
