@@ -554,10 +554,11 @@ def test_reset_cache_reproduces_first_request():
 
 @pytest.mark.parametrize("name,slots,psize", [("mixtral-8x7b", 2, 1),
                                               ("deepseek-v2-lite", 24, 4),
-                                              ("qwen1.5-moe-a2.7b", 24, 4)])
+                                              ("qwen1.5-moe-a2.7b", 24, 4),
+                                              ("mixtral-8x22b", 2, 1)])
 def test_full_width_layers_decisions_and_logits(name, slots, psize):
     """BASELINE configs widths on 2 layers -- Mixtral-8x7B (d 4096, f 14336,
-    8 experts top-2), DeepSeek-V2-Lite (64 routed top-6 + 2 shared) and
+    8 experts top-2), Mixtral-8x22B (d 6144, f 16384, 604 MB experts), DeepSeek-V2-Lite (64 routed top-6 + 2 shared) and
     Qwen1.5-MoE (60 routed top-4 + gated shared): fp64 gating of the bf16
     gate inputs, every DALI decision bit-exact against the oracle replay,
     logits within the bf16 tolerance of the fp32 CPU model -- at the full
