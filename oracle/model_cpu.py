@@ -16,8 +16,6 @@ own gate logits (softmax, optionally renormalised over the selected k).
 
 from __future__ import annotations
 
-import math
-
 import torch
 import torch.nn.functional as F
 

@@ -28,10 +28,10 @@ sys.path.insert(0, REF)
 import moesim  # noqa: E402
 from moesim import cache as mc  # noqa: E402
 from moesim import prefetch as mp  # noqa: E402
-from moesim.assignment import AssignmentInstance, greedy_assign  # noqa: E402
+from moesim.assignment import greedy_assign  # noqa: E402
 from moesim.cost_model import _interp, default_cost_model, fit_cost_model  # noqa: E402
 from moesim.simulator import SimConfig, simulate_run  # noqa: E402
-from moesim.trace import (ModelConfig, ResidualVectors, derive_workloads,  # noqa: E402
+from moesim.trace import (ModelConfig, derive_workloads,  # noqa: E402
                           generate_synthetic_trace, topk_indices)
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))

@@ -1,10 +1,6 @@
 """Native CPU expert worker (AVX-512 BF16) vs a torch fp32 reference -- runs on
 the host, no GPU needed."""
 
-import ctypes
-import time
-
-import numpy as np
 import pytest
 import torch
 

@@ -1,5 +1,5 @@
 """Probe host memory bandwidth and CPU expert GEMV speed on the GPU box."""
-import os, time, torch, numpy as np
+import os, time, torch
 torch.set_num_threads(len(os.sched_getaffinity(0)))
 a = torch.empty(1 << 30, dtype=torch.uint8); a.fill_(1)
 b = torch.empty_like(a)
