@@ -325,9 +325,13 @@ class MoEExecMixin:
             lo, hi = min(lo, r0), max(hi, r1)
         if native and not self._cpu_async:          # synchronous (A/B switch)
             for e, r0, r1 in native:
+                t0 = time.perf_counter()
                 cpu_expert_rows(self._host_block(l, e).view(torch.bfloat16),
                                 rows_host[r0:r1], d, self.arch.ffn_dim, self.cpu_threads,
                                 out=out[r0:r1])
+                if self.cfg.trace_layers:
+                    self.stats.cpu_expert_ms.append((r1 - r0, (time.perf_counter() - t0) * 1e3,
+                                                     "native", t0))
             native = []
         if native:
             n = len(native)
@@ -348,8 +352,12 @@ class MoEExecMixin:
         d, f = a.hidden_dim, a.ffn_dim
         out = job["out"]
         for e, r0, r1 in job["big"]:
+            t0 = time.perf_counter()
             cpu_expert_rows(self._host_block(job["l"], e).view(torch.bfloat16),
                             job["rows"][r0:r1], d, f, self.cpu_threads, out=out[r0:r1])
+            if self.cfg.trace_layers:
+                self.stats.cpu_expert_ms.append((r1 - r0, (time.perf_counter() - t0) * 1e3,
+                                                 "big", t0))
         if job["native"]:
             _lib.call("dali_cpu_expert_wait")
         dev_rows = self._ws("cpu_rows_d", (R, d), torch.float32)

@@ -103,6 +103,7 @@ class RunStats:
     host_ms: dict = field(default_factory=dict)     # host-side time breakdown of _moe
     steps_meta: list = field(default_factory=list)  # (token_index, tokens, eos)
     layer_trace: list = field(default_factory=list)  # per-layer timeline (cfg.trace_layers)
+    cpu_expert_ms: list = field(default_factory=list)  # (rows, ms, kind, t0) per CPU expert (trace_layers)
 
 
 class _Staging:

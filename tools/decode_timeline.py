@@ -53,10 +53,8 @@ for it in range(2):
 torch.cuda.synchronize()
 lt = st.layer_trace
 L = eng.arch.num_layers
-rows = []
+rows, prows = [], []
 for i, r in enumerate(lt):
-    if r["T"] != 1:
-        continue
     tp = r["host"]
     ev_r, ev_dec, t0, ev_c = r["ev"]
     nxt = lt[i + 1] if i + 1 < len(lt) else None
@@ -71,7 +69,7 @@ for i, r in enumerate(lt):
              g_ffn_comb=t0.elapsed_time(ev_c) if t0 is not None else None,
              g_dec_comb=ev_dec.elapsed_time(ev_c),
              g_prev_comb_to_route=(lt[i - 1]["ev"][3].elapsed_time(ev_r) if i > 0 else None))
-    rows.append(d)
+    (rows if r["T"] == 1 else prows).append(d)
 
 
 def mean(key, rs):
@@ -98,6 +96,11 @@ summary["per_layer_wait"] = {l: mean("h_wait", rs) for l, rs in sorted(by_layer.
 summary["per_step_ms"] = {s: round(sum(r["h_launch"] + r["h_wait"] + r["h_disp"] + r["h_cpu"] +
                                        r["h_comb"] + (r["h_gap"] or 0)
                                        for r in rows if r["step"] == s), 2) for s in steps}
+summary["prefill_layers"] = [
+    {k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()} for r in prows]
+summary["cpu_expert_ms"] = [(int(r), round(float(ms), 3), kind, t0)
+                            for r, ms, kind, t0 in st.cpu_expert_ms]
+summary["cost_model_cpu"] = eng.cm.to_dict()["cpu_samples"]
 summary["stats"] = {k: getattr(st, k) for k in ("demand_copies", "prefetch_copies",
                                                   "replace_copies", "cpu_expert_calls",
                                                   "gpu_expert_calls")}
