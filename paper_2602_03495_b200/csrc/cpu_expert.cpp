@@ -10,6 +10,7 @@
 // barrier, phase 2 (W2 -> fp32 outputs).
 #include <immintrin.h>
 
+#include <algorithm>
 #include <atomic>
 #include <condition_variable>
 #include <cmath>
@@ -163,6 +164,15 @@ inline void row_dot(const uint16_t* w, const uint16_t* x, int64_t ldx, int K, in
   for (int r = 0; r < R; ++r) out[r] = _mm512_reduce_add_ps(acc[r]);
 }
 
+// DALI_CPU_DYNAMIC=0 selects the static per-thread partition (A/B switch)
+bool dynamic_chunks() {
+  static const bool v = [] {
+    const char* e = getenv("DALI_CPU_DYNAMIC");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 }  // namespace
 
 extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, const uint16_t* x,
@@ -183,31 +193,50 @@ extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, cons
   const uint16_t* w2 = block + (int64_t)2 * f * d;
   std::vector<uint16_t> hbuf((size_t)R * f);           // SwiGLU intermediate, bf16
   const int groups = f / 64;
-  // phase 1: group b = rows [128b, 128b+64) gate + [128b+64, 128b+128) up
-  pool->run([&](int tid) {
-    const int g0 = (int)((int64_t)groups * tid / nthreads);
-    const int g1 = (int)((int64_t)groups * (tid + 1) / nthreads);
+  auto group = [&](int b) {
     float gv[kMaxRows], uv[kMaxRows];
-    for (int b = g0; b < g1; ++b) {
-      for (int i = 0; i < 64; ++i) {
-        row_dot(w13 + (int64_t)(128 * b + i) * d, x, d, d, R, gv);
-        row_dot(w13 + (int64_t)(128 * b + 64 + i) * d, x, d, d, R, uv);
-        for (int r = 0; r < R; ++r) {
-          const float g = gv[r];
-          hbuf[(size_t)r * f + 64 * b + i] = f2bf(g / (1.0f + std::exp(-g)) * uv[r]);
-        }
+    for (int i = 0; i < 64; ++i) {
+      row_dot(w13 + (int64_t)(128 * b + i) * d, x, d, d, R, gv);
+      row_dot(w13 + (int64_t)(128 * b + 64 + i) * d, x, d, d, R, uv);
+      for (int r = 0; r < R; ++r) {
+        const float g = gv[r];
+        hbuf[(size_t)r * f + 64 * b + i] = f2bf(g / (1.0f + std::exp(-g)) * uv[r]);
       }
     }
-  });
-  // phase 2: y[r, m] = h_r . W2_m
-  pool->run([&](int tid) {
-    const int m0 = (int)((int64_t)d * tid / nthreads);
-    const int m1 = (int)((int64_t)d * (tid + 1) / nthreads);
+  };
+  auto down_rows = [&](int m0, int m1) {
     float acc[kMaxRows];
     for (int m = m0; m < m1; ++m) {
       row_dot(w2 + (int64_t)m * f, hbuf.data(), f, f, R, acc);
       for (int r = 0; r < R; ++r) y[(int64_t)r * d + m] = acc[r];
     }
+  };
+  if (dynamic_chunks()) {
+    // ~1 MB units handed out by an atomic counter: a vCPU the hypervisor
+    // preempts (or the caller's own thread) delays only the units it holds
+    constexpr int kDownRows = 32;
+    std::atomic<int> next_g{0}, next_m{0};
+    pool->run([&](int) {
+      for (int b = next_g.fetch_add(1, std::memory_order_relaxed); b < groups;
+           b = next_g.fetch_add(1, std::memory_order_relaxed))
+        group(b);
+    });
+    pool->run([&](int) {
+      for (int c = next_m.fetch_add(1, std::memory_order_relaxed); c * kDownRows < d;
+           c = next_m.fetch_add(1, std::memory_order_relaxed))
+        down_rows(c * kDownRows, std::min(d, (c + 1) * kDownRows));
+    });
+    return DALI_OK;
+  }
+  // static partition: phase 1 group b = rows [128b, 128b+64) gate +
+  // [128b+64, 128b+128) up; phase 2 y[r, m] = h_r . W2_m
+  pool->run([&](int tid) {
+    const int g0 = (int)((int64_t)groups * tid / nthreads);
+    const int g1 = (int)((int64_t)groups * (tid + 1) / nthreads);
+    for (int b = g0; b < g1; ++b) group(b);
+  });
+  pool->run([&](int tid) {
+    down_rows((int)((int64_t)d * tid / nthreads), (int)((int64_t)d * (tid + 1) / nthreads));
   });
   return DALI_OK;
 }
