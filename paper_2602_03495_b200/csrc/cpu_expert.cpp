@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -61,6 +62,13 @@ class Pool {
   // two phases of an expert and back-to-back experts of a layer start without
   // a futex wake-up; the caller spins on the completion count.
   void run(const std::function<void(int)>& fn) {
+    start(fn);
+    join(fn);
+  }
+  // start: workers 1..n-1 begin fn(tid) and the caller returns at once;
+  // join: the caller runs fn(0), then waits for the workers.  fn must stay
+  // alive until join returns.
+  void start(const std::function<void(int)>& fn) {
     fn_ = &fn;
     pending_.store(n_ - 1, std::memory_order_relaxed);
     {
@@ -68,6 +76,8 @@ class Pool {
       gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
+  }
+  void join(const std::function<void(int)>& fn) {
     fn(0);
     while (pending_.load(std::memory_order_acquire) != 0) _mm_pause();
   }
@@ -173,12 +183,15 @@ bool dynamic_chunks() {
   return v;
 }
 
+bool async_job_busy();
+
 }  // namespace
 
 extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, const uint16_t* x,
                                int32_t R, float* y, int32_t nthreads) {
   if (!block || !x || !y || d % 32 || f % 64 || R < 0) return DALI_ETRACE;
   if (R == 0) return DALI_OK;
+  if (async_job_busy()) return DALI_ESIM;           // the pool is running a submitted job
   if (R > kMaxRows) {
     for (int r0 = 0; r0 < R; r0 += kMaxRows) {
       const int n = R - r0 < kMaxRows ? R - r0 : kMaxRows;
@@ -242,82 +255,76 @@ extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, cons
 }
 
 // ---------------------------------------------------------------------------
-// Asynchronous submission: one dispatcher thread runs a list of experts on the
-// pool while the caller (the engine's Python thread) dispatches the GPU side
-// of the same layer; dali_cpu_expert_wait joins.  One job in flight at a time.
+// Asynchronous submission.  dali_cpu_expert_submit starts a layer's CPU
+// experts on the pool's worker threads and returns; the caller (the engine's
+// Python thread) dispatches the GPU side of the layer meanwhile and then
+// joins in dali_cpu_expert_wait, taking whatever work units are left.  The
+// job is a queue of stages -- (expert 0 gate/up), (expert 0 down), (expert
+// 1 gate/up), ... -- each split into ~1 MB units handed out by an atomic
+// counter; a stage opens when the previous one has finished, so a thread
+// that joins late simply starts at the current stage.  One job in flight.
 // ---------------------------------------------------------------------------
 namespace {
-struct CpuJob {
-  std::vector<const uint16_t*> blocks;
-  std::vector<const uint16_t*> xs;
+constexpr int kDownRows = 32;
+
+struct Stage {
+  int expert = 0, down = 0, units = 0;
+  std::atomic<int> next{0}, done{0};
+};
+
+struct StageJob {
+  int d = 0, f = 0, n_stages = 0;
+  std::vector<const uint16_t*> blocks, xs;
   std::vector<int32_t> rows;
   std::vector<float*> ys;
-  int32_t d = 0, f = 0, nthreads = 1;
-};
+  std::vector<std::vector<uint16_t>> hbuf;     // per expert: SwiGLU intermediate
+  std::unique_ptr<Stage[]> stages;
+  std::function<void(int)> fn;
+  Pool* pool = nullptr;
+  bool busy = false;
 
-class Dispatcher {
- public:
-  Dispatcher() : th_([this] { loop(); }) {}
-  ~Dispatcher() {
-    {
-      std::lock_guard<std::mutex> g(m_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    th_.join();
-  }
-  int submit(CpuJob&& job) {
-    std::unique_lock<std::mutex> lk(m_);
-    if (busy_) return DALI_ESIM;            // previous job not joined
-    job_ = std::move(job);
-    busy_ = true;
-    rc_ = DALI_OK;
-    lk.unlock();
-    cv_.notify_all();
-    return DALI_OK;
-  }
-  int wait() {
-    std::unique_lock<std::mutex> lk(m_);
-    done_.wait(lk, [this] { return !busy_; });
-    return rc_;
-  }
-
- private:
-  void loop() {
-    for (;;) {
-      CpuJob job;
-      {
-        std::unique_lock<std::mutex> lk(m_);
-        cv_.wait(lk, [this] { return stop_ || (busy_ && !running_); });
-        if (stop_) return;
-        running_ = true;
-        job = std::move(job_);
+  void unit(const Stage& st, int u) {
+    const int e = st.expert, R = rows[e];
+    const uint16_t* w13 = blocks[e];
+    const uint16_t* w2 = blocks[e] + (int64_t)2 * f * d;
+    uint16_t* h = hbuf[e].data();
+    float a[kMaxRows], b[kMaxRows];
+    if (!st.down) {                                 // gate/up group u
+      for (int i = 0; i < 64; ++i) {
+        row_dot(w13 + (int64_t)(128 * u + i) * d, xs[e], d, d, R, a);
+        row_dot(w13 + (int64_t)(128 * u + 64 + i) * d, xs[e], d, d, R, b);
+        for (int r = 0; r < R; ++r)
+          h[(size_t)r * f + 64 * u + i] = f2bf(a[r] / (1.0f + std::exp(-a[r])) * b[r]);
       }
-      int rc = DALI_OK;
-      for (size_t i = 0; i < job.blocks.size() && rc == DALI_OK; ++i)
-        rc = dali_cpu_expert(job.blocks[i], job.d, job.f, job.xs[i], job.rows[i], job.ys[i],
-                             job.nthreads);
-      {
-        std::lock_guard<std::mutex> g(m_);
-        rc_ = rc;
-        running_ = false;
-        busy_ = false;
+    } else {                                        // down rows [32u, 32u+32)
+      const int m1 = std::min(d, (u + 1) * kDownRows);
+      for (int m = u * kDownRows; m < m1; ++m) {
+        row_dot(w2 + (int64_t)m * f, h, f, f, R, a);
+        for (int r = 0; r < R; ++r) ys[e][(int64_t)r * d + m] = a[r];
       }
-      done_.notify_all();
     }
   }
-  std::mutex m_;
-  std::condition_variable cv_, done_;
-  CpuJob job_;
-  bool busy_ = false, running_ = false, stop_ = false;
-  int rc_ = DALI_OK;
-  std::thread th_;
+  void work() {
+    for (int s = 0; s < n_stages; ++s) {
+      Stage& st = stages[s];
+      if (s > 0) {
+        const Stage& pv = stages[s - 1];
+        while (pv.done.load(std::memory_order_acquire) < pv.units) _mm_pause();
+      }
+      for (int u = st.next.fetch_add(1, std::memory_order_relaxed); u < st.units;
+           u = st.next.fetch_add(1, std::memory_order_relaxed)) {
+        unit(st, u);
+        st.done.fetch_add(1, std::memory_order_release);
+      }
+    }
+  }
 };
 
-Dispatcher& dispatcher() {
-  static Dispatcher d;
-  return d;
+StageJob& stage_job() {
+  static StageJob j;
+  return j;
 }
+bool async_job_busy() { return stage_job().busy; }
 }  // namespace
 
 extern "C" int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const uint64_t* xs,
@@ -325,17 +332,44 @@ extern "C" int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const u
                                       int32_t f, int32_t nthreads) {
   if (n < 0 || (n > 0 && (!blocks || !xs || !rows || !ys)) || d % 32 || f % 64)
     return DALI_ETRACE;
-  CpuJob job;
-  job.d = d;
-  job.f = f;
-  job.nthreads = nthreads;
+  StageJob& j = stage_job();
+  if (j.busy) return DALI_ESIM;                     // previous job not joined
+  for (int i = 0; i < n; ++i)
+    if (rows[i] < 0 || rows[i] > kMaxRows) return DALI_ETRACE;
+  j.d = d;
+  j.f = f;
+  j.blocks.assign(n, nullptr);
+  j.xs.assign(n, nullptr);
+  j.ys.assign(n, nullptr);
+  j.rows.assign(rows, rows + n);
+  j.hbuf.resize(n);
+  j.n_stages = 2 * n;
+  j.stages.reset(new Stage[std::max(1, 2 * n)]);
   for (int i = 0; i < n; ++i) {
-    job.blocks.push_back(reinterpret_cast<const uint16_t*>(blocks[i]));
-    job.xs.push_back(reinterpret_cast<const uint16_t*>(xs[i]));
-    job.rows.push_back(rows[i]);
-    job.ys.push_back(reinterpret_cast<float*>(ys[i]));
+    j.blocks[i] = reinterpret_cast<const uint16_t*>(blocks[i]);
+    j.xs[i] = reinterpret_cast<const uint16_t*>(xs[i]);
+    j.ys[i] = reinterpret_cast<float*>(ys[i]);
+    j.hbuf[i].resize((size_t)std::max(rows[i], 1) * f);
+    Stage& up = j.stages[2 * i];
+    up.expert = i;
+    up.down = 0;
+    up.units = rows[i] > 0 ? f / 64 : 0;
+    Stage& dn = j.stages[2 * i + 1];
+    dn.expert = i;
+    dn.down = 1;
+    dn.units = rows[i] > 0 ? (d + kDownRows - 1) / kDownRows : 0;
   }
-  return dispatcher().submit(std::move(job));
+  j.pool = pool_for(nthreads < 1 ? 1 : nthreads);
+  j.fn = [&j](int) { j.work(); };
+  j.busy = true;
+  j.pool->start(j.fn);
+  return DALI_OK;
 }
 
-extern "C" int dali_cpu_expert_wait(void) { return dispatcher().wait(); }
+extern "C" int dali_cpu_expert_wait(void) {
+  StageJob& j = stage_job();
+  if (!j.busy) return DALI_OK;
+  j.pool->join(j.fn);
+  j.busy = false;
+  return DALI_OK;
+}

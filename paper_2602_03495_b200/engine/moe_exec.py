@@ -351,6 +351,8 @@ class MoEExecMixin:
         a = self.arch
         d, f = a.hidden_dim, a.ffn_dim
         out = job["out"]
+        if job["native"]:
+            _lib.call("dali_cpu_expert_wait")       # join the pool before oneDNN's threads run
         for e, r0, r1 in job["big"]:
             t0 = time.perf_counter()
             cpu_expert_rows(self._host_block(job["l"], e).view(torch.bfloat16),
@@ -358,8 +360,6 @@ class MoEExecMixin:
             if self.cfg.trace_layers:
                 self.stats.cpu_expert_ms.append((r1 - r0, (time.perf_counter() - t0) * 1e3,
                                                  "big", t0))
-        if job["native"]:
-            _lib.call("dali_cpu_expert_wait")
         dev_rows = self._ws("cpu_rows_d", (R, d), torch.float32)
         lo, hi = job["lo"], job["hi"]
         if hi > lo:
@@ -449,8 +449,10 @@ class MoEExecMixin:
             self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
         offs_np = hv["offsets"].numpy()
         if self._cpu_async:
-            # the CPU experts start first and run on the pool while this thread
-            # dispatches the GPU experts and copies of the same layer
+            # the CPU experts start first on the pool's workers while this
+            # thread dispatches the GPU experts and copies of the same layer;
+            # _cpu_finish then joins the pool (this thread takes the remaining
+            # work units)
             job = self._cpu_submit(l, xp_host, offs_np, rec, R)
             try:
                 yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)

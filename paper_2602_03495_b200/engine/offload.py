@@ -93,6 +93,7 @@ class RunStats:
     insert_copies: int = 0                 # D2D staging -> slot (baseline cache policies)
     cpu_expert_calls: int = 0
     gpu_expert_calls: int = 0
+    decode_host_bytes: int = 0             # expert bytes read from host DRAM while decoding
     dali_launches: int = 0
     initial_on_gpu: np.ndarray | None = None
     captured: list = field(default_factory=list)    # (step, layer, h (T,d) bf16 cpu)
@@ -182,7 +183,10 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         # decode token on the 16-vCPU boxes: the Python thread's GPU dispatch
         # preempts a pool thread and the pool's phase barrier waits for it.
         # Off by default; DALI_CPU_ASYNC=1 enables it.
-        self._cpu_async = os.environ.get("DALI_CPU_ASYNC", "0") == "1"
+        # decode-sized CPU experts start on the pool's workers before the GPU
+        # dispatch and the Python thread joins them afterwards (DALI_CPU_ASYNC=0:
+        # dispatch first, then run them synchronously -- A/B switch)
+        self._cpu_async = os.environ.get("DALI_CPU_ASYNC", "1") == "1"
         torch.set_num_threads(self.cpu_threads)
         # per-layer pinned scratch for pointer table + G mask
         row = (N * 17 + 63) // 64 * 64        # ptrs | maps | G mask, 64-B aligned rows
@@ -421,6 +425,9 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         if self.cfg.capture:
             self.stats.logits.append(logits.float().cpu())
         e1.record(cs)
+        st0 = self.stats
+        blocks0 = (st0.cpu_expert_calls + st0.demand_copies + st0.prefetch_copies +
+                   st0.replace_copies)
         for i in range(max_new_tokens - 1):
             logits = self.decode(nxt, is_eos=(i == max_new_tokens - 2))
             nxt = logits.argmax(-1)
@@ -437,6 +444,10 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         st.prefill_tokens = B * S
         st.decode_tokens = B * max(max_new_tokens - 1, 0)
         st.dali_launches = _lib.launch_count() - l0
+        # expert blocks the decode phase streamed out of host DRAM (CPU experts
+        # + H2D copies): the shared host-memory roofline of offloaded decode
+        st.decode_host_bytes = ((st.cpu_expert_calls + st.demand_copies + st.prefetch_copies +
+                                 st.replace_copies - blocks0) * self.arch.expert_bytes)
         return torch.stack(out, dim=1), st
 
     # ------------------------------------------------------------- reporting

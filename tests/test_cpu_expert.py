@@ -27,3 +27,41 @@ def test_cpu_expert_matches_fp32_reference(d, f, R):
     _lib.call("dali_cpu_expert", block.data_ptr(), d, f, x.data_ptr(), R, y.data_ptr(), 4)
     ref = M.expert_forward(x.float(), block, d, f)
     torch.testing.assert_close(y, ref, rtol=2e-2, atol=2e-2 * ref.abs().max().item())
+
+
+@pytest.mark.skipif(not _has_bf16(), reason="host CPU lacks AVX512-BF16")
+@pytest.mark.parametrize("late_ms", [0.0, 5.0])
+def test_cpu_expert_submit_wait_matches_sync(late_ms):
+    """Asynchronous submission (workers start, the caller joins late and takes
+    the remaining units) gives bit-identical rows to the synchronous call, for
+    a layer's worth of experts with different row counts; a synchronous call
+    while a job is in flight is refused."""
+    import time
+
+    import numpy as np
+    d, f = 512, 1408
+    g = torch.Generator().manual_seed(11)
+    rows = [1, 3, 0, 16, 2]
+    blocks = [(torch.randn(3 * f * d, generator=g) * 0.05).to(torch.bfloat16) for _ in rows]
+    xs = [torch.randn(max(r, 1), d, generator=g).to(torch.bfloat16) for r in rows]
+    ys = [torch.full((max(r, 1), d), float("nan")) for r in rows]
+    refs = []
+    for b, x, r in zip(blocks, xs, rows):
+        y = torch.zeros(max(r, 1), d)
+        _lib.call("dali_cpu_expert", b.data_ptr(), d, f, x.data_ptr(), r, y.data_ptr(), 4)
+        refs.append(y)
+    for _ in range(3):
+        p = lambda ts: np.array([t.data_ptr() for t in ts], np.uint64)  # noqa: E731
+        bp, xp, yp = p(blocks), p(xs), p(ys)
+        rp = np.array(rows, np.int32)
+        _lib.call("dali_cpu_expert_submit", len(rows), bp.ctypes.data, xp.ctypes.data,
+                  rp.ctypes.data, yp.ctypes.data, d, f, 4)
+        y1 = torch.empty(1, d)
+        rc = _lib.load().dali_cpu_expert(blocks[0].data_ptr(), d, f, xs[0].data_ptr(), 1,
+                                         y1.data_ptr(), 4)
+        assert rc != 0                       # pool busy: refused, not corrupted
+        time.sleep(late_ms / 1e3)
+        _lib.call("dali_cpu_expert_wait")
+        for r, y, ref in zip(rows, ys, refs):
+            if r:
+                assert torch.equal(y[:r], ref[:r])
