@@ -100,9 +100,14 @@ template <int BN>
 struct Smem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
-  // BN <= 64: 4 stages so 2-3 CTAs share an SM (decode weight streaming);
-  // BN 128: one CTA per SM with a deeper ring; BN 256: 4 x 48 KB.
-  static constexpr int STAGES = BN == 128 ? 6 : 4;
+  // BN <= 32 (decode weight streaming): 5 stages = 90-100 KB, so two CTAs
+  // still share an SM (measured: 4 -> 5 stages +2% at every decode shape, 6
+  // stages drops to one CTA per SM and loses 12%); BN 64: 4 stages; BN 128:
+  // one CTA per SM with a deeper ring; BN 256: 4 x 48 KB.
+#ifndef DALI_FFN_STAGES_SMALL
+#define DALI_FFN_STAGES_SMALL 5
+#endif
+  static constexpr int STAGES = BN == 128 ? 6 : BN <= 32 ? DALI_FFN_STAGES_SMALL : 4;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr size_t BYTES =
       (size_t)STAGES * (A_BYTES + B_BYTES) + 64 * 17 * 4 + 1024 /*align*/ + 256 /*bars*/;
