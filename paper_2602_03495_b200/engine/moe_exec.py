@@ -308,40 +308,50 @@ class MoEExecMixin:
         experts (<= NATIVE_MAX_ROWS rows) go to the native pool asynchronously
         (``dali_cpu_expert_submit``) so the caller dispatches the GPU side of
         the layer meanwhile; prefill-sized ones are returned for the oneDNN
-        path.  Returns the job description for ``_cpu_finish``."""
-        Cx = np.flatnonzero(np.frombuffer(rec.C, dtype=np.int8, count=self.NL)).tolist()
-        if not Cx or R == 0:
+        path.  Returns the job description for ``_cpu_finish``.  This sits on
+        the decode critical path between the decision and the first CPU byte,
+        so the submission arrays are preallocated and filled in place."""
+        C = np.frombuffer(rec.C, dtype=np.int8, count=self.NL)
+        if R == 0 or not C.any():
             return None
-        d = self.arch.hidden_dim
+        a = self.arch
+        d, f = a.hidden_dim, a.ffn_dim
         out = self._ws("cpu_rows_h", (R, d), torch.float32, pinned=True)
-        native, big = [], []
+        sub = self._cpu_sub
+        if sub is None:
+            arrs = (np.zeros(self.NL, np.uint64), np.zeros(self.NL, np.uint64),
+                    np.zeros(self.NL, np.int32), np.zeros(self.NL, np.uint64))
+            sub = self._cpu_sub = (arrs, tuple(x.ctypes.data for x in arrs),
+                                   _lib.load().dali_cpu_expert_submit)
+        (blocks, xs, rows, ys), addrs, submit = sub
+        xbase, obase = rows_host.data_ptr(), out.data_ptr()
+        n, big = 0, []
         lo, hi = R, 0
-        for e in Cx:
+        for e in np.flatnonzero(C).tolist():
             r0, r1 = int(offs_np[e]), int(offs_np[e + 1])
             if r1 <= r0:
                 continue
-            (native if r1 - r0 <= NATIVE_MAX_ROWS else big).append((e, r0, r1))
             self.stats.cpu_expert_calls += 1
             lo, hi = min(lo, r0), max(hi, r1)
-        if native and not self._cpu_async:          # synchronous (A/B switch)
-            for e, r0, r1 in native:
+            if r1 - r0 > NATIVE_MAX_ROWS:
+                big.append((e, r0, r1))
+            elif self._cpu_async:
+                blocks[n] = self.w.expert_host_ptr(l, e)
+                xs[n] = xbase + r0 * d * 2
+                rows[n] = r1 - r0
+                ys[n] = obase + r0 * d * 4
+                n += 1
+            else:                                   # synchronous (A/B switch)
                 t0 = time.perf_counter()
                 cpu_expert_rows(self._host_block(l, e).view(torch.bfloat16),
-                                rows_host[r0:r1], d, self.arch.ffn_dim, self.cpu_threads,
-                                out=out[r0:r1])
+                                rows_host[r0:r1], d, f, self.cpu_threads, out=out[r0:r1])
                 if self.cfg.trace_layers:
                     self.stats.cpu_expert_ms.append((r1 - r0, (time.perf_counter() - t0) * 1e3,
                                                      "native", t0))
-            native = []
-        if native:
-            n = len(native)
-            blocks = np.array([self.w.expert_host_ptr(l, e) for e, _, _ in native], np.uint64)
-            xs = np.array([rows_host[r0].data_ptr() for _, r0, _ in native], np.uint64)
-            rows = np.array([r1 - r0 for _, r0, r1 in native], np.int32)
-            ys = np.array([out[r0].data_ptr() for _, r0, _ in native], np.uint64)
-            _lib.call("dali_cpu_expert_submit", n, blocks.ctypes.data, xs.ctypes.data,
-                      rows.ctypes.data, ys.ctypes.data, d, self.arch.ffn_dim, self.cpu_threads)
-        return dict(out=out, native=bool(native), big=big, lo=lo, hi=hi, l=l, rows=rows_host)
+        if n:
+            _lib.check(submit(n, addrs[0], addrs[1], addrs[2], addrs[3], d, f, self.cpu_threads),
+                       "dali_cpu_expert_submit")
+        return dict(out=out, native=n > 0, big=big, lo=lo, hi=hi, l=l, rows=rows_host)
 
     def _cpu_finish(self, job, R: int) -> torch.Tensor | None:
         """Run the prefill-sized CPU experts, join the asynchronous ones and
@@ -442,18 +452,26 @@ class MoEExecMixin:
         ev_dec.synchronize()
         tp2 = time.perf_counter()
         rec = self.policy.record(ri)
-        wl_np = hv["wl"].numpy().copy()
-        self.stats.workloads[(step, l)] = wl_np
-        if self.cfg.capture:
-            self.stats.captured.append((step, l, views["h_host"].clone()))
-            self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
         offs_np = hv["offsets"].numpy()
+        job = None
         if self._cpu_async:
             # the CPU experts start first on the pool's workers while this
             # thread dispatches the GPU experts and copies of the same layer;
             # _cpu_finish then joins the pool (this thread takes the remaining
             # work units)
             job = self._cpu_submit(l, xp_host, offs_np, rec, R)
+        tp_sub = time.perf_counter()
+        try:
+            wl_np = hv["wl"].numpy().copy()
+            self.stats.workloads[(step, l)] = wl_np
+            if self.cfg.capture:
+                self.stats.captured.append((step, l, views["h_host"].clone()))
+                self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
+        except BaseException:
+            if job is not None and job["native"]:
+                _lib.load().dali_cpu_expert_wait()
+            raise
+        if self._cpu_async:
             try:
                 yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
                 y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
@@ -484,7 +502,7 @@ class MoEExecMixin:
             self.stats.layer_trace.append(dict(
                 step=step, layer=l, T=T, nC=int(sum(1 for e in range(N) if rec.C[e] and wl_np[e])),
                 hit=le["hit"], pf=le["pf"], dem=le["dem"], rep=le["rep"], done=le["done"],
-                host=(tp0, tp1, tp2, tp3, tp4, time.perf_counter()),
+                host=(tp0, tp1, tp2, tp3, tp4, time.perf_counter()), tp_sub=tp_sub,
                 ev=(ev_r if ev_r is not None else ev_dec, ev_dec, le["t0"], ev_c)))
         return out
 
