@@ -447,11 +447,14 @@ int dali_ep_gather_back(const float* ret, const int32_t* offsets, int32_t N, int
 int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f,
                     const uint16_t* x, int32_t R, float* y, int32_t nthreads);
 
-/* Asynchronous form for the engine: run experts i < n (block[i], rows x[i]
- * (rows[i], d) bf16 -> y[i] (rows[i], d) f32, [host] pointers as uint64) on
- * the worker pool from a dispatcher thread and return immediately, so the
- * caller can dispatch the GPU side of the same layer; dali_cpu_expert_wait
- * joins (returns the first failing status).  One submission in flight. */
+/* Asynchronous form for the engine: experts i < n (block[i], rows x[i]
+ * (rows[i] <= 16, d) bf16 -> y[i] (rows[i], d) f32, [host] pointers as
+ * uint64) start on the pool's worker threads and the call returns at once,
+ * so the caller can dispatch the GPU side of the same layer.  The work is a
+ * queue of stages (expert i gate/up, expert i down, ...) cut into ~1 MB
+ * units; dali_cpu_expert_wait makes the caller take the remaining units and
+ * returns when all are done.  One submission in flight: a second submit, or
+ * a synchronous dali_cpu_expert call, before the wait returns DALI_ESIM. */
 int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const uint64_t* xs,
                            const int32_t* rows, const uint64_t* ys, int32_t d,
                            int32_t f, int32_t nthreads);
