@@ -26,6 +26,7 @@ ap.add_argument("--model", default="mixtral-8x7b")
 ap.add_argument("--cache-gb", type=float, default=24.0)
 ap.add_argument("--prefill", type=int, default=512)
 ap.add_argument("--decode", type=int, default=48)
+ap.add_argument("--prefetch", type=int, default=1)
 ap.add_argument("--out", default="gpurun_out/timeline.json")
 ap.add_argument("--cost-model", default=None,
                 help="cost-model JSON: loaded if it exists, else profiled and saved there "
@@ -37,7 +38,7 @@ if args.cost_model and os.path.exists(args.cost_model):
     cm = load_cost_model(args.cost_model)
 
 cores = len(os.sched_getaffinity(0))
-cfg = EngineConfig(cache_gb=args.cache_gb, prefetch_size=1, w_size=4, seed=0,
+cfg = EngineConfig(cache_gb=args.cache_gb, prefetch_size=args.prefetch, w_size=4, seed=0,
                    cpu_threads=cores, trace_layers=True)
 eng = build_engine(args.model, cfg, seed=0, max_seq=args.prefill + args.decode + 8,
                    log=lambda *a: print(*a, file=sys.stderr), cost_model=cm)
