@@ -226,6 +226,50 @@ def cpu_reference(args, steps: int, warmup: int):
     return res
 
 
+def policy_layer_us(args, eng) -> dict:
+    """the reference policy's per-layer decision time on
+    the host (gating, greedy, residual prediction, cache update; oracle
+    restatement, best of 5) at this config's decode and prefill T."""
+    from oracle.cpu_reference import policy_layer_timing
+    a = eng.arch
+    kw = dict(d=a.hidden_dim, N=a.num_experts, k=a.top_k,
+              capacity=max(eng.slots_per_layer, 1),
+              prefetch_size=args.prefetch)
+    return {"decode_T%d" % args.batch: policy_layer_timing(tokens=args.batch, **kw),
+            "prefill_T%d" % (args.batch * args.prefill):
+                policy_layer_timing(tokens=args.batch * args.prefill, **kw)}
+
+
+def device_decision_us(eng, reps: int = 200) -> float | None:
+    """Device counterpart of policy_layer_us at decode: one layer's decision
+    path -- routing (fp64 gating + top-k + histogram), residual prediction for
+    layer+1, the fused policy kernel (greedy + lookups + prefetch window +
+    cache update), plan/permute and the D2H mirrors the host reads -- as the
+    decode step runs it (CUDA graph, PDL), timed by events over ``reps``
+    replays.  Runs after the timed passes (it rewrites the last record)."""
+    if eng.resident_mode or not getattr(eng, "_heads", None):
+        return None
+    a = eng.arch
+    h = eng._ws("h", (1, a.hidden_dim), torch.bfloat16)
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    eng._capturing = True
+    try:
+        with torch.cuda.graph(g):
+            eng._moe_head(0, h, 0, 0, False, use_desc=True)
+    finally:
+        eng._capturing = False
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    e1.synchronize()
+    return round(e0.elapsed_time(e1) * 1e3 / reps, 2)
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
@@ -384,7 +428,9 @@ def run_dali(args, ws, rank, local):
         r = cpu_reference(args, 1, 0)
         cpu_base = {"value": round(r["decode_tokens_per_s"], 4), "unit": "tokens/s",
                     "cores": r["threads"], "kind": "port", "sample": r["sample"],
-                    "prefill_tokens_per_s": round(r["prefill_tokens_per_s"], 3)}
+                    "prefill_tokens_per_s": round(r["prefill_tokens_per_s"], 3),
+                    "policy_layer_us": policy_layer_us(args, eng),
+                    "device_decision_us_per_layer": device_decision_us(eng)}
     if rank == 0:
         line = {
             "metric": metric_name(args), "value": round(dec_v, 4), "unit": "tokens/s", "n_gpus": ws,

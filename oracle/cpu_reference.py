@@ -126,3 +126,42 @@ def run_sample(arch_dims: dict, total_layers: int, prefill: int, decode_steps: i
             "sample": f"{sample_layers} of {total_layers} layers (time x{total_layers}/"
                       f"{sample_layers}), prefill {prefill} x B{batch}, {decode_steps} decode "
                       f"steps, all experts on CPU, fp64 reference gating"}
+
+
+def policy_layer_timing(d: int, N: int, k: int, capacity: int, prefetch_size: int,
+                        tokens: int = 1, reps: int = 5, seed: int = 0) -> dict:
+    """Per-layer decision latency of the reference policy on the host
+    (SURVEY.md section 8d (i)): gating A4 (trace.py:229-265), greedy A6-A8
+    (cost_model.py:70-96, assignment.py:53-199), residual prediction A11
+    (prefetch.py:107-156) and the cache window update A16 (cache.py:146-214),
+    restated in oracle.policy; 1 warm-up + best of ``reps`` per function, in
+    microseconds.  ``tokens`` = T of the layer (1 for B=1 decode)."""
+    rng = np.random.default_rng(seed)
+    h = rng.standard_normal((tokens, d))
+    gate = rng.standard_normal((d, N)) * (0.4 / math.sqrt(d))
+    gate_next = rng.standard_normal((d, N)) * (0.4 / math.sqrt(d))
+    res = rng.standard_normal(d) * 0.01
+    tables = P.default_tables()
+    cache = P.new_cache(0, N, capacity, 4, P.default_u_size(N, capacity), seed=seed)
+    wl = P.derive_workloads(h, gate, k)
+    cpu_t, gpu_t = P.expert_times(tables, wl, cache.on_gpu)
+
+    def best(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - t0) * 1e6)
+        return min(ts)
+
+    out = {
+        "gating_A4": best(lambda: P.derive_workloads(h, gate, k)),
+        "greedy_A6_A8": best(lambda: P.greedy(wl, cache.on_gpu,
+                                              *P.expert_times(tables, wl, cache.on_gpu),
+                                              capacity)),
+        "prefetch_A11": best(lambda: P.predict_next(h, res, gate_next, k, prefetch_size)),
+        "cache_A16": best(lambda: P.window_update(cache, wl, False)),
+    }
+    out["total"] = sum(out.values())
+    return {key: round(v, 2) for key, v in out.items()}
