@@ -119,6 +119,9 @@ struct Tile {
 
 // Locate this CTA's (expert, m-tile, n-tile, split) from the per-expert row
 // offsets; experts whose map is 0 (not on the GPU) contribute no tiles.
+// Order within an expert: split, then token tile, then weight tile, so the
+// token tiles that share one weight tile run on neighbouring CTAs at the same
+// time and the weight tile comes from DRAM once (L2 serves the others).
 template <int BN>
 __device__ bool find_tile(const int32_t* offs, const uint64_t* maps, int N, int m_tiles,
                           int splits, Tile& t, int idx) {
@@ -126,13 +129,14 @@ __device__ bool find_tile(const int32_t* offs, const uint64_t* maps, int N, int 
     if (!maps[e]) continue;
     const int ne = offs[e + 1] - offs[e];
     if (ne <= 0) continue;
-    const int cnt = ((ne + BN - 1) / BN) * m_tiles * splits;
+    const int n_tiles_e = (ne + BN - 1) / BN;
+    const int cnt = n_tiles_e * m_tiles * splits;
     if (idx < cnt) {
       t.e = e;
       t.split = idx % splits;
       idx /= splits;
-      t.m_tile = idx % m_tiles;
-      const int nt = idx / m_tiles;
+      const int nt = idx % n_tiles_e;
+      t.m_tile = idx / n_tiles_e;
       t.row0 = offs[e] + nt * BN;
       t.n_valid = min(BN, ne - nt * BN);
       return true;

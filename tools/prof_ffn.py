@@ -24,6 +24,7 @@ ap.add_argument("--kernel", default="tc")
 ap.add_argument("--d", type=int, default=4096)
 ap.add_argument("--f", type=int, default=14336)
 ap.add_argument("--splits", type=int, default=0, help="override the split-K planes")
+ap.add_argument("--counts", default=None, help="RxE: R tokens on each of E experts (e.g. 512x8)")
 args = ap.parse_args()
 d, f, N = args.d, args.f, 8
 dev = torch.device("cuda")
@@ -82,6 +83,9 @@ def run(counts, label):
           f"{flops / ms / 1e9:.1f} TFLOP/s, bytes {byts}")
 
 
+if args.counts:
+    r_, e_ = (int(x) for x in args.counts.split("x"))
+    run([r_] * e_ + [0] * (N - e_), f"counts {args.counts}")
 if args.mode == "one":
     run([1, 0, 0, 0, 0, 0, 0, 0], "decode 1x1")
 if args.mode in ("decode", "both"):
