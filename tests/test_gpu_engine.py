@@ -173,6 +173,7 @@ def test_engine_kernel_pieces_vs_torch():
     (512, 1408, [17, 40, 0, 64, 1, 30, 0, 2], 11),
     (256, 512, [100, 128, 129, 0, 3, 60, 250, 300], 4),
     (4096, 1024, [1, 1, 0, 0, 0, 0, 0, 0], 8),
+    (256, 512, [600, 7, 0, 513, 0, 0, 1, 0], 1),          # 3 token tiles per weight tile
 ])
 def test_tc_ffn_matches_simt_and_torch(d, f, counts, splits):
     """tcgen05/TMA grouped FFN vs the CUDA-core kernel and a torch fp32 reference."""
