@@ -491,31 +491,47 @@ def run_dali(args, ws, rank, local):
                          "launches": len(durs),
                          "avg_launch_ms": avg_ms, "algorithmic_bytes_per_launch": avg_b,
                          "share_of_step": round(total_ffn_ms / ms_v, 4) if ms_v else None},
-            "host_dram_roofline": host_dram_roofline(eng, st_v),
+            "offload_roofline": offload_roofline(eng, st_v),
             "clocks": clocks,
             "cpu_baseline": cpu_base,
         }
         emit(line)
 
 
-def host_dram_roofline(eng, st_v) -> dict | None:
+def offload_roofline(eng, st_v) -> dict | None:
     """Offloaded decode streams every CPU-assigned expert and every H2D expert
     copy out of host DRAM, and the two share it: on the GPU box CPU experts
     alone read ~190 GB/s and CPU experts + DMA together read the same total
     (profiles/r01_zero_copy_probe.log).  Peak = one expert block / the
-    profiled t_cpu(1) (the warmed-up single-token CPU expert)."""
+    profiled t_cpu(1) (the warmed-up single-token CPU expert).  The H2D copies
+    are also bounded by PCIe (profiled trans_time): ``pcie_floor_tokens_per_s``;
+    ``floor_tokens_per_s`` is the lower of the two floors."""
     t1 = eng.cm.t_cpu(1)
     ms = float(np.sum([s.decode_ms for s in st_v]))
     byts = float(np.sum([s.decode_host_bytes for s in st_v]))
+    h2d = float(np.sum([s.decode_h2d_bytes for s in st_v]))
     toks = float(np.sum([s.decode_tokens for s in st_v]))
     if t1 <= 0 or ms <= 0 or toks <= 0 or byts <= 0:
         return None
     peak = eng.w.expert_bytes / (t1 * 1e-3) / 1e9
     achieved = byts / (ms * 1e-3) / 1e9
-    return {"bound": "host_dram", "unit": "GB/s", "achieved": round(achieved, 2),
-            "peak": round(peak, 2), "peak_kind": "expert block / profiled t_cpu(1)",
-            "frac": round(achieved / peak, 4), "bytes_per_token": round(byts / toks),
-            "floor_tokens_per_s": round(peak * 1e9 / (byts / toks), 3)}
+    host_floor = peak * 1e9 / (byts / toks)
+    out = {"bound": "host_dram", "unit": "GB/s", "achieved": round(achieved, 2),
+           "peak": round(peak, 2), "peak_kind": "expert block / profiled t_cpu(1)",
+           "frac": round(achieved / peak, 4), "bytes_per_token": round(byts / toks),
+           "host_floor_tokens_per_s": round(host_floor, 3)}
+    floor = host_floor
+    if h2d > 0 and eng.cm.trans_time > 0:
+        pcie = eng.w.expert_bytes / (eng.cm.trans_time * 1e-3) / 1e9
+        pcie_floor = pcie * 1e9 / (h2d / toks)
+        out.update({"pcie_bytes_per_token": round(h2d / toks), "pcie_gbs": round(pcie, 2),
+                    "pcie_floor_tokens_per_s": round(pcie_floor, 3)})
+        floor = min(floor, pcie_floor)
+        if pcie_floor < host_floor:
+            out["bound"] = "pcie"
+    out["floor_tokens_per_s"] = round(floor, 3)
+    out["frac_of_floor"] = round(toks / (ms * 1e-3) / floor, 4)
+    return out
 
 
 def main():

@@ -94,6 +94,7 @@ class RunStats:
     cpu_expert_calls: int = 0
     gpu_expert_calls: int = 0
     decode_host_bytes: int = 0             # expert bytes read from host DRAM while decoding
+    decode_h2d_bytes: int = 0              # of which H2D expert copies (PCIe)
     dali_launches: int = 0
     initial_on_gpu: np.ndarray | None = None
     captured: list = field(default_factory=list)    # (step, layer, h (T,d) bf16 cpu)
@@ -427,8 +428,8 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
             self.stats.logits.append(logits.float().cpu())
         e1.record(cs)
         st0 = self.stats
-        blocks0 = (st0.cpu_expert_calls + st0.demand_copies + st0.prefetch_copies +
-                   st0.replace_copies)
+        copies0 = st0.demand_copies + st0.prefetch_copies + st0.replace_copies
+        blocks0 = st0.cpu_expert_calls + copies0
         for i in range(max_new_tokens - 1):
             logits = self.decode(nxt, is_eos=(i == max_new_tokens - 2))
             nxt = logits.argmax(-1)
@@ -447,8 +448,9 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         st.dali_launches = _lib.launch_count() - l0
         # expert blocks the decode phase streamed out of host DRAM (CPU experts
         # + H2D copies): the shared host-memory roofline of offloaded decode
-        st.decode_host_bytes = ((st.cpu_expert_calls + st.demand_copies + st.prefetch_copies +
-                                 st.replace_copies - blocks0) * self.arch.expert_bytes)
+        copies = st.demand_copies + st.prefetch_copies + st.replace_copies
+        st.decode_host_bytes = (st.cpu_expert_calls + copies - blocks0) * self.arch.expert_bytes
+        st.decode_h2d_bytes = (copies - copies0) * self.arch.expert_bytes
         return torch.stack(out, dim=1), st
 
     # ------------------------------------------------------------- reporting
