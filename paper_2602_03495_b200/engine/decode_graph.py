@@ -100,18 +100,22 @@ class DecodeGraphMixin:
                 ev_r.record(cs)
             tp0 = time.perf_counter()
             if l in heads:
-                g, h, views = heads[l]
+                g, h, views, nk = heads[l]
                 g.replay()
+                self.graph_kernels += nk
             elif capture:
                 g = torch.cuda.CUDAGraph()
                 self._capturing = True
+                k0 = _lib.launch_count()
                 try:
                     with torch.cuda.graph(g):
                         h, views = self._decode_head(l, X, X2, B)
                 finally:
                     self._capturing = False
+                nk = _lib.launch_count() - k0         # our kernels in the graph body
                 g.replay()
-                heads[l] = (g, h, views)
+                self.graph_kernels += nk
+                heads[l] = (g, h, views, nk)
             else:
                 h, views = self._decode_head(l, X, X2, B)
             self._moe_tail(l, X2, h, step, views, tp0, ev_r, X)
@@ -144,6 +148,7 @@ class DecodeGraphMixin:
         if self._graph is not None:
             self._graph_in.copy_(tok_dev.view(B))
             self._graph.replay()
+            self.graph_kernels += self._graph_nk
             self.policy.n_records += L
             return self._graph_logits
         if not getattr(self, "_graph_warm", False):
@@ -162,15 +167,18 @@ class DecodeGraphMixin:
         self._in_capture = True
         n0 = self.policy.n_records
         self._capturing = True
+        k0 = _lib.launch_count()
         with torch.cuda.graph(g):
             out = self._forward(self._graph_in.view(B, 1), B, 1, 0, 0, 0, False)
             _lib.call("dali_step_advance", self.desc_dev.data_ptr(),
                       self._cur().cuda_stream)
+        self._graph_nk = _lib.launch_count() - k0
         self._in_capture = False
         self._capturing = False
         self.cfg.time_ffn = saved
         self.policy.n_records = n0
         self._graph, self._graph_logits = g, out
         g.replay()
+        self.graph_kernels += self._graph_nk
         self.policy.n_records += L
         return out

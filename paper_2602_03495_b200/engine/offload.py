@@ -221,7 +221,8 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         self.desc_host = torch.zeros((8,), dtype=torch.int32, pin_memory=True)
         self.desc_step_host = torch.zeros((8,), dtype=torch.int32, pin_memory=True)
         self._graph = None
-        self._heads: dict = {}              # offloaded decode: layer -> (graph, h, views)
+        self._heads: dict = {}              # offloaded decode: layer -> (graph, h, views, kernels)
+        self.graph_kernels = 0              # our kernels launched by CUDA-graph replays
         self._heads_warm = False
         self._in_capture = False
         self._capturing = False
@@ -394,7 +395,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         B, S = prompt.shape
         self._cs_cached = torch.cuda.current_stream()
         self.start_request(B)
-        l0 = _lib.launch_count()
+        l0, gk0 = _lib.launch_count(), self.graph_kernels
         cs = self._cur()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(cs)
@@ -445,7 +446,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         st.decode_ms = e1.elapsed_time(e2)
         st.prefill_tokens = B * S
         st.decode_tokens = B * max(max_new_tokens - 1, 0)
-        st.dali_launches = _lib.launch_count() - l0
+        st.dali_launches = _lib.launch_count() - l0 + self.graph_kernels - gk0
         # expert blocks the decode phase streamed out of host DRAM (CPU experts
         # + H2D copies): the shared host-memory roofline of offloaded decode
         copies = st.demand_copies + st.prefetch_copies + st.replace_copies
