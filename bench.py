@@ -270,6 +270,22 @@ def device_decision_us(eng, reps: int = 200) -> float | None:
     return round(e0.elapsed_time(e1) * 1e3 / reps, 2)
 
 
+def host_info() -> dict:
+    """CPU model, visible cores and torch intra-op threads of the host the CPU
+    numbers were taken on (state them)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "visible_cores": len(os.sched_getaffinity(0)),
+            "torch_threads": torch.get_num_threads()}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
@@ -285,7 +301,7 @@ def run_reference(args, ws, rank):
         "data": "synthetic", "config": config_dict(args, ws),
         "prefill_tokens_per_s": round(r["prefill_tokens_per_s"], 3),
         "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": r["threads"],
-                         "kind": "port", "sample": r["sample"]},
+                         "kind": "port", "sample": r["sample"], **host_info()},
         "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -445,7 +461,7 @@ def run_dali(args, ws, rank, local):
                     "cores": r["threads"], "kind": "port", "sample": r["sample"],
                     "prefill_tokens_per_s": round(r["prefill_tokens_per_s"], 3),
                     "policy_layer_us": policy_layer_us(args, eng),
-                    "device_decision_us_per_layer": device_decision_us(eng)}
+                    "device_decision_us_per_layer": device_decision_us(eng), **host_info()}
     if rank == 0:
         line = {
             "metric": metric_name(args), "value": round(dec_v, 4), "unit": "tokens/s", "n_gpus": ws,
@@ -455,6 +471,7 @@ def run_dali(args, ws, rank, local):
             "data": "synthetic (random-init weights, uniform random prompt ids)",
             "config": config_dict(args, ws),
             "prefill_tokens_per_s": round(pre_v, 3),
+            "per_sequence_decode_tokens_per_s": round(dec_v / (args.batch * ws), 4),
             "cache_hit_rate": hit,
             "prefetch_accuracy_top1": float(np.mean(acc1)) if acc1 else None,
             "policy_virtual_clock_tokens_per_s": float(np.mean([r["tokens_per_second"]
