@@ -348,11 +348,12 @@ def _mini_mixtral():
                                hidden_dim=512, ffn_dim=1024, vocab_size=2048)
 
 
-@pytest.mark.parametrize("resident", [False, True])
-def test_decode_attention_kernel_logits_vs_cpu_model(resident):
+@pytest.mark.parametrize("resident,B", [(False, 2), (True, 2), (False, 4)])
+def test_decode_attention_kernel_logits_vs_cpu_model(resident, B):
     """head_dim-128 decode path (fused RoPE/KV append + split-K GQA attention,
     device step descriptor) against the fp32 CPU model, offload and
-    all-resident modes."""
+    all-resident modes; at B=4 the CPU experts take multi-row batches through
+    the asynchronous stage-queue worker."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     from paper_2602_03495_b200.cost_model import default_cost_model
@@ -360,16 +361,19 @@ def test_decode_attention_kernel_logits_vs_cpu_model(resident):
     arch = _mini_mixtral()
     w = ModelWeights(arch, seed=8, resident=resident)
     cfg = EngineConfig(cache_slots_per_layer=0 if resident else 2, capture=True, seed=1)
-    eng = OffloadEngine(arch, w, default_cost_model(non_moe_layer_time=1.0), cfg, max_seq=64)
-    prompt = torch.randint(0, arch.vocab_size, (2, 9), generator=torch.Generator().manual_seed(6))
+    eng = OffloadEngine(arch, w, default_cost_model(non_moe_layer_time=1.0), cfg,
+                        max_batch=B, max_seq=64)
+    prompt = torch.randint(0, arch.vocab_size, (B, 9), generator=torch.Generator().manual_seed(6))
     toks, st = eng.generate(prompt, 7)
+    if not resident:
+        assert st.cpu_expert_calls > 0
     seq = torch.cat([prompt, toks[:, :-1]], dim=1)
     S0 = prompt.shape[1]
     over = {}
     for l in range(arch.num_layers):
-        parts = [torch.from_numpy(st.topk[(0, l)]).view(2, S0, -1)]
+        parts = [torch.from_numpy(st.topk[(0, l)]).view(B, S0, -1)]
         for s_ in range(1, len(st.steps_meta)):
-            parts.append(torch.from_numpy(st.topk[(s_, l)]).view(2, 1, -1))
+            parts.append(torch.from_numpy(st.topk[(s_, l)]).view(B, 1, -1))
         over[l] = torch.cat(parts, dim=1).reshape(-1, arch.top_k)
     dense = M.dense_from_weights(w)
     blk = (lambda l, e: w.expert_dev(l, e).cpu()) if resident else \
