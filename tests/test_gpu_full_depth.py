@@ -1,0 +1,96 @@
+"""Full-size parity (BASELINE configs[1]): the headline configuration itself --
+Mixtral-8x7B, all 32 layers at full width, 24 GB HBM expert cache (2 slots /
+layer), residual prefetch P=1, w_size 4, the cost model profiled on this box
+-- runs a request through the offloaded engine, and the CPU oracle replays
+the engine's captured gate inputs: every routing result and every DALI
+decision (CPU/GPU split, lookups, prefetch set and arrivals, replacement
+events) is bit-exact, and the RunReport-shaped metrics are equal.
+
+Needs ~91 GB of page-locked host memory (the whole expert store); skipped
+on a host with less available memory."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import driver as D
+from oracle import policy as P
+
+pytestmark = pytest.mark.gpu
+
+NEED_HOST_GB = 120
+
+
+def _available_gb() -> float:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) / 1e6
+    except OSError:
+        pass
+    return 0.0
+
+
+def test_full_mixtral_request_decisions_bit_exact():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    if _available_gb() < NEED_HOST_GB:
+        pytest.skip(f"needs {NEED_HOST_GB} GB of available host memory for the expert store")
+    import gc
+
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    from paper_2602_03495_b200.engine.profiler import profile_cost_model
+    gc.collect()
+    arch = preset("mixtral-8x7b")
+    L, N, k = arch.num_layers, arch.num_experts, arch.top_k
+    w = ModelWeights(arch, seed=0)
+    try:
+        cores = len(os.sched_getaffinity(0))
+        cm = profile_cost_model(arch, w, threads=cores, max_w=256)
+        res = np.random.default_rng(5).standard_normal((L - 1, arch.hidden_dim)) * 0.01
+        cfg = EngineConfig(cache_gb=24.0, prefetch_size=1, w_size=4, seed=3, capture=True,
+                           cpu_threads=cores)
+        eng = OffloadEngine(arch, w, cm, cfg, residuals=res, max_seq=192)
+        assert eng.slots_per_layer == 2
+        prompt = torch.randint(0, arch.vocab_size, (1, 128),
+                               generator=torch.Generator().manual_seed(11))
+        toks, st = eng.generate(prompt, 17)
+        by_step = {}
+        for (s, l, h) in st.captured:
+            by_step.setdefault(s, {})[l] = h.double().numpy()
+        steps = [D.StepInput(ti, ntok, np.stack([st.workloads[(s, l)] for l in range(L)]),
+                             np.stack([by_step[s][l] for l in range(L)]), eos)
+                 for s, (ti, ntok, eos) in enumerate(st.steps_meta)]
+        gates = np.stack([w.router[l].double().cpu().numpy() for l in range(L)])
+        for s, step in enumerate(steps):
+            for l in range(L):
+                o_idx, _, o_wl = P.route(step.hidden[l], gates[l], k)
+                assert np.array_equal(o_wl, st.workloads[(s, l)]), (s, l)
+                assert np.array_equal(o_idx, st.topk[(s, l)]), (s, l)
+        tables = P.tables_from_samples(list(zip(cm.cpu_xs, cm.cpu_ys)),
+                                       list(zip(cm.gpu_xs, cm.gpu_ys)), cm.trans_time,
+                                       cm.shared_expert_gpu_time, cm.non_moe_layer_time)
+        dcfg = D.DriverConfig(tables=tables, prefetch_size=1, residuals=res, cache_capacity=2,
+                              w_size=4, u_size=eng.cfg.u_size, seed=3,
+                              initial_on_gpu=st.initial_on_gpu, num_shared_experts=0)
+        orep, recs = D.run(steps, gates, dcfg, L, N, k)
+        got = eng.policy.decision_log()
+        assert len(got) == len(recs) == len(steps) * L
+        for g, o in zip(got, recs):
+            assert np.array_equal(g["C"], o.C) and np.array_equal(g["G"], o.G), (o.step, o.layer)
+            assert g["hits"] == o.lookups and g["event"] == o.event, (o.step, o.layer)
+            if o.prefetch_set is not None:
+                assert g["pset"] == o.prefetch_set.tolist() and g["done"] == o.completed
+        rep = eng.policy_report()
+        for key in ("cache_hit_rate", "prefetch_accuracy_top1", "replacement_events",
+                    "total_time_ms"):
+            assert rep[key] == orep[key], key
+        # the run exercised the hybrid path: CPU experts, cached GPU experts, swaps
+        assert st.cpu_expert_calls > 0 and st.gpu_expert_calls > 0
+        assert any(o.event for o in recs)
+    finally:
+        del w
+        gc.collect()
