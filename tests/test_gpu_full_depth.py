@@ -1,13 +1,15 @@
-"""Full-size parity (BASELINE configs[1]): the headline configuration itself --
-Mixtral-8x7B, all 32 layers at full width, 24 GB HBM expert cache (2 slots /
-layer), residual prefetch P=1, w_size 4, the cost model profiled on this box
--- runs a request through the offloaded engine, and the CPU oracle replays
-the engine's captured gate inputs: every routing result and every DALI
-decision (CPU/GPU split, lookups, prefetch set and arrivals, replacement
-events) is bit-exact, and the RunReport-shaped metrics are equal.
+"""Full-size parity (BASELINE configs[1..3]): the bench configurations
+themselves -- Mixtral-8x7B (all 32 layers, 24 GB HBM expert cache = 2 slots
+per layer, P=1), Qwen1.5-MoE (24 layers, 16 GB, P=4, B=4) and
+DeepSeek-V2-Lite (26 layers, 16 GB, P=4), full widths, w_size 4, the cost
+model profiled on this box -- run a request through the offloaded engine,
+and the CPU oracle replays the engine's captured gate inputs: every routing
+result and every DALI decision (CPU/GPU split, lookups, prefetch set and
+arrivals, replacement events) is bit-exact, and the RunReport-shaped
+metrics are equal.
 
-Needs ~91 GB of page-locked host memory (the whole expert store); skipped
-on a host with less available memory."""
+Needs the whole page-locked expert store in host memory (91 GB for Mixtral,
+~30 GB for the others); skipped on a host with less available memory."""
 
 import os
 
@@ -20,7 +22,7 @@ from oracle import policy as P
 
 pytestmark = pytest.mark.gpu
 
-NEED_HOST_GB = 120
+MARGIN_GB = 30
 
 
 def _available_gb() -> float:
@@ -34,30 +36,37 @@ def _available_gb() -> float:
     return 0.0
 
 
-def test_full_mixtral_request_decisions_bit_exact():
+# BASELINE configs[1..3]: model, HBM cache GB, prefetch size, batch, prompt, new tokens
+CONFIGS = [("mixtral-8x7b", 24.0, 1, 1, 128, 17),
+           ("qwen1.5-moe-a2.7b", 16.0, 4, 4, 48, 9),
+           ("deepseek-v2-lite", 16.0, 4, 1, 256, 9)]
+
+
+@pytest.mark.parametrize("name,cache_gb,psize,B,S,new", CONFIGS)
+def test_full_depth_request_decisions_bit_exact(name, cache_gb, psize, B, S, new):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    if _available_gb() < NEED_HOST_GB:
-        pytest.skip(f"needs {NEED_HOST_GB} GB of available host memory for the expert store")
     import gc
 
     from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
     from paper_2602_03495_b200.engine.profiler import profile_cost_model
+    arch = preset(name)
+    need = arch.num_layers * arch.num_experts * arch.expert_bytes / 1e9 + MARGIN_GB
     gc.collect()
-    arch = preset("mixtral-8x7b")
+    if _available_gb() < need:
+        pytest.skip(f"needs {need:.0f} GB of available host memory for the expert store")
     L, N, k = arch.num_layers, arch.num_experts, arch.top_k
     w = ModelWeights(arch, seed=0)
     try:
         cores = len(os.sched_getaffinity(0))
         cm = profile_cost_model(arch, w, threads=cores, max_w=256)
         res = np.random.default_rng(5).standard_normal((L - 1, arch.hidden_dim)) * 0.01
-        cfg = EngineConfig(cache_gb=24.0, prefetch_size=1, w_size=4, seed=3, capture=True,
-                           cpu_threads=cores)
-        eng = OffloadEngine(arch, w, cm, cfg, residuals=res, max_seq=192)
-        assert eng.slots_per_layer == 2
-        prompt = torch.randint(0, arch.vocab_size, (1, 128),
+        cfg = EngineConfig(cache_gb=cache_gb, prefetch_size=psize, w_size=4, seed=3,
+                           capture=True, cpu_threads=cores)
+        eng = OffloadEngine(arch, w, cm, cfg, residuals=res, max_batch=B, max_seq=S + new + 8)
+        prompt = torch.randint(0, arch.vocab_size, (B, S),
                                generator=torch.Generator().manual_seed(11))
-        toks, st = eng.generate(prompt, 17)
+        toks, st = eng.generate(prompt, new)
         by_step = {}
         for (s, l, h) in st.captured:
             by_step.setdefault(s, {})[l] = h.double().numpy()
@@ -73,9 +82,10 @@ def test_full_mixtral_request_decisions_bit_exact():
         tables = P.tables_from_samples(list(zip(cm.cpu_xs, cm.cpu_ys)),
                                        list(zip(cm.gpu_xs, cm.gpu_ys)), cm.trans_time,
                                        cm.shared_expert_gpu_time, cm.non_moe_layer_time)
-        dcfg = D.DriverConfig(tables=tables, prefetch_size=1, residuals=res, cache_capacity=2,
-                              w_size=4, u_size=eng.cfg.u_size, seed=3,
-                              initial_on_gpu=st.initial_on_gpu, num_shared_experts=0)
+        dcfg = D.DriverConfig(tables=tables, prefetch_size=psize, residuals=res,
+                              cache_capacity=eng.slots_per_layer, w_size=4,
+                              u_size=eng.cfg.u_size, seed=3, initial_on_gpu=st.initial_on_gpu,
+                              num_shared_experts=arch.num_shared_experts)
         orep, recs = D.run(steps, gates, dcfg, L, N, k)
         got = eng.policy.decision_log()
         assert len(got) == len(recs) == len(steps) * L
