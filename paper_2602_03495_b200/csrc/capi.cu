@@ -28,15 +28,50 @@ extern "C" int64_t dali_launch_count(void) { return dali::g_launches.load(); }
 // ---------------------------------------------------------------------------
 #include <sys/mman.h>
 
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
+
+namespace {
+// On a multi-socket host, spread the store's pages over every NUMA node
+// before first touch (MPOL_INTERLEAVE): the CPU-expert workers of every
+// local rank and the GPUs' H2D copies then draw on all memory controllers
+// instead of the node local rank 0 happened to run on.  One node: no-op.
+// DALI_NUMA_INTERLEAVE=0 turns it off.
+void interleave_numa(void* p, size_t bytes) {
+  const char* env = getenv("DALI_NUMA_INTERLEAVE");
+  if (env && env[0] == '0') return;
+  FILE* f = fopen("/sys/devices/system/node/online", "r");
+  if (!f) return;
+  char buf[256] = {0};
+  const bool ok = fgets(buf, sizeof(buf), f) != nullptr;
+  fclose(f);
+  if (!ok) return;
+  unsigned long mask[4] = {0, 0, 0, 0};           // nodes 0..255
+  int n_nodes = 0;
+  for (char* tok = strtok(buf, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+    int a = 0, b = 0;
+    if (sscanf(tok, "%d-%d", &a, &b) != 2) b = a = atoi(tok);
+    for (int node = a; node <= b && node < 256; ++node, ++n_nodes)
+      mask[node / 64] |= 1ul << (node % 64);
+  }
+  if (n_nodes < 2) return;
+  constexpr int kMpolInterleave = 3;
+  syscall(SYS_mbind, p, bytes, kMpolInterleave, mask, 256ul, 0u);   // best effort
+}
+}  // namespace
 
 extern "C" int dali_host_alloc(size_t bytes, int32_t nthreads, void** out) {
   DALI_REQUIRE(out != nullptr && bytes > 0, DALI_ECUDA, "bad host allocation request");
   void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
   DALI_REQUIRE(p != MAP_FAILED, DALI_ECUDA, "mmap of %zu bytes failed", bytes);
   madvise(p, bytes, MADV_HUGEPAGE);
+  interleave_numa(p, bytes);
   if (nthreads < 1) nthreads = 1;
   std::vector<std::thread> th;
   const size_t chunk = (bytes + nthreads - 1) / nthreads;
@@ -68,8 +103,6 @@ extern "C" int dali_host_free(void* p, size_t bytes) {
 }
 
 #include <fcntl.h>
-#include <sys/syscall.h>
-#include <unistd.h>
 
 extern "C" int dali_host_alloc_shared(size_t bytes, int32_t nthreads, int32_t create, int32_t* fd,
                                       int32_t owner_pid, void** out) {
@@ -91,6 +124,7 @@ extern "C" int dali_host_alloc_shared(size_t bytes, int32_t nthreads, int32_t cr
   DALI_REQUIRE(p != MAP_FAILED, DALI_ECUDA, "mmap of shared store failed");
   madvise(p, bytes, MADV_HUGEPAGE);
   if (create) {
+    interleave_numa(p, bytes);
     if (nthreads < 1) nthreads = 1;
     std::vector<std::thread> th;
     const size_t chunk = (bytes + nthreads - 1) / nthreads;
