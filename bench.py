@@ -367,6 +367,13 @@ def run_dali(args, ws, rank, local):
         store = shared_host_store(nbytes, local, local_ws, rank - local, cores)
         weights = ModelWeights(arch, seed=0, host_store=store, fill_experts=(local == 0))
         barrier(ws)
+    if local_ws > 1:
+        # each local rank's CPU-expert workers get their own slice of the cores
+        # (threads created from here on inherit it); cpu_threads matches
+        allc = sorted(os.sched_getaffinity(0))
+        per = max(1, len(allc) // local_ws)
+        mine = allc[local * per:(local + 1) * per] or allc
+        os.sched_setaffinity(0, mine)
     eng = build_engine(args.model, cfg, seed=0, max_batch=args.batch,
                        max_seq=args.prefill + args.decode + 8, log=log if rank == 0 else None,
                        weights=weights, ep=ep, resident=args.resident)
