@@ -259,16 +259,19 @@ extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, cons
 // experts on the pool's worker threads and returns; the caller (the engine's
 // Python thread) dispatches the GPU side of the layer meanwhile and then
 // joins in dali_cpu_expert_wait, taking whatever work units are left.  The
-// job is a queue of stages -- (expert 0 gate/up), (expert 0 down), (expert
-// 1 gate/up), ... -- each split into ~1 MB units handed out by an atomic
-// counter; a stage opens when the previous one has finished, so a thread
-// that joins late simply starts at the current stage.  One job in flight.
+// job is a queue of stages -- every expert's gate/up stage first, then every
+// expert's down stage -- each split into ~1 MB units handed out by an
+// atomic counter.  A down stage waits only for its own expert's gate/up
+// stage, so the only barrier a layer pays is at the last expert's gate/up
+// tail, and a thread that joins late simply starts at the current stage.
+// One job in flight.
 // ---------------------------------------------------------------------------
 namespace {
 constexpr int kDownRows = 32;
+constexpr int kUpCols = 64;                         // SwiGLU columns per gate/up unit
 
 struct Stage {
-  int expert = 0, down = 0, units = 0;
+  int expert = 0, down = 0, units = 0, dep = -1;   // dep: stage that must finish first
   std::atomic<int> next{0}, done{0};
 };
 
@@ -289,12 +292,13 @@ struct StageJob {
     const uint16_t* w2 = blocks[e] + (int64_t)2 * f * d;
     uint16_t* h = hbuf[e].data();
     float a[kMaxRows], b[kMaxRows];
-    if (!st.down) {                                 // gate/up group u
-      for (int i = 0; i < 64; ++i) {
-        row_dot(w13 + (int64_t)(128 * u + i) * d, xs[e], d, d, R, a);
-        row_dot(w13 + (int64_t)(128 * u + 64 + i) * d, xs[e], d, d, R, b);
+    if (!st.down) {                                 // SwiGLU columns [64u, 64u+64)
+      const int g = u / (64 / kUpCols), c0 = (u % (64 / kUpCols)) * kUpCols;
+      for (int i = c0; i < c0 + kUpCols; ++i) {
+        row_dot(w13 + (int64_t)(128 * g + i) * d, xs[e], d, d, R, a);
+        row_dot(w13 + (int64_t)(128 * g + 64 + i) * d, xs[e], d, d, R, b);
         for (int r = 0; r < R; ++r)
-          h[(size_t)r * f + 64 * u + i] = f2bf(a[r] / (1.0f + std::exp(-a[r])) * b[r]);
+          h[(size_t)r * f + 64 * g + i] = f2bf(a[r] / (1.0f + std::exp(-a[r])) * b[r]);
       }
     } else {                                        // down rows [32u, 32u+32)
       const int m1 = std::min(d, (u + 1) * kDownRows);
@@ -307,8 +311,8 @@ struct StageJob {
   void work() {
     for (int s = 0; s < n_stages; ++s) {
       Stage& st = stages[s];
-      if (s > 0) {
-        const Stage& pv = stages[s - 1];
+      if (st.dep >= 0) {
+        const Stage& pv = stages[st.dep];
         while (pv.done.load(std::memory_order_acquire) < pv.units) _mm_pause();
       }
       for (int u = st.next.fetch_add(1, std::memory_order_relaxed); u < st.units;
@@ -350,13 +354,14 @@ extern "C" int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const u
     j.xs[i] = reinterpret_cast<const uint16_t*>(xs[i]);
     j.ys[i] = reinterpret_cast<float*>(ys[i]);
     j.hbuf[i].resize((size_t)std::max(rows[i], 1) * f);
-    Stage& up = j.stages[2 * i];
+    Stage& up = j.stages[i];
     up.expert = i;
     up.down = 0;
-    up.units = rows[i] > 0 ? f / 64 : 0;
-    Stage& dn = j.stages[2 * i + 1];
+    up.units = rows[i] > 0 ? f / kUpCols : 0;
+    Stage& dn = j.stages[n + i];
     dn.expert = i;
     dn.down = 1;
+    dn.dep = i;
     dn.units = rows[i] > 0 ? (d + kDownRows - 1) / kDownRows : 0;
   }
   j.pool = pool_for(nthreads < 1 ? 1 : nthreads);
