@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -476,6 +477,254 @@ ffn_tc_persistent(const __grid_constant__ CUtensorMap b_map, const int32_t* __re
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// CTA-pair variant for wide token tiles (tensor-bound prefill): a cluster of
+// two CTAs on one TPC issues tcgen05.mma.cta_group::2 with M = 256.  Each CTA
+// stages its own 128 weight rows (A) and HALF of the BN token columns (B) per
+// k-block, so every SM moves 32 KB instead of 48 KB of operands per k-block
+// for the same MMA work; each CTA's TMEM holds its 128 rows x all BN columns,
+// so the epilogue is the single-CTA one.  Protocol (rank 0 = leader):
+//   * both CTAs' TMA loads complete_tx on the LEADER's full[s] (2-SM TMA form);
+//     only the leader arrives (expect_tx = both CTAs' bytes);
+//   * the leader's single thread issues the MMAs; tcgen05.commit multicasts
+//     to empty[s] / tfull[acc] of both CTAs;
+//   * both CTAs' epilogue warps arrive on the leader's tempty[acc] (8
+//     arrivals: 4 local + 4 remote) before the leader reuses the accumulator.
+// ---------------------------------------------------------------------------
+template <int BN>
+struct PairSmem {
+  static constexpr int A_BYTES = BM * BK * 2;            // this CTA's 128 weight rows
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;      // this CTA's half of the tokens
+  static constexpr int STAGES = 6;
+  static constexpr int TMEM_COLS = 2 * BN;               // two accumulator stages
+  static constexpr size_t BYTES =
+      (size_t)STAGES * (A_BYTES + B_BYTES) + 64 * 17 * 4 + 1024 + 512;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, uint64_t* bar, int x,
+                                                 int y) {
+  // barrier address with the peer bit cleared: the transaction bytes land on
+  // the leader CTA's mbarrier
+  const uint32_t b = su32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(b), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  const uint16_t mask = 0x3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
+template <int BN>
+__device__ bool find_pair_tile(const int32_t* offs, const uint64_t* maps, int N, int m_pairs,
+                               int splits, Tile& t, int idx, int rank) {
+  for (int e = 0; e < N; ++e) {
+    if (!maps[e]) continue;
+    const int ne = offs[e + 1] - offs[e];
+    if (ne <= 0) continue;
+    const int n_tiles_e = (ne + BN - 1) / BN;
+    const int cnt = n_tiles_e * m_pairs * splits;
+    if (idx < cnt) {
+      t.e = e;
+      t.split = idx % splits;
+      idx /= splits;
+      const int nt = idx % n_tiles_e;
+      t.m_tile = 2 * (idx / n_tiles_e) + rank;
+      t.row0 = offs[e] + nt * BN;
+      t.n_valid = min(BN, ne - nt * BN);
+      return true;
+    }
+    idx -= cnt;
+  }
+  return false;
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kPThreads, 1)
+ffn_tc_pair(const __grid_constant__ CUtensorMap b_map, const int32_t* __restrict__ offs,
+            const uint64_t* __restrict__ a_maps, int N, int K, int m_tiles, int splits,
+            int out_ld, uint16_t* __restrict__ H, float* __restrict__ Y, int64_t y_plane) {
+  using S = PairSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + S::STAGES * S::A_BYTES;
+  float* sU = reinterpret_cast<float*>(sB + S::STAGES * S::B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sU + 64 * 17);
+  uint64_t* empty = full + S::STAGES;
+  uint64_t* tfull = empty + S::STAGES;      // [2]
+  uint64_t* tempty = tfull + 2;             // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int nk = (K / BK) / splits;
+  const int m_pairs = m_tiles / 2;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma_prefetch_desc(&b_map);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tslot)),
+                 "r"(S::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int n_tiles = 0;
+  for (int e = 0; e < N; ++e) {
+    if (!a_maps[e]) continue;
+    const int ne = offs[e + 1] - offs[e];
+    if (ne > 0) n_tiles += ((ne + BN - 1) / BN) * m_pairs * splits;
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {                                  // ---- TMA producer (both CTAs)
+      uint32_t it = 0;
+      for (int ti = pair; ti < n_tiles; ti += n_pairs) {
+        Tile t;
+        find_pair_tile<BN>(offs, a_maps, N, m_pairs, splits, t, ti, (int)rank);
+        const void* a_map = reinterpret_cast<const void*>(a_maps[t.e] + (MODE == 0 ? 0 : 128));
+        const int kb0 = t.split * nk;
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % S::STAGES;
+          const uint32_t ph = (it / S::STAGES) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          if (rank == 0) mbar_expect_tx(full + s, 2 * (S::A_BYTES + S::B_BYTES));
+          const int kx = (kb0 + i) * BK;
+          tma_load_2d_pair(sA + s * S::A_BYTES, a_map, full + s, kx, t.m_tile * BM);
+          tma_load_2d_pair(sB + s * S::B_BYTES, &b_map, full + s, kx,
+                           t.row0 + (int)rank * (BN / 2));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {                     // ---- MMA issuer (leader only)
+      constexpr uint32_t idesc = idesc_bf16(2 * BM, BN);
+      uint32_t it = 0, tc = 0;
+      for (int ti = pair; ti < n_tiles; ti += n_pairs, ++tc) {
+        const int acc = tc & 1;
+        const uint32_t aph = (tc >> 1) & 1;
+        mbar_wait(tempty + acc, aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * BN;
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % S::STAGES;
+          const uint32_t ph = (it / S::STAGES) & 1;
+          mbar_wait(full + s, ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = sw128_desc(su32(sA + s * S::A_BYTES));
+          const uint64_t db = sw128_desc(su32(sB + s * S::B_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_pair(d, da + 2 * kk, db + 2 * kk, idesc, (i | kk) != 0);
+          umma_commit_pair(empty + s);
+        }
+        umma_commit_pair(tfull + acc);
+      }
+    }
+  } else {                                            // ---- epilogue (warps 2-5)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    uint32_t tc = 0;
+    for (int ti = pair; ti < n_tiles; ti += n_pairs, ++tc) {
+      Tile t;
+      find_pair_tile<BN>(offs, a_maps, N, m_pairs, splits, t, ti, (int)rank);
+      const int acc = tc & 1;
+      const uint32_t aph = (tc >> 1) & 1;
+      mbar_wait(tfull + acc, aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t lane_addr = tmem + acc * BN + ((uint32_t)(q * 32) << 16);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(lane_addr + c0, v);
+        if (MODE == 0) {
+          if (r >= 64) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sU[(r - 64) * 17 + i] = v[i];
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (r < 64) {
+            const int j = t.m_tile * 64 + r;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int c = c0 + i;
+              if (c < t.n_valid) {
+                const float g = v[i], u = sU[r * 17 + i];
+                H[(int64_t)(t.row0 + c) * out_ld + j] = f32_to_bf16_bits(g / (1.0f + __expf(-g)) * u);
+              }
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        } else {
+          const int m = t.m_tile * BM + r;
+          float* y = Y + (int64_t)t.split * y_plane;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int c = c0 + i;
+            if (c < t.n_valid) y[(int64_t)(t.row0 + c) * out_ld + m] = v[i];
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) mbar_arrive(tempty + acc);
+        else mbar_arrive_leader(tempty + acc);
+      }
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();                                 // both CTAs done with TMEM / barriers
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(S::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -592,6 +841,67 @@ static int launch_persistent(const int32_t* offs, const uint64_t* maps, int N, i
   return DALI_OK;
 }
 
+template <int BN>
+static int launch_pair(const int32_t* offs, const uint64_t* maps, int N, int d, int f,
+                       int64_t rows, int n_gpu, uint16_t* hbuf, float* yp, int splits,
+                       const uint16_t* xp, cudaStream_t st, int n_sm) {
+  using S = PairSmem<BN>;
+  CUtensorMap xmap, hmap;                          // token boxes of BN/2 rows per CTA
+  const uint64_t cap_rows = (uint64_t)std::max<int64_t>(rows, 1);
+  int rc = make_map(&xmap, xp, cap_rows, d, BN / 2);
+  if (rc) return rc;
+  rc = make_map(&hmap, hbuf, cap_rows, f, BN / 2);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ffn_tc_pair<BN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::BYTES);
+    cudaFuncSetAttribute(ffn_tc_pair<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)S::BYTES);
+    attr = true;
+  }
+  const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;
+  const int m_up = (2 * f) / BM, m_dn = d / BM;
+  const int max_ctas = (n_sm / 2) * 2;
+  const unsigned g_up = (unsigned)std::min<int64_t>(2 * ntile_bound * (m_up / 2), max_ctas);
+  const unsigned g_dn = (unsigned)std::min<int64_t>(2 * ntile_bound * (m_dn / 2) * splits, max_ctas);
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.stream = st;
+  cfg.gridDim = dim3(g_up);
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, ffn_tc_pair<BN, 0>, xmap, offs, maps, N, d, m_up, 1, f, hbuf,
+                     (float*)nullptr, (int64_t)0);
+  DALI_LAUNCH_CHECK("ffn_tc_pair<up>");
+  cfg.gridDim = dim3(g_dn);
+  cfg.numAttrs = 2;                                // down prologue overlaps the up tail
+  cudaLaunchKernelEx(&cfg, ffn_tc_pair<BN, 1>, hmap, offs, maps, N, f, m_dn, splits, d,
+                     (uint16_t*)nullptr, yp, rows * (int64_t)d);
+  DALI_LAUNCH_CHECK("ffn_tc_pair<down>");
+  return DALI_OK;
+}
+
+// Token tiles of 256 go through the CTA-pair kernel (measured +3-4% at 256-512
+// tokens per expert, equal at 1024; at 128-token tiles, which are HBM-bound,
+// the pair kernel was 1.5% slower and is not used).  DALI_FFN_PAIR=0 selects
+// the single-CTA persistent kernel (A/B switch).
+static bool use_pair() {
+  static const bool v = [] {
+    const char* e = getenv("DALI_FFN_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 static int sm_count_tc() {
   static int n = 0;
   if (!n) {
@@ -643,6 +953,9 @@ extern "C" int dali_expert_ffn_tc(const uint16_t* xp, const int32_t* offsets, in
   if (mr <= 128)
     return tc::launch_persistent<128>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf,
                                       yp, splits, xp, st, nsm);
+  if (tc::use_pair())
+    return tc::launch_pair<256>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp,
+                                splits, xp, st, nsm);
   return tc::launch_persistent<256>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp,
                                     splits, xp, st, nsm);
 }
