@@ -114,12 +114,23 @@ class MoEExecMixin:
         v["blk"], v["layout"], v["perm"] = rblk, (o_off, o_idx, o_w, nb), perm
         return v
 
+    def _d2h(self, dst: torch.Tensor, src: torch.Tensor) -> None:
+        """Device -> pinned host mirror on the compute stream.  Decode-sized
+        mirrors (<= 1 MiB) are kernel copies over UVA (no copy-engine launch
+        latency on the decision path); prefill-sized ones use the copy engine."""
+        nbytes = src.numel() * src.element_size()
+        if nbytes <= (1 << 20):
+            _lib.call("dali_copy_mapped", dst.data_ptr(), src.data_ptr(), nbytes,
+                      self._cur().cuda_stream)
+        else:
+            dst.copy_(src, non_blocking=True)
+
     def _host_view(self, v, T: int):
         """Pinned host mirror of the routing block (valid after the event wait)."""
         N, k = self.arch.num_experts, self.arch.top_k
         o_off, o_idx, o_w, nb = v["layout"]
         hb = self._ws("route_h", (nb,), torch.uint8, pinned=True)
-        hb.copy_(v["blk"], non_blocking=True)
+        self._d2h(hb, v["blk"])
         return {
             "wl": hb[:o_off].view(torch.int64),
             "offsets": hb[o_off:o_off + (N + 1) * 4].view(torch.int32),
@@ -427,7 +438,7 @@ class MoEExecMixin:
                                         gate_this=self.w.router[l])
         hv = self._host_view(v, T)
         xp_host = self._ws("xp_h", (R, d), torch.bfloat16, pinned=True)
-        xp_host.copy_(v["xp"], non_blocking=True)
+        self._d2h(xp_host, v["xp"])
         h_host = None
         if self.cfg.capture:
             h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)

@@ -23,7 +23,7 @@ def test_offload_roofline_host_bound():
     # peak = 0.4 GB / 2 ms = 200 GB/s; 10 blocks (4 GB) per token, 1 of them H2D
     eng = _eng()
     r = bench.offload_roofline(eng, [_stats(decode_ms=1000.0, host_blocks=400, h2d_blocks=40,
-                                            tokens=40)])
+                                            tokens=40)], peak_ms=2.0)
     assert r["bound"] == "host_dram"
     assert abs(r["peak"] - 200.0) < 1e-6
     assert abs(r["achieved"] - 160.0) < 1e-6             # 160 GB in 1 s
@@ -36,10 +36,11 @@ def test_offload_roofline_host_bound():
 
 def test_offload_roofline_pcie_bound_and_empty():
     eng = _eng(t_cpu1_ms=0.1, trans_ms=6.0)
-    r = bench.offload_roofline(eng, [_stats(1000.0, host_blocks=100, h2d_blocks=90, tokens=10)])
+    r = bench.offload_roofline(eng, [_stats(1000.0, host_blocks=100, h2d_blocks=90, tokens=10)],
+                               peak_ms=0.1)
     assert r["bound"] == "pcie"
     assert r["floor_tokens_per_s"] == r["pcie_floor_tokens_per_s"]
-    assert bench.offload_roofline(eng, [_stats(1000.0, 0, 0, 10)]) is None
+    assert bench.offload_roofline(eng, [_stats(1000.0, 0, 0, 10)], peak_ms=0.1) is None
 
 
 def test_l2_note_and_host_info():
