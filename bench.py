@@ -326,7 +326,10 @@ def config_dict(args, ws):
             "cache_gb": args.cache_gb,
             "parallelism": (f"ep{ws}" if args.ep else f"replicas{ws}") +
                            ("-resident" if args.resident else ""),
-            "l2": l2_note(args)}
+            "l2": l2_note(args),
+            "decode_inputs": "teacher-forced token ids from a seeded synthetic stream with "
+                             "Zipf(1.1) unigram frequencies (argmax still computed and read "
+                             "back every step)"}
 
 
 def l2_note(args) -> str:
@@ -341,6 +344,14 @@ def l2_note(args) -> str:
                 f"L2-resident (small functional config, no flush)")
     return (f"working set: {mb:.1f} MB expert blocks, ~{step_mb / 1e3:.1f} GB of routed expert "
             f"weights per decode step >> 126 MB L2; no flush")
+
+
+def zipf_tokens(vocab: int, shape, seed: int, s: float = 1.1) -> torch.Tensor:
+    """Synthetic token ids with a Zipf(s) unigram distribution over a fixed
+    (seed-independent) permutation of the vocabulary."""
+    perm = np.random.default_rng(12345).permutation(vocab)
+    r = np.random.default_rng(seed).zipf(s, size=shape)
+    return torch.from_numpy(perm[(r - 1) % vocab].astype(np.int64))
 
 
 def run_dali(args, ws, rank, local):
@@ -383,14 +394,24 @@ def run_dali(args, ws, rank, local):
     g = torch.Generator().manual_seed(1000 + rank)
     n_req = args.warmup + args.steps
     prompts = [torch.randint(0, V, (args.batch, args.prefill), generator=g) for _ in range(n_req)]
+    # decode inputs are teacher-forced from a seeded synthetic stream: with random
+    # weights the argmax sits on near-ties, so free-running generation would route
+    # a different workload on every box (observed: 1.8k-3.6k CPU experts per
+    # request); the argmax is still computed and read back every step.  The
+    # stream has natural-text-like unigram frequencies (Zipf, s = 1.1, over a
+    # seeded permutation of the vocabulary).
+    forced = [zipf_tokens(V, (args.batch, max(args.decode - 1, 0)), seed=2000 + 97 * rank + i)
+              for i in range(n_req)]
 
-    def request(p, host_io):
-        toks, st = eng.generate(p if host_io else p.cuda(), args.decode, host_io=host_io)
+    def request(i, host_io):
+        p = prompts[i]
+        toks, st = eng.generate(p if host_io else p.cuda(), args.decode, host_io=host_io,
+                                forced=forced[i])
         rep = eng.policy_report()
         return st, rep
 
     for i in range(args.warmup):
-        st, rep = request(prompts[i], True)
+        st, rep = request(i, True)
         log(f"warmup {i}: prefill {st.prefill_tokens / st.prefill_ms * 1e3:.1f} tok/s, decode "
             f"{st.decode_tokens / max(st.decode_ms, 1e-9) * 1e3:.2f} tok/s, hit {rep['cache_hit_rate']}")
 
@@ -409,8 +430,9 @@ def run_dali(args, ws, rank, local):
         with ClockSampler(torch.cuda.current_device()) as clk:
             torch.cuda.nvtx.range_push("timed")
             e0.record(cs)
-            for p in dev_prompts:
-                toks, st = eng.generate(p, args.decode, host_io=host_io)
+            for j, p in enumerate(dev_prompts):
+                toks, st = eng.generate(p, args.decode, host_io=host_io,
+                                        forced=forced[offset + j])
                 stats.append(st)
                 reps.append(eng.policy_report())
                 log(f"{'e2e' if host_io else 'value'} request: decode "
@@ -458,7 +480,7 @@ def run_dali(args, ws, rank, local):
     achieved = (avg_b / (avg_ms / 1e3) / 1e9) if durs else None
     total_ffn_ms = float(np.sum(durs)) if durs else 0.0
     t_ratio, t_src = ffn_traffic_ratio()
-    h2d_step = int(np.mean([args.batch * args.prefill * 8 for _ in st_e]))
+    h2d_step = int(args.batch * (args.prefill + max(args.decode - 1, 0)) * 8)
     d2h_step = int(args.batch * 8 * args.decode)
 
     cpu_base = None

@@ -384,13 +384,19 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         self.kv.len = pos + 1
         return logits
 
-    def generate(self, prompt: torch.Tensor, max_new_tokens: int, host_io: bool = True):
+    def generate(self, prompt: torch.Tensor, max_new_tokens: int, host_io: bool = True,
+                 forced: torch.Tensor | None = None):
         """Greedy generation for one request.
 
         host_io=True (the end-to-end path a user sees): ``prompt`` (B, S)
         int64 on the HOST, copied in inside the timed region, and every
         generated token is read back to the host as it is produced.
         host_io=False: ``prompt`` already in HBM and tokens stay on device.
+        ``forced`` (B, max_new_tokens - 1) int64 on the host: teacher forcing --
+        decode step i consumes forced[:, i] instead of the argmax (which is
+        still computed and returned), so the routed workload does not depend
+        on argmax near-ties of a random-weight model (the benchmark uses this
+        for a workload that is identical on every box).
         Returns (tokens (B, n) int64, stats)."""
         B, S = prompt.shape
         self._cs_cached = torch.cuda.current_stream()
@@ -422,6 +428,16 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
 
             def fetch(t, i):
                 return t
+        f_pin = f_dev = None
+        if forced is not None:
+            assert forced.shape == (B, max(max_new_tokens - 1, 0)), "forced must be (B, n - 1)"
+            n_f = max(max_new_tokens - 1, 1)
+            f_pin = self._ws("forced_h", (n_f, B), torch.int64, pinned=True)
+            f_dev = self._ws("forced_d", (n_f, B), torch.int64)
+            if max_new_tokens > 1:
+                f_pin[:max_new_tokens - 1].copy_(forced.t())
+            if not host_io:                     # device-resident inputs: one upload
+                f_dev.copy_(f_pin, non_blocking=True)
         logits = self.prefill(p_dev, is_eos=(max_new_tokens <= 1))
         nxt = logits.argmax(-1)
         out = [fetch(nxt, 0)]
@@ -432,6 +448,11 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         copies0 = st0.demand_copies + st0.prefetch_copies + st0.replace_copies
         blocks0 = st0.cpu_expert_calls + copies0
         for i in range(max_new_tokens - 1):
+            if f_dev is not None:
+                if host_io:                     # this step's input ids: one H2D kernel copy
+                    _lib.call("dali_copy_mapped", f_dev[i].data_ptr(), f_pin[i].data_ptr(),
+                              B * 8, cs.cuda_stream)
+                nxt = f_dev[i].view(nxt.shape)
             logits = self.decode(nxt, is_eos=(i == max_new_tokens - 2))
             nxt = logits.argmax(-1)
             out.append(fetch(nxt, i + 1))

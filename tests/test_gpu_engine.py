@@ -53,8 +53,8 @@ def _oracle_replay(eng, st):
     return steps, gates, D.run(steps, gates, dcfg, L, N, k)
 
 
-def _check_request(eng, prompt, n_new):
-    toks, st = eng.generate(prompt, n_new)
+def _check_request(eng, prompt, n_new, forced=None):
+    toks, st = eng.generate(prompt, n_new, forced=forced)
     a = eng.arch
     steps, gates, (orep, recs) = _oracle_replay(eng, st)
     # 1. routing: the oracle's fp64 gating of the captured bf16 gate inputs
@@ -91,6 +91,23 @@ def test_engine_decisions_bit_exact_two_requests(eng):
     # second request starts from the first one's final residency (carry-over)
     _, st2, rep2 = _check_request(eng, p2, 10)
     assert rep1["cache_hit_rate"] is not None
+
+
+def test_engine_teacher_forced_decode(eng):
+    """Teacher-forced decode (the benchmark's reproducible workload): every
+    decision still replays bit-exactly through the oracle, the decode steps
+    consume the forced ids (captured gate inputs differ from a free-running
+    request), and the engine still returns its argmax tokens."""
+    g = torch.Generator().manual_seed(4)
+    p = torch.randint(0, eng.arch.vocab_size, (1, 16), generator=g)
+    forced = torch.randint(0, eng.arch.vocab_size, (1, 7), generator=g)
+    toks_f, st_f, _ = _check_request(eng, p, 8, forced=forced)
+    assert toks_f.shape == (1, 8)
+    eng.reset_cache()
+    toks_a, st_a = eng.generate(p, 8)
+    assert torch.equal(toks_a[:, 0], toks_f[:, 0])          # same prefill
+    assert any(not np.array_equal(st_a.workloads[(s, 0)], st_f.workloads[(s, 0)])
+               for s in range(1, 8)) or not torch.equal(toks_a[:, 1:], forced)
 
 
 def test_engine_logits_match_cpu_model(eng):
