@@ -27,6 +27,7 @@ ap.add_argument("--cache-gb", type=float, default=24.0)
 ap.add_argument("--prefill", type=int, default=512)
 ap.add_argument("--decode", type=int, default=48)
 ap.add_argument("--prefetch", type=int, default=1)
+ap.add_argument("--forced", type=int, default=1, help="teacher-forced decode like bench.py")
 ap.add_argument("--out", default="gpurun_out/timeline.json")
 ap.add_argument("--cost-model", default=None,
                 help="cost-model JSON: loaded if it exists, else profiled and saved there "
@@ -46,9 +47,13 @@ if args.cost_model and cm is None:
     save_cost_model(eng.cm, args.cost_model)
 V = eng.arch.vocab_size
 g = torch.Generator().manual_seed(1000)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import zipf_tokens  # noqa: E402  (the bench's teacher-forced decode stream)
+
 for it in range(2):
     p = torch.randint(0, V, (1, args.prefill), generator=g)
-    toks, st = eng.generate(p, args.decode, host_io=True)
+    forced = zipf_tokens(V, (1, args.decode - 1), seed=3000 + it) if args.forced else None
+    toks, st = eng.generate(p, args.decode, host_io=True, forced=forced)
     print(f"request {it}: prefill {st.prefill_tokens / st.prefill_ms * 1e3:.1f} tok/s decode "
           f"{st.decode_tokens / st.decode_ms * 1e3:.2f} tok/s", flush=True)
 torch.cuda.synchronize()
