@@ -383,6 +383,9 @@ class MoEExecMixin:
                                                  "big", t0))
         dev_rows = self._ws("cpu_rows_d", (R, d), torch.float32)
         lo, hi = job["lo"], job["hi"]
+        if self.cfg.trace_layers:
+            self._ev_rows = torch.cuda.Event(enable_timing=True)
+            self._ev_rows.record(self._cur())
         if hi > lo:
             _lib.call("dali_copy_mapped", dev_rows[lo].data_ptr(), out[lo].data_ptr(),
                       (hi - lo) * d * 4, self._cur().cuda_stream)
@@ -514,6 +517,7 @@ class MoEExecMixin:
                 step=step, layer=l, T=T, nC=int(sum(1 for e in range(N) if rec.C[e] and wl_np[e])),
                 hit=le["hit"], pf=le["pf"], dem=le["dem"], rep=le["rep"], done=le["done"],
                 host=(tp0, tp1, tp2, tp3, tp4, time.perf_counter()), tp_sub=tp_sub,
+                ev_rows=self._ev_rows if cpu_rows is not None else None,
                 ev=(ev_r if ev_r is not None else ev_dec, ev_dec, le["t0"], ev_c)))
         return out
 

@@ -189,6 +189,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         # dispatch first, then run them synchronously -- A/B switch)
         self._cpu_async = os.environ.get("DALI_CPU_ASYNC", "1") == "1"
         self._cpu_sub = None                  # preallocated submission arrays (_cpu_submit)
+        self._ev_rows = None                  # trace: event before the CPU-row upload
         torch.set_num_threads(self.cpu_threads)
         # per-layer pinned scratch for pointer table + G mask
         row = (N * 17 + 63) // 64 * 64        # ptrs | maps | G mask, 64-B aligned rows

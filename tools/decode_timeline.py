@@ -68,6 +68,8 @@ for i, r in enumerate(lt):
              pf=r["pf"], rep=r["rep"],
              h_launch=(tp[1] - tp[0]) * 1e3, h_wait=(tp[2] - tp[1]) * 1e3,
              h_presub=(r["tp_sub"] - tp[2]) * 1e3,
+             g_rows_comb=(r["ev_rows"].elapsed_time(ev_c) if r.get("ev_rows") is not None
+                          else None),
              h_disp=(tp[3] - tp[2]) * 1e3, h_cpu=(tp[4] - tp[3]) * 1e3,
              h_comb=(tp[5] - tp[4]) * 1e3,
              h_gap=((nxt["host"][0] - tp[5]) * 1e3) if nxt else None,
@@ -84,7 +86,7 @@ def mean(key, rs):
     return round(float(np.mean(v)), 3) if v else None
 
 
-keys = ["h_launch", "h_wait", "h_presub", "h_disp", "h_cpu", "h_comb", "h_gap", "g_route_dec",
+keys = ["h_launch", "h_wait", "h_presub", "g_rows_comb", "h_disp", "h_cpu", "h_comb", "h_gap", "g_route_dec",
         "g_dec_ffn", "g_ffn_comb", "g_dec_comb", "g_prev_comb_to_route"]
 steps = sorted({r["step"] for r in rows})
 per_tok = (sum(r["h_launch"] + r["h_wait"] + r["h_disp"] + r["h_cpu"] + r["h_comb"] +
