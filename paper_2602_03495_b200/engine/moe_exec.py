@@ -365,8 +365,8 @@ class MoEExecMixin:
         return dict(out=out, native=n > 0, big=big, lo=lo, hi=hi, l=l, rows=rows_host)
 
     def _cpu_finish(self, job, R: int) -> torch.Tensor | None:
-        """Run the prefill-sized CPU experts, join the asynchronous ones and
-        move the CPU rows to the device (kernel copy: no copy-engine queueing)."""
+        """Run the prefill-sized CPU experts and join the asynchronous ones;
+        returns the pinned (R, d) f32 rows, which device kernels read over UVA."""
         if job is None:
             return None
         a = self.arch
@@ -381,15 +381,15 @@ class MoEExecMixin:
             if self.cfg.trace_layers:
                 self.stats.cpu_expert_ms.append((r1 - r0, (time.perf_counter() - t0) * 1e3,
                                                  "big", t0))
-        dev_rows = self._ws("cpu_rows_d", (R, d), torch.float32)
-        lo, hi = job["lo"], job["hi"]
         if self.cfg.trace_layers:
             self._ev_rows = torch.cuda.Event(enable_timing=True)
             self._ev_rows.record(self._cur())
-        if hi > lo:
-            _lib.call("dali_copy_mapped", dev_rows[lo].data_ptr(), out[lo].data_ptr(),
-                      (hi - lo) * d * 4, self._cur().cuda_stream)
-        return dev_rows
+        # the consumer kernel (combine / EP return) reads the rows straight from
+        # the pinned buffer over UVA: no separate upload kernel and PCIe round
+        # trip on the critical path.  The buffer is rewritten only by the next
+        # layer's CPU experts, which start after that layer's decision event --
+        # i.e. after the device has passed this layer's consumer.
+        return out
 
     def _cpu_rows(self, l: int, rows_host: torch.Tensor, offs_np: np.ndarray, rec,
                   R: int) -> torch.Tensor | None:
