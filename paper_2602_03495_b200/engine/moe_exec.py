@@ -467,13 +467,11 @@ class MoEExecMixin:
         tp2 = time.perf_counter()
         rec = self.policy.record(ri)
         offs_np = hv["offsets"].numpy()
-        job = None
-        if self._cpu_async:
-            # the CPU experts start first on the pool's workers while this
-            # thread dispatches the GPU experts and copies of the same layer;
-            # _cpu_finish then joins the pool (this thread takes the remaining
-            # work units)
-            job = self._cpu_submit(l, xp_host, offs_np, rec, R)
+        # the CPU experts start first on the pool's workers while this thread
+        # dispatches the GPU experts and copies of the same layer; _cpu_finish
+        # then joins the pool (this thread takes the remaining work units).
+        # DALI_CPU_ASYNC=0: GPU work first, then the CPU experts synchronously.
+        job = self._cpu_submit(l, xp_host, offs_np, rec, R) if self._cpu_async else None
         tp_sub = time.perf_counter()
         try:
             wl_np = hv["wl"].numpy().copy()
@@ -481,25 +479,14 @@ class MoEExecMixin:
             if self.cfg.capture:
                 self.stats.captured.append((step, l, views["h_host"].clone()))
                 self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
-        except BaseException:
-            if job is not None and job["native"]:
-                _lib.load().dali_cpu_expert_wait()
-            raise
-        if self._cpu_async:
-            try:
-                yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
-                y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
-            except BaseException:
-                if job is not None and job["native"]:
-                    _lib.load().dali_cpu_expert_wait()     # never leave a job in flight
-                raise
-            tp3 = time.perf_counter()
-        else:
-            # GPU work is queued first (it runs during the CPU experts), then the
-            # CPU experts run on this thread's pool
             yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
             y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
-            tp3 = time.perf_counter()
+        except BaseException:
+            if job is not None and job["native"]:
+                _lib.load().dali_cpu_expert_wait()     # never leave a job in flight
+            raise
+        tp3 = time.perf_counter()
+        if not self._cpu_async:
             job = self._cpu_submit(l, xp_host, offs_np, rec, R)
         cpu_rows = self._cpu_finish(job, R)
         tp4 = time.perf_counter()
