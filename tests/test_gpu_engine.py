@@ -653,3 +653,19 @@ def test_decode_gemv_vs_torch(B, M, K):
               torch.cuda.current_stream().cuda_stream)
     ref = x.float() @ w.float().t()
     torch.testing.assert_close(y.float(), ref, rtol=1e-2, atol=1e-2 * ref.abs().max().item())
+
+
+def test_tc_ffn_single_cta_wide_path_subprocess():
+    """The single-CTA persistent BN=256 kernel (DALI_FFN_PAIR=0, the A/B
+    alternative to the CTA-pair kernel) passes the same FFN parity cases."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DALI_FFN_PAIR="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p",
+                        "no:cacheprovider",
+                        f"{__file__}::test_tc_ffn_matches_simt_and_torch"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
