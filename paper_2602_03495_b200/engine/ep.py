@@ -332,6 +332,7 @@ class EPMoEMixin:
         for s_ in range(1, splits):
             y_l += yp[s_, :R]
         if cpu_rows is not None:
+            cpu_rows = cpu_rows[:R].to(y_l.device)          # pinned host rows -> HBM, once
             for e in range(NL):
                 if rec.C[e] and offs_l[e + 1] > offs_l[e]:
                     y_l[offs_l[e]:offs_l[e + 1]] = cpu_rows[offs_l[e]:offs_l[e + 1]]
