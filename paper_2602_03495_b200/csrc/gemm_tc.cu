@@ -308,11 +308,37 @@ struct PSmem {
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;      // one accumulator stage
   static constexpr int TMEM_COLS = 2 * ACC_COLS;          // <= 512
   static constexpr size_t BYTES =
-      (size_t)STAGES * (A_BYTES + B_BYTES) + 64 * 17 * 4 + 1024 + 512;
+      (size_t)STAGES * (A_BYTES + B_BYTES) + 2 * 64 * 17 * 4 + 1024 + 512;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+
+// SwiGLU epilogue of one 16-column accumulator chunk for wide token tiles:
+// rows 0-63 of the 128-row tile are gate, 64-127 up (block layout).  Both
+// halves go through shared memory so that all 128 epilogue threads finish 8
+// (SwiGLU column, token) outputs each -- half the per-thread exp/mul work of
+// letting the 64 gate-row threads do it alone.  r = this thread's accumulator
+// row (0..127, a permutation of the epilogue threads).
+__device__ __forceinline__ void swiglu_chunk(const float (&v)[16], int r, float* sG, float* sU,
+                                             int c0, int n_valid, int m_tile, int row0,
+                                             int out_ld, uint16_t* __restrict__ H) {
+  float* dst = r < 64 ? sG + r * 17 : sU + (r - 64) * 17;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) dst[i] = v[i];
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const int j = r & 63, h = r >> 6;
+  const int col = m_tile * 64 + j;
+#pragma unroll
+  for (int i = 8 * h; i < 8 * h + 8; ++i) {
+    const int c = c0 + i;
+    if (c < n_valid) {
+      const float g = sG[j * 17 + i], u = sU[j * 17 + i];
+      H[(int64_t)(row0 + c) * out_ld + col] = f32_to_bf16_bits(g / (1.0f + __expf(-g)) * u);
+    }
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
 template <int BN>
@@ -339,7 +365,8 @@ ffn_tc_persistent(const __grid_constant__ CUtensorMap b_map, const int32_t* __re
   uint8_t* sA = base;
   uint8_t* sB = base + S::STAGES * S::A_BYTES;
   float* sU = reinterpret_cast<float*>(sB + S::STAGES * S::B_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sU + 64 * 17);
+  float* sG = sU + 64 * 17;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sG + 64 * 17);
   uint64_t* empty = full + S::STAGES;
   uint64_t* tfull = empty + S::STAGES;      // [2]
   uint64_t* tempty = tfull + 2;             // [2]
@@ -433,23 +460,7 @@ ffn_tc_persistent(const __grid_constant__ CUtensorMap b_map, const int32_t* __re
         float v[16];
         tmem_ld16(lane_addr + c0, v);
         if (MODE == 0) {
-          if (r >= 64) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) sU[(r - 64) * 17 + i] = v[i];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (r < 64) {
-            const int j = t.m_tile * 64 + r;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int c = c0 + i;
-              if (c < t.n_valid) {
-                const float g = v[i], u = sU[r * 17 + i];
-                H[(int64_t)(t.row0 + c) * out_ld + j] = f32_to_bf16_bits(g / (1.0f + __expf(-g)) * u);
-              }
-            }
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          swiglu_chunk(v, r, sG, sU, c0, t.n_valid, t.m_tile, t.row0, out_ld, H);
         } else {
           const int m = t.m_tile * BM + r;
           float* y = Y + (int64_t)t.split * y_plane;
@@ -497,7 +508,7 @@ struct PairSmem {
   static constexpr int STAGES = 6;
   static constexpr int TMEM_COLS = 2 * BN;               // two accumulator stages
   static constexpr size_t BYTES =
-      (size_t)STAGES * (A_BYTES + B_BYTES) + 64 * 17 * 4 + 1024 + 512;
+      (size_t)STAGES * (A_BYTES + B_BYTES) + 2 * 64 * 17 * 4 + 1024 + 512;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -577,7 +588,8 @@ ffn_tc_pair(const __grid_constant__ CUtensorMap b_map, const int32_t* __restrict
   uint8_t* sA = base;
   uint8_t* sB = base + S::STAGES * S::A_BYTES;
   float* sU = reinterpret_cast<float*>(sB + S::STAGES * S::B_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sU + 64 * 17);
+  float* sG = sU + 64 * 17;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sG + 64 * 17);
   uint64_t* empty = full + S::STAGES;
   uint64_t* tfull = empty + S::STAGES;      // [2]
   uint64_t* tempty = tfull + 2;             // [2]
@@ -679,23 +691,7 @@ ffn_tc_pair(const __grid_constant__ CUtensorMap b_map, const int32_t* __restrict
         float v[16];
         tmem_ld16(lane_addr + c0, v);
         if (MODE == 0) {
-          if (r >= 64) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) sU[(r - 64) * 17 + i] = v[i];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (r < 64) {
-            const int j = t.m_tile * 64 + r;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int c = c0 + i;
-              if (c < t.n_valid) {
-                const float g = v[i], u = sU[r * 17 + i];
-                H[(int64_t)(t.row0 + c) * out_ld + j] = f32_to_bf16_bits(g / (1.0f + __expf(-g)) * u);
-              }
-            }
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          swiglu_chunk(v, r, sG, sU, c0, t.n_valid, t.m_tile, t.row0, out_ld, H);
         } else {
           const int m = t.m_tile * BM + r;
           float* y = Y + (int64_t)t.split * y_plane;
