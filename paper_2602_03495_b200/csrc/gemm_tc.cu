@@ -949,7 +949,9 @@ extern "C" int dali_expert_ffn_tc(const uint16_t* xp, const int32_t* offsets, in
   if (mr <= 128)
     return tc::launch_persistent<128>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf,
                                       yp, splits, xp, st, nsm);
-  if (tc::use_pair())
+  // CTA pairs tile M in 256-row pairs: both projections need an even count
+  // of 128-row weight tiles (true for every shipped config)
+  if (tc::use_pair() && ((2 * f) / tc::BM) % 2 == 0 && (d / tc::BM) % 2 == 0)
     return tc::launch_pair<256>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp,
                                 splits, xp, st, nsm);
   return tc::launch_persistent<256>(offsets, expert_maps, N, d, f, rows, n_gpu_experts, hbuf, yp,

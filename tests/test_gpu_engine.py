@@ -191,6 +191,7 @@ def test_engine_kernel_pieces_vs_torch():
     (256, 512, [100, 128, 129, 0, 3, 60, 250, 300], 4),
     (4096, 1024, [1, 1, 0, 0, 0, 0, 0, 0], 8),
     (256, 512, [600, 7, 0, 513, 0, 0, 1, 0], 1),          # 3 token tiles per weight tile
+    (384, 576, [300, 0, 1, 290, 0, 0, 0, 0], 1),          # odd weight-tile counts (3 / 9)
 ])
 def test_tc_ffn_matches_simt_and_torch(d, f, counts, splits):
     """tcgen05/TMA grouped FFN vs the CUDA-core kernel and a torch fp32 reference."""
