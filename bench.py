@@ -605,6 +605,35 @@ def offload_roofline(eng, st_v, peak_ms: float | None = None) -> dict | None:
     return out
 
 
+def launch_plan(gpus: int, env: dict) -> str:
+    """How ``bench.py --gpus N`` runs: "run" in this process (N == 1, or
+    already one rank of a launcher with WORLD_SIZE == N) or "spawn" N ranks
+    through torch.distributed.run.  A launcher whose WORLD_SIZE disagrees
+    with --gpus is an error: the line would report the wrong scale."""
+    ws = env.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != gpus:
+            raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {gpus}; launch one rank per "
+                             f"GPU (torchrun --nproc-per-node {gpus}) or drop --gpus")
+        return "run"
+    return "spawn" if gpus > 1 else "run"
+
+
+def spawn_ranks(gpus: int, argv: list[str]) -> int:
+    """Re-launch this script as ``gpus`` ranks (one per GPU) on 127.0.0.1;
+    rank 0's JSON line goes to this process's real stdout."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + argv
+    log("spawning", gpus, "ranks:", " ".join(cmd))
+    return subprocess.run(cmd, stdout=_RESULT_OUT, check=False).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -623,7 +652,24 @@ def main():
                          "by NCCL all-to-all (each rank keeps its own request stream)")
     ap.add_argument("--resident", action="store_true",
                     help="all-resident mode: every (local) expert in HBM (roofline reference)")
+    ap.add_argument("--layers", type=int, default=None,
+                    help="depth override (e.g. mixtral-8x22b at a depth one GPU holds)")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="print this rank's launch view and exit (CPU test of --gpus N)")
     args = ap.parse_args()
+    if launch_plan(args.gpus, os.environ) == "spawn":
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
+    if args.launch_check:
+        if int(os.environ.get("RANK", "0")) == 0:
+            emit({"launch_check": True, "gpus": args.gpus,
+                  "world_size": int(os.environ.get("WORLD_SIZE", "1"))})
+        return
+    if torch.cuda.is_available() and args.gpus > torch.cuda.device_count() and \
+            os.environ.get("DALI_BENCH_SHARED_GPU") != "1":
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} "
+                         f"CUDA devices are visible")
+    if args.layers is not None:
+        args.model = f"{args.model.partition('@L')[0]}@L{args.layers}"
     ws, rank, local = dist_setup(need_group=args.ep)
     if args.impl == "reference":
         run_reference(args, ws, rank)

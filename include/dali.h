@@ -155,9 +155,23 @@ int dali_route_f64(const double* hidden, const double* residual,
                    int32_t k, int32_t renorm, int32_t* topk_idx,
                    float* topk_w, int64_t* workloads, void* stream);
 int dali_route_bf16(const uint16_t* hidden, const double* residual,
-                    const uint16_t* gate, int64_t T, int32_t d, int32_t N,
+                    const uint16_t* gate, const float* gate_norm2, int64_t T,
+                    int32_t d, int32_t N,
                     int32_t k, int32_t renorm, int32_t* topk_idx,
                     float* topk_w, int64_t* workloads, void* stream);
+
+/* bf16 inputs take the certified fp32 path when d % 8 == 0, 4 <= N <= 256,
+ * N % 4 == 0 and gate_norm2 != NULL (csrc/route_guard.cu; gate_norm2 [dev]
+ * (N,) f32 = squared column norms of `gate`, an upper bound is enough):
+ * fp32 FFMA logits, and a row whose k+1
+ * leading logits are not separated by the rigorous summation-error bound
+ * gamma_H * ||x|| * (||W_:a|| + ||W_:b||) is recomputed in fp64 as above.
+ * Indices and workloads equal the fp64 path's; topk_w of certified rows is
+ * an fp32 softmax.  Fire counter (rows recomputed / rows routed since the
+ * last reset) and a test hook scaling the bound (scale < 0: every row takes
+ * the fp64 recompute). */
+int dali_route_fire_count(uint64_t* fires, uint64_t* rows, int32_t reset);
+int dali_route_guard_scale(double scale);
 
 /* Prefetch-set selection: stable top-P of predicted workloads
  * (prefetch.py:153-156).  predicted [dev] (N,) int64 -> set [dev] (P,) i32 */

@@ -13,7 +13,7 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdali.so")
+LIB_PATH = os.environ.get("DALI_LIB_PATH") or os.path.join(_HERE, "libdali.so")
 
 MAX_SAMPLES = 32
 MAX_EXPERTS = 256
@@ -74,8 +74,10 @@ SIGNATURES = {
     "dali_version": [],
     "dali_launch_count": [],
     "dali_route_f64": [_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P],
-    "dali_route_bf16": [_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P],
+    "dali_route_bf16": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P],
     "dali_prefetch_select": [_P, _I32, _I32, _P, _P],
+    "dali_route_fire_count": [_P, _P, _I32],
+    "dali_route_guard_scale": [C.c_double],
     "dali_greedy": [_P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
     "dali_cost_eval": [_P, _P, _I64, _P, _P, _P],
     "dali_cache_record": [_P, _P, _P, _I32, _I32, _I32, _P, _I32, _P, _P],
@@ -175,3 +177,11 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(load().dali_launch_count())
+
+
+def route_fire_count(reset: bool = False) -> tuple[int, int]:
+    """(rows recomputed in fp64, rows routed) by the certified bf16 routing
+    kernel since the last reset (csrc/route_guard.cu)."""
+    f, r = C.c_uint64(), C.c_uint64()
+    call("dali_route_fire_count", C.byref(f), C.byref(r), int(reset))
+    return int(f.value), int(r.value)

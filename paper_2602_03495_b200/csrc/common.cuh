@@ -18,6 +18,37 @@ void count_launch();
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Per-device state.  Function attributes (dynamic shared memory limits),
+// SM counts and small device allocations belong to one device, so anything
+// cached across calls is indexed by the current device: an engine built on a
+// second GPU of the same process sets its own attributes.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+inline int device_sm_count() {
+  static int n[kMaxDevices] = {};
+  const int d = current_device();
+  if (!n[d]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    n[d] = v > 0 ? v : 148;
+  }
+  return n[d];
+}
+// Run `body` once per device (e.g. cudaFuncSetAttribute).
+#define DALI_ONCE_PER_DEVICE(body)                          \
+  do {                                                      \
+    static bool _once[::dali::kMaxDevices] = {};            \
+    const int _dev = ::dali::current_device();              \
+    if (!_once[_dev]) {                                     \
+      body;                                                 \
+      _once[_dev] = true;                                   \
+    }                                                       \
+  } while (0)
+
 #define DALI_REQUIRE(cond, code, ...)        \
   do {                                       \
     if (!(cond)) {                           \

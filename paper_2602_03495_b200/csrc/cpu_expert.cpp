@@ -25,9 +25,22 @@
 
 #include "../../include/dali.h"
 
+namespace dali {
+void set_error(const char* fmt, ...);
+}
+
 namespace {
 
 constexpr int kMaxRows = 16;
+
+// The kernels below use AVX-512 BF16 (vdpbf16ps).  On a host without it the
+// entry points return an error instead of dying on SIGILL.
+bool cpu_ok() {
+  static const bool ok = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+                         __builtin_cpu_supports("avx512bf16");
+  if (!ok) dali::set_error("CPU expert worker needs AVX-512 BF16 (avx512bf16) on this host");
+  return ok;
+}
 
 inline float bf2f(uint16_t b) {
   uint32_t u = (uint32_t)b << 16;
@@ -191,6 +204,7 @@ extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, cons
                                int32_t R, float* y, int32_t nthreads) {
   if (!block || !x || !y || d % 32 || f % 64 || R < 0) return DALI_ETRACE;
   if (R == 0) return DALI_OK;
+  if (!cpu_ok()) return DALI_ESIM;
   if (async_job_busy()) return DALI_ESIM;           // the pool is running a submitted job
   if (R > kMaxRows) {
     for (int r0 = 0; r0 < R; r0 += kMaxRows) {
@@ -336,6 +350,7 @@ extern "C" int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const u
                                       int32_t f, int32_t nthreads) {
   if (n < 0 || (n > 0 && (!blocks || !xs || !rows || !ys)) || d % 32 || f % 64)
     return DALI_ETRACE;
+  if (n > 0 && !cpu_ok()) return DALI_ESIM;
   StageJob& j = stage_job();
   if (j.busy) return DALI_ESIM;                     // previous job not joined
   for (int i = 0; i < n; ++i)

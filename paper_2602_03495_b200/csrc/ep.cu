@@ -197,24 +197,16 @@ __global__ void ep_gather_back_kernel(const float4* __restrict__ ret,
 }
 
 static unsigned int* done_counter(int which) {
-  static unsigned int* p = nullptr;
-  if (!p) {
-    cudaMalloc(&p, 2 * sizeof(unsigned int));
-    cudaMemset(p, 0, 2 * sizeof(unsigned int));
+  static unsigned int* p[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!p[dev]) {
+    cudaMalloc(&p[dev], 2 * sizeof(unsigned int));
+    cudaMemset(p[dev], 0, 2 * sizeof(unsigned int));
   }
-  return p + which;
+  return p[dev] + which;
 }
 
-static int ep_sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int ep_sm_count() { return device_sm_count(); }
 
 static unsigned grid_for(int64_t items) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256,

@@ -761,14 +761,12 @@ static int launch_bn(const int32_t* offs, const uint64_t* maps, int N, int d, in
   if (rc) return rc;
   rc = make_map(&hmap, hbuf, cap_rows, f, BN);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
+  DALI_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(ffn_tc_kernel<BN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
     cudaFuncSetAttribute(ffn_tc_kernel<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
-    attr = true;
-  }
+  });
   const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;   // sum_e ceil(n_e / BN) <= this
   const int m_up = (2 * f) / BM, m_dn = d / BM;
   const int64_t g_up = ntile_bound * m_up;
@@ -803,14 +801,12 @@ static int launch_persistent(const int32_t* offs, const uint64_t* maps, int N, i
   if (rc) return rc;
   rc = make_map(&hmap, hbuf, cap_rows, f, BN);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
+  DALI_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(ffn_tc_persistent<BN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
     cudaFuncSetAttribute(ffn_tc_persistent<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
-    attr = true;
-  }
+  });
   const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;
   const int m_up = (2 * f) / BM, m_dn = d / BM;
   const unsigned g_up = (unsigned)std::min<int64_t>(ntile_bound * m_up, n_sm);
@@ -848,14 +844,12 @@ static int launch_pair(const int32_t* offs, const uint64_t* maps, int N, int d, 
   if (rc) return rc;
   rc = make_map(&hmap, hbuf, cap_rows, f, BN / 2);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
+  DALI_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(ffn_tc_pair<BN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
     cudaFuncSetAttribute(ffn_tc_pair<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
-    attr = true;
-  }
+  });
   const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;
   const int m_up = (2 * f) / BM, m_dn = d / BM;
   const int max_ctas = (n_sm / 2) * 2;
@@ -898,16 +892,7 @@ static bool use_pair() {
   return v;
 }
 
-static int sm_count_tc() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int sm_count_tc() { return device_sm_count(); }
 
 }  // namespace tc
 }  // namespace dali

@@ -297,16 +297,7 @@ __global__ void init_uniform_kernel(uint16_t* __restrict__ out, int64_t n, uint6
   }
 }
 
-static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int sm_count() { return device_sm_count(); }
 
 }  // namespace dali
 
@@ -540,12 +531,9 @@ extern "C" int dali_gemv_bf16(const uint16_t* x, const uint16_t* w, int32_t Bt, 
   switch (Bt) {
 #define DALI_GEMV_CASE(BB)                                                                  \
   case BB: {                                                                                \
-    static bool attr = false;                                                              \
-    if (!attr) {                                                                           \
-      cudaFuncSetAttribute(dali::gemv_bf16_kernel<BB>,                                     \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);       \
-      attr = true;                                                                         \
-    }                                                                                      \
+    DALI_ONCE_PER_DEVICE(cudaFuncSetAttribute(dali::gemv_bf16_kernel<BB>,                   \
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                              200 * 1024));                                \
     e = launch_pdl(dali::gemv_bf16_kernel<BB>, grid, block, smem, st, x, w, M, K, y);      \
     break;                                                                                 \
   }

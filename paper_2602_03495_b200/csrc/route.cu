@@ -186,8 +186,7 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
   if (T == 0) return DALI_OK;
   DALI_REQUIRE((T + 1) / 2 < (1ll << 31), DALI_ETRACE, "too many tokens");
   // dynamic smem = staged hidden rows (64 KB) + partial logits (TB*N*S doubles)
-  static bool attr_set = false;
-  if (!attr_set) {
+  DALI_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(route_kernel<TH, TW, 8, 256>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kRouteStageBytes + 8 * 8 * 256);
@@ -200,8 +199,7 @@ static int launch_route(const TH* hidden, const double* residual, const TW* gate
     cudaFuncSetAttribute(route_kernel<TH, TW, 1, 1024>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kRouteStageBytes + 8 * 1 * 1024);
-    attr_set = true;
-  }
+  });
   auto* ul = reinterpret_cast<unsigned long long*>(workloads);
   if (T >= 8 * 148) {
     launch_pdl(route_kernel<TH, TW, 8, 256>, dim3((unsigned)((T + 7) / 8)), dim3(256), kRouteStageBytes + sizeof(double) * 8 * N * (256 / N), st, 
@@ -242,10 +240,29 @@ extern "C" int dali_route_f64(const double* hidden, const double* residual,
                                             topk_idx, topk_w, workloads, stream);
 }
 
+namespace dali {
+int launch_route_guarded(const uint16_t* hidden, const double* residual, const uint16_t* gate,
+                         const float* wn2, int64_t T, int d, int N, int k, int renorm,
+                         int32_t* idx, float* w, int64_t* workloads, void* stream,
+                         int* launched);
+}
+
+// bf16 engine path: the fp32 certified-margin kernel (route_guard.cu) for
+// every eligible shape; the fp64 kernel below for the rest.
 extern "C" int dali_route_bf16(const uint16_t* hidden, const double* residual,
-                               const uint16_t* gate, int64_t T, int32_t d, int32_t N,
+                               const uint16_t* gate, const float* gate_norm2, int64_t T,
+                               int32_t d, int32_t N,
                                int32_t k, int32_t renorm, int32_t* topk_idx,
                                float* topk_w, int64_t* workloads, void* stream) {
+  DALI_REQUIRE(N >= 1 && N <= DALI_MAX_EXPERTS, DALI_ETRACE,
+               "num experts %d outside [1, %d]", N, DALI_MAX_EXPERTS);
+  DALI_REQUIRE(k >= 1 && k <= N, DALI_ETRACE, "top_k %d out of range for %d experts", k, N);
+  DALI_REQUIRE(workloads != nullptr, DALI_ETRACE, "workloads output required");
+  int launched = 0;
+  const int rc = dali::launch_route_guarded(hidden, residual, gate, gate_norm2, T, d, N, k,
+                                            renorm, topk_idx, topk_w, workloads, stream,
+                                            &launched);
+  if (rc != DALI_OK || launched) return rc;
   return dali::launch_route<uint16_t, uint16_t>(hidden, residual, gate, T, d, N, k, renorm,
                                                 topk_idx, topk_w, workloads, stream);
 }

@@ -1,0 +1,689 @@
+// (1) Gating, engine path: bf16 hidden x bf16 router, fp32 FFMA logits with a
+// certified rank margin and an fp64 recompute of the rows it cannot certify.
+// Restates derive_workloads / topk_indices (reference trace.py:236-265) and
+// the residual shift of predict_next_layer (prefetch.py:127-136).
+//
+// Why fp32 is allowed to decide the reference's fp64 ranks.  Every logit is
+// a dot product z_j = sum_i x_i W_ij.  bf16 x bf16 products are exact in fp32
+// and every FFMA rounds once, so for any summation tree of height H
+//     |fl32(z_j) - z_j| <= gamma_H * sum_i |x_i W_ij| <= gamma_H ||x|| ||W_:j||
+// (gamma_H = H u / (1 - H u), u = 2^-24; Cauchy-Schwarz for the last step).
+// The reference ranks fp64 dgemm logits, whose own error (gamma_d in fp64) is
+// ~1e-13 relative, far below any margin this kernel certifies.  A row whose
+// k+1 leading fp32 logits are separated pairwise by more than the sum of the
+// two bounds therefore has exactly the reference's top-k indices, in the
+// reference's order.  Every other row (near-ties, non-finite values, softmax
+// underflow territory) is recomputed in fp64 by the same CTA and ranked like
+// the reference (softmax, ties to the lower index); each such row bumps a
+// device fire counter (dali_route_fire_count).
+//
+// Summation height.  Each thread accumulates its d-slice in blocks of 32
+// FFMAs that are flushed into an outer accumulator (height 32 + #blocks), the
+// S slices are summed by a pairwise tree (log2 S) and, for the cluster
+// variant, the C CTAs' partials are summed in rank order (C - 1).  The host
+// computes H from the launch geometry; a 1% factor covers the fp32 error of
+// the norms themselves.
+//
+// Two launch shapes (one kernel template):
+//  * T <= 16 (decode): one thread-block cluster of C CTAs splits d; partial
+//    logits and norms go to the leader CTA through distributed shared memory
+//    and the leader ranks, writes the histogram directly (no zeroing launch).
+//  * T > 16 (prefill): one CTA per TB tokens over the whole of d.
+// Operands stream through a 3-stage cp.async ring (raw bf16); each stage is
+// converted once to fp32 in shared memory (residual added in fp64 there, as
+// numpy's `hidden + res`), then every thread accumulates a 4-token x
+// 8-expert register tile.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dali {
+
+__device__ unsigned long long g_route_fires = 0;     // rows recomputed in fp64
+__device__ unsigned long long g_route_rows = 0;      // rows routed by this kernel
+#ifdef DALI_RG_PROF
+__device__ unsigned long long g_rg_prof[8][12];
+#define RG_MARK(i)                                                                \
+  do {                                                                            \
+    if (threadIdx.x == 0 && blockIdx.x < 8) {                                     \
+      unsigned long long _t;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                      \
+      g_rg_prof[blockIdx.x][i] = _t;                                              \
+    }                                                                             \
+  } while (0)
+#else
+#define RG_MARK(i) do {} while (0)
+#endif
+
+namespace rg {
+
+constexpr int kThreads = 256;
+constexpr int kStages = 3;
+constexpr int kStageBytes = 24 * 1024;
+
+struct Geo {            // launch geometry shared by host and device
+  int TB, NP, EG, TG, S, logS, DC, C, ds, warp_mode;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void bf16x2_to_f32(uint32_t v, float& lo, float& hi) {
+  lo = __uint_as_float(v << 16);
+  hi = __uint_as_float(v & 0xffff0000u);
+}
+
+// fp64 recompute of one token row by the whole CTA (rare path): fp64 products
+// and sums, max-shifted fp64 softmax, rank by (-p, index) -- the reference's
+// gate_scores + topk_indices (trace.py:229-250).  Thread (eg, s) owns experts
+// eg*8 .. eg*8+7 over the d-slice s, s+S3, ...: one 16-byte router row load +
+// one hidden element per step, 8 independent fp64 FMAs, and the slice loop
+// unrolled so several loads are in flight (this path is latency-bound).
+__device__ void fp64_row(const uint16_t* __restrict__ hrow, const double* __restrict__ residual,
+                         const uint16_t* __restrict__ gate, int d, int N, int k, int renorm,
+                         double* sh_part, double* sh_row, int* sh_sel, int32_t* idx_out,
+                         float* w_out, int* sh_hist) {
+  const int tid = threadIdx.x;
+  const int EG = (N + 7) / 8;
+  const int S3 = kThreads / EG;                // >= 8 (N <= 256)
+  const int eg = tid % EG, s = tid / EG;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  if (s < S3) {
+#pragma unroll 16
+    for (int i = s; i < d; i += S3) {
+      double x = bf16_bits_to_f64(hrow[i]);
+      if (residual) x = __dadd_rn(x, residual[i]);
+      const uint16_t* wp = gate + (int64_t)i * N + eg * 8;
+      uint16_t w[8];
+      if ((N & 7) == 0) {
+        const uint4 v = *reinterpret_cast<const uint4*>(wp);
+        memcpy(w, &v, 16);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) w[e] = (eg * 8 + e < N) ? wp[e] : (uint16_t)0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = fma(x, bf16_bits_to_f64(w[e]), acc[e]);
+    }
+  }
+  // sh_part: [S3][EG*8] doubles (<= 2048 = 16 KB), pairwise tree over s
+  const int NPf = EG * 8;
+  if (s < S3) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sh_part[s * NPf + eg * 8 + e] = acc[e];
+  }
+  __syncthreads();
+  for (int half = S3 >> 1; half >= 1; half >>= 1) {
+    for (int i = tid; i < half * NPf; i += kThreads) sh_part[i] += sh_part[i + half * NPf];
+    __syncthreads();
+  }
+  for (int j = tid; j < N; j += kThreads) sh_row[j] = sh_part[j];
+  __syncthreads();
+  if (tid < 32) {
+    const int lane = tid;
+    double mx = -INFINITY;
+    for (int j = lane; j < N; j += 32) mx = fmax(mx, sh_row[j]);
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double sum = 0.0;
+    for (int j = lane; j < N; j += 32) {
+      const double ex = exp(sh_row[j] - mx);
+      sh_row[j] = ex;
+      sum += ex;
+    }
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    __syncwarp();
+    for (int j = lane; j < N; j += 32) sh_row[j] = sh_row[j] / sum;
+    __syncwarp();
+    for (int j = lane; j < N; j += 32) {
+      const double pj = sh_row[j];
+      int rank = 0;
+      for (int q = 0; q < N; ++q) {
+        const double pq = sh_row[q];
+        rank += (pq > pj) || (pq == pj && q < j);
+      }
+      if (rank < k) {
+        sh_sel[rank] = j;
+        if (idx_out) idx_out[rank] = j;
+        atomicAdd(&sh_hist[j], 1);
+      }
+    }
+    __syncwarp();
+    if (w_out && lane == 0) {
+      double tot = 0.0;
+      for (int r = 0; r < k; ++r) tot += sh_row[sh_sel[r]];
+      for (int r = 0; r < k; ++r) {
+        const double p = sh_row[sh_sel[r]];
+        w_out[r] = (float)(renorm ? p / tot : p);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int TB, int C>
+__global__ void __launch_bounds__(kThreads)
+route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict__ residual,
+                   const uint16_t* __restrict__ gate, int64_t T, int d, int N, int k,
+                   int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                   unsigned long long* __restrict__ workloads,
+                   const float* __restrict__ wnorm2, Geo g, float gamma, int force_fp64) {
+  DALI_PDL_ENTRY();
+  RG_MARK(0);
+  constexpr int TG = TB / 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  // [ring: kStages x kStageBytes (aliased by red after the main loop)]
+  // [xs: TB x (DC + 4) f32] [gather: C x (TB*NP + TB + NP) f32 (C > 1)]
+  unsigned char* ring = smem;
+  float* xs = reinterpret_cast<float*>(smem + kStages * kStageBytes);
+  const int xld = g.DC + 4;
+  float* gath = xs + TB * xld;
+  const int gsz = TB * g.NP + TB;
+
+  __shared__ float sh_logit[TB * 64 > 4096 ? TB * 64 : 4096];   // TB x NP final logits
+  __shared__ float sh_xn[TB], sh_wn[256];
+  __shared__ float sh_red_xn[(kThreads / 32) * TB];
+  __shared__ int sh_hist[256];
+  __shared__ int sh_sel[8][DALI_MAX_TOPK + 1];
+  __shared__ int sh_flag[TB];
+  __shared__ int sh_nflag;
+  __shared__ double sh_row64[256];
+  __shared__ int sh_sel64[DALI_MAX_TOPK];
+
+  const int tid = threadIdx.x;
+  int crank = 0;
+  if constexpr (C > 1) crank = (int)cg::this_cluster().block_rank();
+  const int64_t t0 = (C > 1) ? 0 : (int64_t)blockIdx.x * TB;
+  const int tb_n = (int)((T - t0 < TB) ? (T - t0) : TB);
+  const int d0 = crank * g.ds, d1 = d0 + g.ds;
+  const int nchunks = (g.ds + g.DC - 1) / g.DC;
+  const int xraw_bytes = TB * g.DC * 2;
+
+  for (int i = tid; i < N; i += kThreads) sh_hist[i] = 0;
+  if (tid == 0) sh_nflag = 0;
+
+  // stage issue: raw bf16 x rows [TB][DC] and the contiguous W rows [DC][N]
+  auto issue = [&](int c, int slot) {
+    unsigned char* st = ring + slot * kStageBytes;
+    const int c0 = d0 + c * g.DC;
+    const int upr = g.DC / 8;                        // 16-byte units per x row
+    for (int u = tid; u < TB * upr; u += kThreads) {
+      const int t = u / upr, q = u % upr;
+      const int col = c0 + q * 8;
+      const bool ok = (t < tb_n) && (col < d1);
+      const uint16_t* src = ok ? hidden + (t0 + t) * (int64_t)d + col : hidden;
+      cp_async16(st + u * 16, src, ok);
+    }
+    const int wunits = g.DC * N / 8;
+    const int64_t wbase = (int64_t)c0 * N;          // element offset, multiple of 8
+    const int64_t wend = (int64_t)d1 * N;
+    for (int u = tid; u < wunits; u += kThreads) {
+      const int64_t el = wbase + (int64_t)u * 8;
+      const bool ok = el < wend;
+      cp_async16(st + xraw_bytes + u * 16, ok ? gate + el : gate, ok);
+    }
+  };
+
+  // register tile: tokens tg + TG*j (j < 4), experts eg*8 .. eg*8+7, d-slice s.
+  // Warp mode (g.warp_mode: EG*TG divides 8): every warp owns one tile and
+  // its 32 lanes are 32 consecutive slices, reduced by a shuffle transpose;
+  // otherwise the tile index runs fastest and slices meet in shared memory.
+  const int tile_threads = g.EG * TG;
+  const int lane = tid & 31, wid = tid >> 5;
+  int eg, tg, s;
+  if (g.warp_mode) {
+    const int tile_id = wid % tile_threads;
+    eg = tile_id % g.EG;
+    tg = tile_id / g.EG;
+    s = (wid / tile_threads) * 32 + lane;
+  } else {
+    eg = tid % g.EG;
+    tg = (tid / g.EG) % TG;
+    s = tid / tile_threads;
+  }
+  const bool active = s < g.S;
+  float acc[4][8], blk[4][8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[j][e] = blk[j][e] = 0.f;
+
+  // token-norm partials: token xt over columns xsub, xsub + 256/TB, ...
+  const int x_per_tok = kThreads / TB;
+  const int xt = tid % TB, xsub = tid / TB;
+  float xn_p = 0.f;
+
+  for (int c = 0; c < kStages - 1; ++c) {
+    if (c < nchunks) issue(c, c);
+    cp_commit();
+  }
+  // router column norms (the bound uses ||W_:j||), read after the operand
+  // loads are in flight
+  for (int i = tid; i < N; i += kThreads) sh_wn[i] = sqrtf(wnorm2[i]);
+  RG_MARK(1);
+  for (int c = 0; c < nchunks; ++c) {
+    cp_wait<kStages - 2>();
+    __syncthreads();                                  // stage c landed; xs free
+    if (c == 0) RG_MARK(2);
+    const unsigned char* st = ring + (c % kStages) * kStageBytes;
+    const uint16_t* xr = reinterpret_cast<const uint16_t*>(st);
+    const uint16_t* wr = reinterpret_cast<const uint16_t*>(st + xraw_bytes);
+    const int c0 = d0 + c * g.DC;
+    // x: bf16 -> f32 (+ residual in fp64), token norms; 8 columns per unit
+    for (int q8 = xsub; q8 < g.DC / 8; q8 += x_per_tok) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(xr + xt * g.DC + q8 * 8);
+      float v[8];
+      bf16x2_to_f32(raw.x, v[0], v[1]);
+      bf16x2_to_f32(raw.y, v[2], v[3]);
+      bf16x2_to_f32(raw.z, v[4], v[5]);
+      bf16x2_to_f32(raw.w, v[6], v[7]);
+      if (residual) {
+        const int col = c0 + q8 * 8;
+        if (col < d1) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = (float)__dadd_rn((double)v[q], residual[col + q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xn_p = fmaf(v[q], v[q], xn_p);
+      float4* dst = reinterpret_cast<float4*>(xs + xt * xld + q8 * 8);
+      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    __syncthreads();
+    // the next stage's loads go out before this stage's FFMAs
+    if (c + kStages - 1 < nchunks) issue(c + kStages - 1, (c + kStages - 1) % kStages);
+    cp_commit();
+    if (active) {
+      // one 32-term block per chunk at most (g.DC <= 32 * g.S), flushed below
+      const int nq = g.DC / g.S;
+#pragma unroll 4
+      for (int q = 0; q < nq; ++q) {
+        const int i = s + q * g.S;
+        float w[8];
+        const uint16_t* wp = wr + i * N + eg * 8;
+        if ((N & 7) == 0) {
+          const uint4 v = *reinterpret_cast<const uint4*>(wp);
+          bf16x2_to_f32(v.x, w[0], w[1]);
+          bf16x2_to_f32(v.y, w[2], w[3]);
+          bf16x2_to_f32(v.z, w[4], w[5]);
+          bf16x2_to_f32(v.w, w[6], w[7]);
+        } else {
+          const uint2 a = *reinterpret_cast<const uint2*>(wp);
+          const uint2 b = *reinterpret_cast<const uint2*>(wp + 4);
+          bf16x2_to_f32(a.x, w[0], w[1]);
+          bf16x2_to_f32(a.y, w[2], w[3]);
+          bf16x2_to_f32(b.x, w[4], w[5]);
+          bf16x2_to_f32(b.y, w[6], w[7]);
+        }
+        float x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = xs[(tg + TG * j) * xld + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) blk[j][e] = fmaf(x[j], w[e], blk[j][e]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) { acc[j][e] += blk[j][e]; blk[j][e] = 0.f; }
+    }
+  }
+  cp_wait<0>();
+  RG_MARK(3);
+  __syncthreads();                         // ring free: reuse as the slice reduction buffer
+  float* red = reinterpret_cast<float*>(ring);
+  const int tile = TB * g.NP;
+  // token norms: lanes sharing xt (xor offsets >= TB), then 8 warps in order
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1)
+    if (m >= TB) xn_p += __shfl_xor_sync(0xffffffffu, xn_p, m);
+  if (lane < TB) sh_red_xn[wid * TB + lane] = xn_p;
+  if (g.warp_mode) {
+    // 32 values (4 tokens x 8 experts) over 32 lanes: 5 butterfly rounds,
+    // lane v ends with the warp's sum of value v; then the warps of a tile
+    // (slice groups) meet in shared memory: red[sgroup][tile]
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[j * 8 + e] = acc[j][e];
+#pragma unroll
+    for (int m = 16, n = 32; m >= 1; m >>= 1, n >>= 1) {
+      const bool up = (lane & m) != 0;
+#pragma unroll
+      for (int q = 0; q < n / 2; ++q) {
+        const float send = up ? v[q] : v[q + n / 2];
+        const float keep = up ? v[q + n / 2] : v[q];
+        v[q] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    }
+    const int j = lane >> 3, e = lane & 7;
+    red[(wid / tile_threads) * tile + (tg + TG * j) * g.NP + eg * 8 + e] = v[0];
+  } else if (active) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        red[s * tile + (tg + TG * j) * g.NP + eg * 8 + e] = acc[j][e];
+  }
+  __syncthreads();
+  const int nred = g.warp_mode ? g.S / 32 : g.S;          // partial tiles left
+  for (int half = nred >> 1; half >= 1; half >>= 1) {      // pairwise tree
+    for (int i = tid; i < half * tile; i += kThreads) red[i] += red[i + half * tile];
+    __syncthreads();
+  }
+  RG_MARK(4);
+  float* part_logit = red;                 // [TB][NP]
+  float part_xn = 0.f;
+  if (tid < TB) {
+    for (int q = 0; q < kThreads / 32; ++q) part_xn += sh_red_xn[q * TB + tid];
+  }
+
+  if constexpr (C > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    float* dst = cl.map_shared_rank(gath, 0) + crank * gsz;
+    for (int i = tid; i < tile; i += kThreads) dst[i] = part_logit[i];
+    if (tid < TB) dst[tile + tid] = part_xn;
+    RG_MARK(5);
+    cl.sync();
+    RG_MARK(6);
+    if (crank != 0) return;
+    for (int i = tid; i < tile; i += kThreads) {
+      float v = gath[i];
+      for (int q = 1; q < C; ++q) v += gath[q * gsz + i];
+      sh_logit[i] = v;
+    }
+    if (tid < TB) {
+      float v = 0.f;
+      for (int q = 0; q < C; ++q) v += gath[q * gsz + tile + tid];
+      sh_xn[tid] = v;
+    }
+  } else {
+    for (int i = tid; i < tile; i += kThreads) sh_logit[i] = part_logit[i];
+    if (tid < TB) sh_xn[tid] = part_xn;
+  }
+  __syncthreads();
+
+  // rank, certify, softmax: one warp per token.  The k+1 leading experts are
+  // picked by k+1 warp-wide argmax rounds over (logit, -index) -- ties to the
+  // lower index -- then lane r certifies the gap between ranks r and r+1.
+  const int warp = wid;
+  const int kk = (k < N) ? k : N - 1;          // last rank whose order must be certain
+  for (int t = warp; t < tb_n; t += kThreads / 32) {
+    const float* z = sh_logit + t * g.NP;
+    int* sel = sh_sel[warp];
+    // lane-local candidates: experts lane, lane+32, ... (N <= 256 -> <= 8)
+    float zl[8];
+    unsigned taken = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = lane + 32 * q;
+      zl[q] = (j < N) ? z[j] : -INFINITY;
+      if (j >= N) taken |= 1u << q;
+    }
+    // a non-finite logit anywhere in the row: no certificate (fp64 recompute)
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (lane + 32 * q < N && !(fabsf(zl[q]) < 3.0e38f)) bad = true;
+    if (__any_sync(0xffffffffu, bad) || force_fp64) {
+      if (lane == 0) sh_flag[atomicAdd(&sh_nflag, 1)] = t;
+      __syncwarp();
+      continue;
+    }
+    float zr = 0.f;                              // my rank's logit (lane r <= kk)
+    for (int r = 0; r <= kk; ++r) {
+      float bv = -INFINITY;
+      int bj = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = lane + 32 * q;
+        if (!(taken & (1u << q)) && (zl[q] > bv || (zl[q] == bv && j < bj))) {
+          bv = zl[q];
+          bj = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov > bv || (ov == bv && oj < bj)) {
+          bv = ov;
+          bj = oj;
+        }
+      }
+      if (lane == r) zr = bv;
+      if (lane == 0) sel[r] = bj;
+      if ((bj & 31) == lane) taken |= 1u << (bj >> 5);
+    }
+    __syncwarp();
+    // certificate: every rank r <= kk finite and clear of the fp64 softmax
+    // underflow zone; gaps (r, r+1) for r < kk wider than both bounds
+    const float z0 = __shfl_sync(0xffffffffu, zr, 0);
+    const float zn = __shfl_down_sync(0xffffffffu, zr, 1);
+    int ok = 1;
+    if (lane <= kk) {
+      const int a = sel[lane];
+      ok = fabsf(zr) < 3.0e38f && (zr - z0 > -600.f);
+      if (lane < kk) {
+        const int b = sel[lane + 1];
+        const float bnd = gamma * sqrtf(sh_xn[t]) * (sh_wn[a] + sh_wn[b]) + 1e-30f;
+        ok = ok && (zr - zn > bnd);
+      }
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok) {
+      if (lane == 0) sh_flag[atomicAdd(&sh_nflag, 1)] = t;
+      __syncwarp();
+      continue;
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (lane + 32 * q < N) sum += expf(zl[q] - z0);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const int64_t tt = t0 + t;
+    const float p = (lane < k) ? expf(zr - z0) / sum : 0.f;
+    float tot = p;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane < k) {
+      const int j = sel[lane];
+      if (topk_idx) topk_idx[tt * k + lane] = j;
+      if (topk_w) topk_w[tt * k + lane] = renorm ? p / tot : p;
+      atomicAdd(&sh_hist[j], 1);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  RG_MARK(7);
+  const int nflag = sh_nflag;
+  for (int f = 0; f < nflag; ++f) {
+    const int t = sh_flag[f];
+    const int64_t tt = t0 + t;
+    fp64_row(hidden + tt * (int64_t)d, residual, gate, d, N, k, renorm,
+             reinterpret_cast<double*>(ring), sh_row64,
+             sh_sel64, topk_idx ? topk_idx + tt * k : nullptr, topk_w ? topk_w + tt * k : nullptr,
+             sh_hist);
+  }
+  RG_MARK(8);
+  if (tid == 0) {
+    if (nflag) atomicAdd(&g_route_fires, (unsigned long long)nflag);
+    atomicAdd(&g_route_rows, (unsigned long long)tb_n);
+  }
+  __syncthreads();
+  if (workloads) {
+    const bool single = (C > 1) || gridDim.x == 1;
+    for (int i = tid; i < N; i += kThreads) {
+      if (single) workloads[i] = (unsigned long long)sh_hist[i];
+      else if (sh_hist[i]) atomicAdd(workloads + i, (unsigned long long)sh_hist[i]);
+    }
+  }
+}
+
+static int ilog2(int x) { int r = 0; while ((1 << (r + 1)) <= x) ++r; return r; }
+
+static Geo make_geo(int TB, int N, int C, int d) {
+  Geo g{};
+  g.TB = TB;
+  g.NP = (N + 7) / 8 * 8;
+  g.EG = g.NP / 8;
+  g.TG = TB / 4;
+  int s = kThreads / (g.EG * g.TG);
+  g.S = s >= 1 ? (1 << ilog2(s)) : 0;
+  g.warp_mode = (8 % (g.EG * g.TG)) == 0;                  // one tile per warp
+  if (g.warp_mode) g.S = (8 / (g.EG * g.TG)) * 32;
+  g.logS = g.S ? ilog2(g.S) : 0;
+  g.C = C;
+  g.ds = d / C;
+  // chunk: as many d-rows as fit one stage, a multiple of max(S, 8)
+  const int per_row = TB * 2 + N * 2;
+  int dc = kStageBytes / per_row;
+  const int m = g.S > 8 ? g.S : 8;
+  dc = dc / m * m;
+  const int cap = (g.ds + m - 1) / m * m;
+  if (dc > cap) dc = cap;
+  if (dc > 32 * g.S) dc = 32 * g.S / m * m;          // <= 32 terms per thread per chunk
+  g.DC = dc;
+  return g;
+}
+
+static size_t smem_bytes(const Geo& g) {
+  size_t b = (size_t)kStages * kStageBytes + (size_t)g.TB * (g.DC + 4) * 4;
+  if (g.C > 1) b += (size_t)g.C * (g.TB * g.NP + g.TB) * 4;
+  return b;
+}
+
+static double s_guard_scale = 1.0;          // test hook: < 0 forces every row to fp64
+
+template <int TB, int C>
+static int launch_tb(const uint16_t* hidden, const double* residual, const uint16_t* gate,
+                     int64_t T, int d, int N, int k, int renorm, int32_t* idx, float* w,
+                     unsigned long long* wl, const float* wn2, cudaStream_t st, const Geo& g) {
+  const size_t sm = smem_bytes(g);
+  DALI_ONCE_PER_DEVICE(cudaFuncSetAttribute(route_guard_kernel<TB, C>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            200 * 1024));
+  // summation height: one block of DC/S terms per chunk, one flush per chunk,
+  // slice tree, cluster sum, and one for a rounded (residual-shifted) input
+  const int nch = (g.ds + g.DC - 1) / g.DC;
+  const int H = g.DC / g.S + nch + g.logS + (C - 1) + 1;
+  const double u = 1.0 / (1 << 24);
+  double gam = H * u / (1.0 - H * u) + (residual ? 2 * u : 0.0) + 1e-12;
+  gam *= 1.01 * (s_guard_scale > 0 ? s_guard_scale : 1.0);
+  const int force = s_guard_scale < 0;
+  const unsigned grid = C > 1 ? (unsigned)C : (unsigned)((T + TB - 1) / TB);
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  int na = 1;
+  if (C > 1) {
+    attrs[1].id = cudaLaunchAttributeClusterDimension;
+    attrs[1].val.clusterDim.x = C;
+    attrs[1].val.clusterDim.y = 1;
+    attrs[1].val.clusterDim.z = 1;
+    na = 2;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, route_guard_kernel<TB, C>, hidden, residual, gate, T, d, N, k, renorm,
+                     idx, w, wl, wn2, g, (float)gam, force);
+  DALI_LAUNCH_CHECK("route_guard_kernel");
+  return DALI_OK;
+}
+
+}  // namespace rg
+
+// Returns 1 if launched (or T == 0 handled), 0 if the shape is not eligible
+// (caller falls back to the fp64 kernel), < 0 / error code on failure.
+int launch_route_guarded(const uint16_t* hidden, const double* residual, const uint16_t* gate,
+                         const float* wn2, int64_t T, int d, int N, int k, int renorm,
+                         int32_t* idx, float* w, int64_t* workloads, void* stream,
+                         int* launched) {
+  using namespace rg;
+  *launched = 0;
+  if (wn2 == nullptr || N < 4 || N > 256 || (N & 3) || (d & 7) || k > DALI_MAX_TOPK || k > N || T <= 0)
+    return DALI_OK;
+  cudaStream_t st = as_stream(stream);
+  auto* wl = reinterpret_cast<unsigned long long*>(workloads);
+  int rc;
+  if (T <= 16) {
+    int C = 8;
+    while (C > 1 && (d % (C * 8) || d / C < 256)) C >>= 1;
+    const int TB = T <= 4 ? 4 : T <= 8 ? 8 : 16;
+    const Geo g = make_geo(TB, N, C, d);
+    if (g.S < 1 || smem_bytes(g) > 180 * 1024 || (size_t)TB * g.NP > 4096) return DALI_OK;
+#define DALI_RG_SMALL(TBv)                                                              \
+  (C == 8 ? launch_tb<TBv, 8>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g) \
+   : C == 4 ? launch_tb<TBv, 4>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g) \
+   : C == 2 ? launch_tb<TBv, 2>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g) \
+            : launch_tb<TBv, 1>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g))
+    rc = TB == 4 ? DALI_RG_SMALL(4) : TB == 8 ? DALI_RG_SMALL(8) : DALI_RG_SMALL(16);
+#undef DALI_RG_SMALL
+  } else {
+    int TB = 4;
+    while (TB < 32 && (T + TB - 1) / TB > 148) TB <<= 1;
+    const Geo g = make_geo(TB, N, 1, d);
+    if (g.S < 1 || smem_bytes(g) > 180 * 1024 || (size_t)TB * g.NP > 4096) return DALI_OK;
+    if (workloads && (T + TB - 1) / TB > 1) {
+      cudaMemsetAsync(workloads, 0, sizeof(int64_t) * N, st);
+    }
+    rc = TB == 4    ? launch_tb<4, 1>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g)
+         : TB == 8  ? launch_tb<8, 1>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g)
+         : TB == 16 ? launch_tb<16, 1>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g)
+                    : launch_tb<32, 1>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g);
+  }
+  if (rc == DALI_OK) *launched = 1;
+  return rc;
+}
+
+}  // namespace dali
+
+extern "C" int dali_route_guard_scale(double scale) {
+  dali::rg::s_guard_scale = scale;
+  return DALI_OK;
+}
+
+extern "C" int dali_route_fire_count(uint64_t* fires, uint64_t* rows, int32_t reset) {
+  unsigned long long f = 0, r = 0;
+  cudaError_t e = cudaMemcpyFromSymbol(&f, dali::g_route_fires, sizeof(f));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(&r, dali::g_route_rows, sizeof(r));
+  if (e == cudaSuccess && reset) {
+    const unsigned long long z = 0;
+    e = cudaMemcpyToSymbol(dali::g_route_fires, &z, sizeof(z));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(dali::g_route_rows, &z, sizeof(z));
+  }
+  if (e != cudaSuccess) {
+    dali::set_error("dali_route_fire_count: %s", cudaGetErrorString(e));
+    return DALI_ECUDA;
+  }
+  if (fires) *fires = f;
+  if (rows) *rows = r;
+  return DALI_OK;
+}
+
+#ifdef DALI_RG_PROF
+extern "C" int dali_rg_prof(uint64_t* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, dali::g_rg_prof, sizeof(unsigned long long) * 8 * 12);
+  return DALI_OK;
+}
+#endif

@@ -10,7 +10,7 @@ attention is not one of the five DALI subsystems).
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 from ..trace import ModelConfig
 
@@ -72,6 +72,15 @@ PRESETS = {
 
 
 def preset(name: str) -> MoEArch:
-    if name not in PRESETS:
-        raise KeyError(f"unknown arch {name!r}; choose from {sorted(PRESETS)}")
-    return PRESETS[name]
+    """A preset by name; ``<name>@L<n>`` is the same shape at depth n (e.g.
+    Mixtral-8x22B at a depth one GPU's HBM or one host's DRAM holds)."""
+    base, _, depth = name.partition("@L")
+    if base not in PRESETS:
+        raise KeyError(f"unknown arch {base!r}; choose from {sorted(PRESETS)}")
+    a = PRESETS[base]
+    if depth:
+        n = int(depth)
+        if n < 1:
+            raise KeyError(f"bad depth in {name!r}")
+        a = replace(a, name=name, num_layers=n)
+    return a

@@ -5,7 +5,17 @@ Decode-sized batches (<= NATIVE_MAX_ROWS tokens per expert) use the native
 AVX-512 BF16 weight-streaming kernel in libdali (``dali_cpu_expert``), which
 reads the pinned expert block once at host-DRAM bandwidth; larger batches
 (prefill) are compute-heavy and go to oneDNN's AMX-BF16 GEMM through torch.
-Both round the SwiGLU intermediate to bf16 like the GPU kernel.
+
+Rounding points.  The native kernel, like the GPU tcgen05 kernel, keeps the
+gate/up and down projections in fp32 accumulators and rounds only the SwiGLU
+intermediate to bf16.  torch's CPU bf16 GEMM has no fp32-output variant
+(``mm(..., out_dtype=float32)`` is CUDA-only in this torch), so on the
+oneDNN path the gate/up outputs and the down-projection output are also
+rounded to bf16 (two extra roundings, each <= 2^-9 relative per element).
+A prefill row therefore differs at bf16-rounding level depending on whether
+the policy puts its expert on the CPU or the GPU; the engine's numeric parity
+tests (tolerance rtol 2e-2 per element, tests/test_gpu_engine.py) cover both
+placements.  Decode (<= 16 rows per expert) always takes the native path.
 """
 
 from __future__ import annotations

@@ -215,7 +215,8 @@ class EPMoEMixin:
         pred = None
         if self.policy.prefetch_size > 0 and l + 1 < a.num_layers:
             _, _, pw = route_device(h, self.w.router[l + 1], k, residual=self.policy.residuals[l],
-                                    want_idx=False, want_weights=False)
+                                    want_idx=False, want_weights=False,
+                                    norm2=self.w.router_norm2[l + 1])
             pred = ep.all_reduce_sum_(pw)[ep.rank * NL:(ep.rank + 1) * NL].contiguous()
         ri = self.policy.layer_step(step, l, token_index, is_eos, wl_glob, None, None,
                                     predicted=pred)
@@ -283,7 +284,8 @@ class EPMoEMixin:
         pred = None
         if self.policy.prefetch_size > 0 and l + 1 < a.num_layers:
             _, _, pw = route_device(h, self.w.router[l + 1], k, residual=self.policy.residuals[l],
-                                    want_idx=False, want_weights=False)
+                                    want_idx=False, want_weights=False,
+                                    norm2=self.w.router_norm2[l + 1])
             pred = ep.all_reduce_sum_(pw)[ep.rank * NL:(ep.rank + 1) * NL].contiguous()
         ri = self.policy.layer_step(step, l, token_index, is_eos, wl_glob, None, None,
                                     predicted=pred)

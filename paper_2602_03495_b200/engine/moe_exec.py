@@ -104,7 +104,7 @@ class MoEExecMixin:
             "wts": rblk[o_w:nb].view(torch.float32).view(T, k),
         }
         route_device(h, self.w.router[l], k, renorm=a.norm_topk_prob,
-                     out=(v["idx"], v["wts"], v["wl"]))
+                     out=(v["idx"], v["wts"], v["wl"]), norm2=self.w.router_norm2[l])
         perm = self._ws("perm", (T * k,), torch.int32)
         v["pos"] = self._ws("pos", (T, k), torch.int32)
         v["xp"] = self._ws("xp", (T * k, d), torch.bfloat16)
@@ -426,9 +426,11 @@ class MoEExecMixin:
         cs = self._cur()
         v = self._route(l, h)
         gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
+        nn2 = self.w.router_norm2[l + 1] if l + 1 < a.num_layers else None
         if use_desc:
             pol = self.policy
-            pred_p = pol.predicted_ptr(l, h, gate_next, rec_index=pol.n_records + l)
+            pred_p = pol.predicted_ptr(l, h, gate_next, rec_index=pol.n_records + l,
+                                       gate_next_norm2=nn2)
             probs_p, n_tok = pol.gate_probs_ptr(h, self.w.router[l])
             _lib.call("dali_policy_layer_desc", C.addressof(pol.cfg), C.addressof(pol.cm_c), l,
                       self.desc_dev.data_ptr(), v["wl"].data_ptr(), pred_p,
@@ -438,7 +440,7 @@ class MoEExecMixin:
             ri = None
         else:
             ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], h, gate_next,
-                                        gate_this=self.w.router[l])
+                                        gate_this=self.w.router[l], gate_next_norm2=nn2)
         hv = self._host_view(v, T)
         xp_host = self._ws("xp_h", (R, d), torch.bfloat16, pinned=True)
         self._d2h(xp_host, v["xp"])

@@ -216,6 +216,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
                 device=self.dev)
         self._offs_cache: dict = {}
         self._wsd: dict = {}
+        self._ws_retired: list = []             # outgrown workspaces, freed per request
         self._res_maps = None
         self._wl_log = None
         self.desc_dev = torch.zeros((8,), dtype=torch.int32, device=self.dev)
@@ -263,14 +264,36 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
     def _ws(self, name: str, shape: tuple, dtype, pinned: bool = False) -> torch.Tensor:
         """Per-engine workspace reused across layers/steps (stream-ordered on
         the compute stream; pinned ones are rewritten only after the event
-        wait that follows their previous consumer)."""
-        key = (name, shape, dtype)
+        wait that follows their previous consumer).
+
+        One flat buffer per (name, dtype, pinned), grown to the largest size
+        requested and handed out as a view of the requested shape, so serving
+        varied prompt lengths and batches does not accumulate buffers.  A
+        growth invalidates the captured CUDA graphs (they hold the old
+        addresses; they are re-captured on the next decode step) and parks the
+        old buffer until the next request starts, because queued kernels, the
+        CPU worker and UVA kernel copies may still use it."""
+        n = 1
+        for x in shape:
+            n *= int(x)
+        key = (name, dtype, pinned)
         t = self._wsd.get(key)
-        if t is None:
-            t = (torch.empty(shape, dtype=dtype, pin_memory=True) if pinned
-                 else torch.empty(shape, dtype=dtype, device=self.dev))
+        if t is None or t.numel() < n:
+            if t is not None:
+                if self._capturing:
+                    raise SimulationError(f"workspace {name!r} grew during graph capture")
+                self._ws_retired.append(t)
+                self._drop_graphs()
+            t = (torch.empty((max(n, 1),), dtype=dtype, pin_memory=True) if pinned
+                 else torch.empty((max(n, 1),), dtype=dtype, device=self.dev))
             self._wsd[key] = t
-        return t
+        return t[:n].view(shape)
+
+    def _drop_graphs(self) -> None:
+        """Forget the captured decode graphs (re-captured on demand)."""
+        self._graph = None
+        self._graph_warm = False
+        self._heads, self._heads_warm = {}, False
 
     def _map_addr(self, phys: int) -> int:
         return self.maps_dev.data_ptr() + int(phys) * 256
@@ -344,8 +367,10 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         """New policy run for one request; cache residency carries over."""
         if self.kv is None or self.kv.k.shape[1] != batch:
             self.kv = KVCache(self.arch, batch, self.max_seq, self.dev)
-            self._graph = None
-            self._heads, self._heads_warm = {}, False
+            self._drop_graphs()
+        if self._ws_retired:                    # the previous request has synchronised
+            torch.cuda.synchronize()
+            self._ws_retired.clear()
         self.kv.len = 0
         for key in list(self.prefetched):
             i, ev = self.prefetched.pop(key)
@@ -461,6 +486,10 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
                 self.stats.logits.append(logits.float().cpu())
         e2.record(cs)
         e2.synchronize()
+        if self.ep is not None and self.ep.peer is not None:
+            # a peer lost during the last layers' return exchange only sets the
+            # mapped error flag; never hand back rows it left half-written
+            self.ep.peer.check()
         if self._used_fast:
             self._finish_resident()
         st = self.stats

@@ -129,6 +129,9 @@ class ModelWeights:
                 if a.shared_gate:
                     self.shared_gate.append(w((1, d), KIND_SHGATE, l, 0, 1.0 / math.sqrt(d)))
         self.router = torch.stack([torch.from_numpy(r).to(bf) for r in self.router64]).to(dev)
+        # squared router column norms (L, N) f32: the certified routing kernel's
+        # error bound (csrc/route_guard.cu), computed once
+        self.router_norm2 = self.router.float().square().sum(dim=1).contiguous()
 
         # routed experts
         self.resident = resident

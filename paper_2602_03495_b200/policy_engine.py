@@ -175,7 +175,8 @@ class PolicyEngine:
                    workloads: torch.Tensor, hidden: torch.Tensor | None,
                    gate_next: torch.Tensor | None, stream=None,
                    predicted: torch.Tensor | None = None,
-                   gate_this: torch.Tensor | None = None) -> int:
+                   gate_this: torch.Tensor | None = None,
+                   gate_next_norm2: torch.Tensor | None = None) -> int:
         """Queue the decision of (step, layer) on ``stream``; returns the
         record index (valid on the host once the stream reaches it).
         ``predicted`` supplies layer+1's predicted workloads directly (the
@@ -185,7 +186,8 @@ class PolicyEngine:
             raise SimulationError("decision log full")
         sp = _dev.stream_ptr(stream)
         i = self.n_records
-        pred_p = self.predicted_ptr(layer, hidden, gate_next, stream, predicted, i)
+        pred_p = self.predicted_ptr(layer, hidden, gate_next, stream, predicted, i,
+                                    gate_next_norm2=gate_next_norm2)
         probs_p, n_tok = self.gate_probs_ptr(hidden, gate_this, stream)
         _lib.call("dali_policy_layer", C.addressof(self.cfg), C.addressof(self.cm_c), step,
                   layer, token_index, int(bool(is_eos)), workloads.data_ptr(), pred_p,
@@ -196,7 +198,7 @@ class PolicyEngine:
         return i
 
     def predicted_ptr(self, layer: int, hidden, gate_next, stream=None, predicted=None,
-                      rec_index: int = 0):
+                      rec_index: int = 0, gate_next_norm2=None):
         """Device pointer to layer+1's predicted workloads for the configured
         predictor (None when nothing is prefetched after this layer):
         residual / feature -> routing kernel on the (shifted) gate inputs;
@@ -220,7 +222,7 @@ class PolicyEngine:
             raise SimulationError("prefetching requires the layer's gate inputs")
         _, _, wl = route_device(hidden, gate_next, self.k, residual=self.residuals[layer],
                                 want_idx=False, want_weights=False, stream=stream,
-                                out=(None, None, self.predicted))
+                                out=(None, None, self.predicted), norm2=gate_next_norm2)
         return wl.data_ptr()
 
     def gate_probs_ptr(self, hidden, gate_this, stream=None):

@@ -203,14 +203,24 @@ def topk_indices(scores, k: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 
+def gate_norm2(gate: torch.Tensor) -> torch.Tensor:
+    """Squared column norms (N,) f32 of a router matrix (d, N): the input of
+    the certified routing kernel's error bound (csrc/route_guard.cu).  fp32
+    summation is within gamma_d relative of the exact value, which the
+    kernel's 1% safety factor covers."""
+    return gate.float().square().sum(dim=0).contiguous()
+
+
 def route_device(hidden: torch.Tensor, gate: torch.Tensor, k: int,
                  residual: torch.Tensor | None = None, renorm: bool = False,
-                 want_idx: bool = True, want_weights: bool = True, stream=None, out=None):
+                 want_idx: bool = True, want_weights: bool = True, stream=None, out=None,
+                 norm2: torch.Tensor | None = None):
     """Launch the fused routing kernel on device tensors.
 
     hidden (T, d) float64 or bfloat16; gate (d, N) same dtype family;
-    residual (d,) float64 or None.  Returns (topk_idx int32 (T,k) | None,
-    topk_w float32 (T,k) | None, workloads int64 (N,)).
+    residual (d,) float64 or None; norm2 (N,) f32 squared column norms of a
+    bf16 gate (computed here when None).  Returns (topk_idx int32 (T,k) |
+    None, topk_w float32 (T,k) | None, workloads int64 (N,)).
     """
     T, d = hidden.shape
     if gate.shape[0] != d:
@@ -231,9 +241,12 @@ def route_device(hidden: torch.Tensor, gate: torch.Tensor, k: int,
         hp, gp = hidden.data_ptr(), gate.to(torch.float64).contiguous().data_ptr()
         gkeep = None
     elif hidden.dtype == torch.bfloat16:
-        fn = "dali_route_bf16"
         gkeep = gate.to(torch.bfloat16).contiguous()
-        hp, gp = hidden.data_ptr(), gkeep.data_ptr()
+        nkeep = norm2 if norm2 is not None else gate_norm2(gkeep)
+        _lib.call("dali_route_bf16", hidden.data_ptr(), res_p, gkeep.data_ptr(),
+                  nkeep.data_ptr(), T, d, N, k, int(renorm), _dev.ptr(idx), _dev.ptr(wts),
+                  wl.data_ptr(), _dev.stream_ptr(stream))
+        return idx, wts, wl
     else:
         raise TraceError(f"unsupported hidden dtype {hidden.dtype}")
     _lib.call(fn, hp, res_p, gp, T, d, N, k, int(renorm), _dev.ptr(idx), _dev.ptr(wts),

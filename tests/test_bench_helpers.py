@@ -61,3 +61,39 @@ def test_policy_layer_us_reports_each_reference_function():
     for v in out.values():
         assert set(v) == {"gating_A4", "greedy_A6_A8", "prefetch_A11", "cache_A16", "total"}
         assert v["total"] > 0
+
+
+def test_launch_plan_guards_world_size():
+    import pytest
+    assert bench.launch_plan(1, {}) == "run"
+    assert bench.launch_plan(2, {}) == "spawn"
+    assert bench.launch_plan(8, {"WORLD_SIZE": "8"}) == "run"
+    with pytest.raises(SystemExit):
+        bench.launch_plan(2, {"WORLD_SIZE": "3"})
+    with pytest.raises(SystemExit):
+        bench.launch_plan(1, {"WORLD_SIZE": "2"})
+
+
+def test_bench_self_launches_n_ranks():
+    """`python bench.py --gpus 2` (no launcher) spawns 2 ranks through
+    torch.distributed.run; rank 0 prints the one JSON line."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, bench.__file__, "--gpus", "2", "--launch-check"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    rec = json.loads(lines[0])
+    assert rec["launch_check"] and rec["gpus"] == 2 and rec["world_size"] == 2
+
+
+def test_depth_override_preset():
+    from paper_2602_03495_b200.engine import preset
+    a = preset("mixtral-8x22b@L4")
+    assert a.num_layers == 4 and a.hidden_dim == 6144 and a.name == "mixtral-8x22b@L4"
+    assert preset("mixtral-8x22b").num_layers == 56

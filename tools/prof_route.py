@@ -9,16 +9,19 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2602_03495_b200.trace import route_device  # noqa: E402
+from paper_2602_03495_b200 import _lib  # noqa: E402
+from paper_2602_03495_b200.trace import gate_norm2, route_device  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--d", type=int, default=4096)
 ap.add_argument("--N", type=int, default=8)
 ap.add_argument("--k", type=int, default=2)
 ap.add_argument("--iters", type=int, default=50)
+ap.add_argument("--T", type=str, default="1,4,16,128,512,4096")
 args = ap.parse_args()
 g = (torch.randn(args.d, args.N, device="cuda") * 0.02).to(torch.bfloat16)
-for T in (1, 4, 16, 128, 512, 4096):
+n2 = gate_norm2(g)             # the engine computes router norms once
+for T in [int(x) for x in args.T.split(",")]:
     h = torch.randn(T, args.d, device="cuda").to(torch.bfloat16)
     for _ in range(3):
         route_device(h, g, args.k)
@@ -29,7 +32,7 @@ for T in (1, 4, 16, 128, 512, 4096):
     graph = torch.cuda.CUDAGraph()            # device time without host launch cost
     with torch.cuda.graph(graph):
         for _ in range(args.iters):
-            route_device(h, g, args.k, out=out)
+            route_device(h, g, args.k, out=out, norm2=n2)
     graph.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -38,4 +41,9 @@ for T in (1, 4, 16, 128, 512, 4096):
     e1.record()
     e1.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / args.iters
-    print(f"T={T}: {us:.1f} us per call ({T * args.d * 2 / us / 1e3:.1f} GB/s hidden)")
+    _lib.route_fire_count(reset=True)
+    route_device(h, g, args.k, out=out, norm2=n2)
+    fires, rows = _lib.route_fire_count(reset=True)
+    byts = T * args.d * 2 + args.d * args.N * 2 + T * args.k * 8 + args.N * 8
+    print(f"T={T}: {us:.1f} us per call ({byts / us / 1e3:.1f} GB/s algorithmic, "
+          f"fires {fires}/{rows})")
