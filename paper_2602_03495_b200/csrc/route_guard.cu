@@ -82,56 +82,83 @@ __device__ __forceinline__ void bf16x2_to_f32(uint32_t v, float& lo, float& hi) 
   hi = __uint_as_float(v & 0xffff0000u);
 }
 
-// fp64 recompute of one token row by the whole CTA (rare path): fp64 products
-// and sums, max-shifted fp64 softmax, rank by (-p, index) -- the reference's
-// gate_scores + topk_indices (trace.py:229-250).  Thread (eg, s) owns experts
-// eg*8 .. eg*8+7 over the d-slice s, s+S3, ...: one 16-byte router row load +
-// one hidden element per step, 8 independent fp64 FMAs, and the slice loop
-// unrolled so several loads are in flight (this path is latency-bound).
-__device__ void fp64_row(const uint16_t* __restrict__ hrow, const double* __restrict__ residual,
-                         const uint16_t* __restrict__ gate, int d, int N, int k, int renorm,
-                         double* sh_part, double* sh_row, int* sh_sel, int32_t* idx_out,
-                         float* w_out, int* sh_hist) {
+// fp64 recompute of one uncertified row by the whole CTA (rare path).  Only
+// the candidate experts U -- every j whose fp32 upper bound z_j + B_j reaches
+// L = min over the k fp32-leading experts of z - B -- are recomputed: the k
+// leaders certainly beat every expert outside U (their exact logits are >= L
+// > the outsider's), so the exact top-k lies in U and its order is the fp64
+// order within U.  fp64 products and sums, max-shifted fp64 softmax (logits
+// outside U enter the denominator from fp32), rank by (-p, index): the
+// reference's gate_scores + topk_indices (trace.py:229-250).  B200's fp64
+// pipe is narrow, so recomputing 2-4 candidates instead of all N experts is
+// what keeps a fire cheap.
+__device__ __forceinline__ double bf16_to_f64_fast(uint32_t b) {
+  const uint32_t e = (b >> 7) & 0xffu;
+  if (e - 1u < 254u) {                          // normal: rebias exponent, shift mantissa
+    const uint32_t hi = ((b & 0x8000u) << 16) | ((e + 896u) << 20) | ((b & 0x7fu) << 13);
+    return __hiloint2double((int)hi, 0);
+  }
+  return (double)__uint_as_float(b << 16);      // zero / subnormal / inf / nan
+}
+
+__device__ void fp64_row_cand(const uint16_t* __restrict__ hrow,
+                              const double* __restrict__ residual,
+                              const uint16_t* __restrict__ gate, int d, int N, int k, int renorm,
+                              const uint32_t* cmask, const float* z32, double* xs64,
+                              double* sh_part, double* sh_row, int* sh_cl, int* sh_nc,
+                              int32_t* idx_out, float* w_out, int* sh_hist) {
   const int tid = threadIdx.x;
-  const int EG = (N + 7) / 8;
-  const int S3 = kThreads / EG;                // >= 8 (N <= 256)
-  const int eg = tid % EG, s = tid / EG;
-  double acc[8];
+  if (tid < 32) {                                // candidate list, ascending index
+    int base = 0;
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t m = cmask[q];
+      if ((m >> tid) & 1u) sh_cl[base + __popc(m & ((1u << tid) - 1u))] = 32 * q + tid;
+      base += __popc(m);
+    }
+    if (tid == 0) *sh_nc = base;
+  }
+  for (int i = tid; i < d; i += kThreads) {      // the row in fp64 (+ residual), once
+    double x = bf16_to_f64_fast(hrow[i]);
+    if (residual) x = __dadd_rn(x, residual[i]);
+    xs64[i] = x;
+  }
+  __syncthreads();
+  const int nc = *sh_nc;
+  int S = 1;
+  while (2 * S * nc <= kThreads) S *= 2;         // power-of-two slices per candidate
+  const int c = tid % nc, sl = tid / nc;
+  if (sl < S) {
+    const int e = sh_cl[c];
+    double acc0 = 0.0, acc1 = 0.0;
+    constexpr int kB = 16;                      // router loads in flight per thread
+    for (int i0 = sl; i0 < d; i0 += kB * S) {
+      uint16_t w[kB];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-  if (s < S3) {
-#pragma unroll 16
-    for (int i = s; i < d; i += S3) {
-      double x = bf16_bits_to_f64(hrow[i]);
-      if (residual) x = __dadd_rn(x, residual[i]);
-      const uint16_t* wp = gate + (int64_t)i * N + eg * 8;
-      uint16_t w[8];
-      if ((N & 7) == 0) {
-        const uint4 v = *reinterpret_cast<const uint4*>(wp);
-        memcpy(w, &v, 16);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) w[e] = (eg * 8 + e < N) ? wp[e] : (uint16_t)0;
+      for (int b = 0; b < kB; ++b) {
+        const int i = i0 + b * S;
+        w[b] = i < d ? __ldg(gate + (int64_t)i * N + e) : (uint16_t)0;
       }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = fma(x, bf16_bits_to_f64(w[e]), acc[e]);
+      for (int b = 0; b < kB; b += 2) {
+        const int i = i0 + b * S;
+        if (i < d) acc0 = fma(xs64[i], bf16_to_f64_fast(w[b]), acc0);
+        if (i + S < d) acc1 = fma(xs64[i + S], bf16_to_f64_fast(w[b + 1]), acc1);
+      }
     }
-  }
-  // sh_part: [S3][EG*8] doubles (<= 2048 = 16 KB), pairwise tree over s
-  const int NPf = EG * 8;
-  if (s < S3) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) sh_part[s * NPf + eg * 8 + e] = acc[e];
+    sh_part[sl * nc + c] = acc0 + acc1;
   }
   __syncthreads();
-  for (int half = S3 >> 1; half >= 1; half >>= 1) {
-    for (int i = tid; i < half * NPf; i += kThreads) sh_part[i] += sh_part[i + half * NPf];
+  for (int half = S >> 1; half >= 1; half >>= 1) {
+    for (int i = tid; i < half * nc; i += kThreads) sh_part[i] += sh_part[i + half * nc];
     __syncthreads();
   }
-  for (int j = tid; j < N; j += kThreads) sh_row[j] = sh_part[j];
-  __syncthreads();
   if (tid < 32) {
     const int lane = tid;
+    // logits: fp64 for candidates, fp32 for the rest (denominator only)
+    for (int j = lane; j < N; j += 32) sh_row[j] = (double)z32[j];
+    __syncwarp();
+    for (int q = lane; q < nc; q += 32) sh_row[sh_cl[q]] = sh_part[q];
+    __syncwarp();
     double mx = -INFINITY;
     for (int j = lane; j < N; j += 32) mx = fmax(mx, sh_row[j]);
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -145,15 +172,18 @@ __device__ void fp64_row(const uint16_t* __restrict__ hrow, const double* __rest
     __syncwarp();
     for (int j = lane; j < N; j += 32) sh_row[j] = sh_row[j] / sum;
     __syncwarp();
-    for (int j = lane; j < N; j += 32) {
+    int sel[DALI_MAX_TOPK];                    // lane 0 only (k <= 16)
+    for (int q = lane; q < nc; q += 32) {
+      const int j = sh_cl[q];
       const double pj = sh_row[j];
       int rank = 0;
-      for (int q = 0; q < N; ++q) {
-        const double pq = sh_row[q];
-        rank += (pq > pj) || (pq == pj && q < j);
+      for (int u = 0; u < nc; ++u) {
+        const int ju = sh_cl[u];
+        const double pu = sh_row[ju];
+        rank += (pu > pj) || (pu == pj && ju < j);
       }
       if (rank < k) {
-        sh_sel[rank] = j;
+        sh_part[1024 + rank] = (double)j;       // selected ids, rank order
         if (idx_out) idx_out[rank] = j;
         atomicAdd(&sh_hist[j], 1);
       }
@@ -161,9 +191,12 @@ __device__ void fp64_row(const uint16_t* __restrict__ hrow, const double* __rest
     __syncwarp();
     if (w_out && lane == 0) {
       double tot = 0.0;
-      for (int r = 0; r < k; ++r) tot += sh_row[sh_sel[r]];
       for (int r = 0; r < k; ++r) {
-        const double p = sh_row[sh_sel[r]];
+        sel[r] = (int)sh_part[1024 + r];
+        tot += sh_row[sel[r]];
+      }
+      for (int r = 0; r < k; ++r) {
+        const double p = sh_row[sel[r]];
         w_out[r] = (float)(renorm ? p / tot : p);
       }
     }
@@ -198,7 +231,9 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
   __shared__ int sh_flag[TB];
   __shared__ int sh_nflag;
   __shared__ double sh_row64[256];
-  __shared__ int sh_sel64[DALI_MAX_TOPK];
+  __shared__ int sh_cl[256];
+  __shared__ int sh_nc;
+  __shared__ uint32_t sh_cmask[TB][8];
 
   const int tid = threadIdx.x;
   int crank = 0;
@@ -439,7 +474,13 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
     for (int q = 0; q < 8; ++q)
       if (lane + 32 * q < N && !(fabsf(zl[q]) < 3.0e38f)) bad = true;
     if (__any_sync(0xffffffffu, bad) || force_fp64) {
-      if (lane == 0) sh_flag[atomicAdd(&sh_nflag, 1)] = t;
+      if (lane == 0) {
+        const int f = atomicAdd(&sh_nflag, 1);
+        sh_flag[f] = t;
+        for (int q = 0; q < 8; ++q)
+          sh_cmask[f][q] = (32 * q >= N) ? 0u : (N - 32 * q >= 32 ? 0xffffffffu
+                                                                 : ((1u << (N - 32 * q)) - 1u));
+      }
       __syncwarp();
       continue;
     }
@@ -483,9 +524,28 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
         ok = ok && (zr - zn > bnd);
       }
     }
+    const bool spread = __any_sync(0xffffffffu, lane <= kk && !(zr - z0 > -600.f));
     ok = __all_sync(0xffffffffu, ok);
     if (!ok) {
-      if (lane == 0) sh_flag[atomicAdd(&sh_nflag, 1)] = t;
+      // candidates: j with z_j + B_j >= L = min_{r<k} (z_r - B_r); every
+      // expert when the row reaches the fp64 softmax underflow zone
+      const float xnr = gamma * sqrtf(sh_xn[t]);
+      float lo = INFINITY;
+      if (lane < k) lo = zr - (xnr * sh_wn[sel[lane]] + 1e-30f);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      uint32_t words[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = lane + 32 * q;
+        const bool in = j < N && (spread || zl[q] + (xnr * sh_wn[j] + 1e-30f) >= lo);
+        words[q] = __ballot_sync(0xffffffffu, in);
+      }
+      if (lane == 0) {
+        const int f = atomicAdd(&sh_nflag, 1);
+        sh_flag[f] = t;
+        for (int q = 0; q < 8; ++q) sh_cmask[f][q] = words[q];
+      }
       __syncwarp();
       continue;
     }
@@ -514,10 +574,11 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
   for (int f = 0; f < nflag; ++f) {
     const int t = sh_flag[f];
     const int64_t tt = t0 + t;
-    fp64_row(hidden + tt * (int64_t)d, residual, gate, d, N, k, renorm,
-             reinterpret_cast<double*>(ring), sh_row64,
-             sh_sel64, topk_idx ? topk_idx + tt * k : nullptr, topk_w ? topk_w + tt * k : nullptr,
-             sh_hist);
+    double* ring64 = reinterpret_cast<double*>(ring);          // [d] x row, then partials
+    fp64_row_cand(hidden + tt * (int64_t)d, residual, gate, d, N, k, renorm, sh_cmask[f],
+                  sh_logit + t * g.NP, ring64, ring64 + d, sh_row64, sh_cl, &sh_nc,
+                  topk_idx ? topk_idx + tt * k : nullptr, topk_w ? topk_w + tt * k : nullptr,
+                  sh_hist);
   }
   RG_MARK(8);
   if (tid == 0) {
@@ -576,7 +637,7 @@ static int launch_tb(const uint16_t* hidden, const double* residual, const uint1
   const size_t sm = smem_bytes(g);
   DALI_ONCE_PER_DEVICE(cudaFuncSetAttribute(route_guard_kernel<TB, C>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            200 * 1024));
+                                            180 * 1024));
   // summation height: one block of DC/S terms per chunk, one flush per chunk,
   // slice tree, cluster sum, and one for a rounded (residual-shifted) input
   const int nch = (g.ds + g.DC - 1) / g.DC;
@@ -620,7 +681,8 @@ int launch_route_guarded(const uint16_t* hidden, const double* residual, const u
                          int* launched) {
   using namespace rg;
   *launched = 0;
-  if (wn2 == nullptr || N < 4 || N > 256 || (N & 3) || (d & 7) || k > DALI_MAX_TOPK || k > N || T <= 0)
+  // d <= 8000: the fp64 recompute stages one row (d doubles) in the 72 KB ring
+  if (wn2 == nullptr || d > 8000 || N < 4 || N > 256 || (N & 3) || (d & 7) || k > DALI_MAX_TOPK || k > N || T <= 0)
     return DALI_OK;
   cudaStream_t st = as_stream(stream);
   auto* wl = reinterpret_cast<unsigned long long*>(workloads);
@@ -640,7 +702,7 @@ int launch_route_guarded(const uint16_t* hidden, const double* residual, const u
 #undef DALI_RG_SMALL
   } else {
     int TB = 4;
-    while (TB < 32 && (T + TB - 1) / TB > 148) TB <<= 1;
+    while (TB < 32 && (T + TB - 1) / TB > 2 * 148) TB <<= 1;   // up to 2 CTAs per SM
     const Geo g = make_geo(TB, N, 1, d);
     if (g.S < 1 || smem_bytes(g) > 180 * 1024 || (size_t)TB * g.NP > 4096) return DALI_OK;
     if (workloads && (T + TB - 1) / TB > 1) {

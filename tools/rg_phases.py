@@ -14,6 +14,8 @@ from paper_2602_03495_b200 import _lib  # noqa: E402
 from paper_2602_03495_b200.trace import gate_norm2, route_device  # noqa: E402
 
 lib = _lib.load()
+if os.environ.get("RG_FORCE_FP64") == "1":
+    lib.dali_route_guard_scale(-1.0)
 d, N, k = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (4096, 8, 2)))
 Ts = [int(x) for x in (sys.argv[4].split(",") if len(sys.argv) > 4 else ["1", "16", "512"])]
 g = (torch.randn(d, N, device="cuda") * 0.02).to(torch.bfloat16)
