@@ -318,14 +318,15 @@ def metric_name(args):
     return f"decode tokens/s, {args.model} shape, {mode} (prefill tokens/s + hit rate reported)"
 
 
-def config_dict(args, ws):
+def config_dict(args, ws, resident=None):
     return {"workload": f"{args.model} random-init, prefill {args.prefill} + decode {args.decode} "
                         f"per request, B={args.batch}, expert cache {args.cache_gb} GB HBM, "
                         f"prefetch {args.prefetch}, w_size 4",
             "global_batch": args.batch * ws, "prefill": args.prefill, "decode": args.decode,
             "cache_gb": args.cache_gb,
             "parallelism": (f"ep{ws}" if args.ep else f"replicas{ws}") +
-                           ("-resident" if args.resident else ""),
+                           ("-resident" if (args.resident if resident is None else resident)
+                            else ""),
             "l2": l2_note(args),
             "decode_inputs": "teacher-forced token ids from a seeded synthetic stream with "
                              "Zipf(1.1) unigram frequencies (argmax still computed and read "
@@ -498,7 +499,7 @@ def run_dali(args, ws, rank, local):
             "ms_per_step": round(ms_v / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, uniform random prompt ids)",
-            "config": config_dict(args, ws),
+            "config": config_dict(args, ws, resident=eng.resident_mode),
             "prefill_tokens_per_s": round(pre_v, 3),
             "per_sequence_decode_tokens_per_s": round(dec_v / (args.batch * ws), 4),
             "cache_hit_rate": hit,

@@ -60,6 +60,11 @@ class StepInput:
     workloads: np.ndarray        # (L, N) int64
     hidden: np.ndarray | None    # (L, T, d) gate inputs, needed for prefetch
     eos: bool
+    # (L-1, N) next-layer predicted workloads supplied by the caller instead of
+    # the residual predictor over ``hidden`` -- the expert-parallel shard
+    # semantics: the owner's slice of the prediction summed over every rank's
+    # tokens (repo engine/ep.py), not a reference feature
+    predicted: np.ndarray | None = None
 
 
 @dataclass
@@ -205,7 +210,11 @@ def run(steps, gates, cfg: DriverConfig, L: int, N: int, k: int):
             demand_end = demand[-1][1] if demand else 0.0
             rec.demand_end = demand_end
             if prefetch_on and l < L - 1:
-                if cfg.prefetch_kind in ("residual", "feature"):
+                if st.predicted is not None:
+                    predicted = np.asarray(st.predicted[l], np.int64).copy()
+                    pset = P.stable_topk(predicted.astype(np.float64),
+                                         min(cfg.prefetch_size, N))
+                elif cfg.prefetch_kind in ("residual", "feature"):
                     res = (cfg.residuals[l] if cfg.residuals is not None
                            and cfg.prefetch_kind == "residual" else None)
                     predicted, pset = P.predict_next(st.hidden[l], res, gates[l + 1],

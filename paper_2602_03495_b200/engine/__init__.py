@@ -47,6 +47,19 @@ def build_engine(name: str, cfg: EngineConfig, seed: int = 0, cost_model=None,
     from .profiler import profile_cost_model
     arch = preset(name)
     experts = ep.local_experts if ep is not None else None
+    if ep is not None and not resident and weights is None and cfg.cache_gb is not None:
+        # EP: the shard stays in HBM whenever the per-GPU expert budget covers
+        # it -- aggregate HBM is the point of expert parallelism (Mixtral-8x7B
+        # at G >= 4 under 24 GB, Mixtral-8x22B at G = 8 under 34 GB).  A shard
+        # the budget does not cover is cached like the 1-GPU engine, with
+        # capacity min(budget blocks / L, NL - 1) slots per layer (the
+        # reference's 0 < capacity < N rule, cache.py:75-78).
+        shard = arch.num_layers * len(experts) * arch.expert_bytes
+        if shard <= cfg.cache_gb * 1e9:
+            resident = True
+            if log is not None:
+                log(f"EP shard of {len(experts)} experts x {arch.num_layers} layers "
+                    f"({shard / 1e9:.1f} GB) fits the {cfg.cache_gb} GB budget: resident")
     w = weights if weights is not None else ModelWeights(arch, seed=seed, resident=resident,
                                                          experts=experts)
     if cost_model is None:

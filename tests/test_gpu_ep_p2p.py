@@ -1,10 +1,20 @@
 """Peer-memory expert-parallel exchange (csrc/ep.cu) across two processes.
 
-This pool gives one GPU per call, so both ranks share cuda:0: the CUDA IPC
-mappings, system-scope arrival counters, dispatch / regroup / return /
-gather-back kernels run exactly as between two GPUs on an NVSwitch node
-(gloo only bootstraps the IPC handles).  Each owner applies a per-expert
-scale as its "FFN", so every returned row checks routing and placement."""
+Every test runs twice: both ranks on cuda:0 (the CUDA IPC mappings,
+system-scope arrival counters, dispatch / regroup / return / gather-back
+kernels run exactly as between two GPUs on an NVSwitch node; this pool gives
+one GPU per call), and ranks on cuda:0 / cuda:1 -- the cross-device NVLink
+path, skipped when fewer than 2 devices are visible.  gloo only bootstraps
+the IPC handles.  Each owner applies a per-expert scale as its "FFN", so
+every returned row checks routing and placement.
+
+EP decision semantics (a deliberate change from the single-GPU engine, which
+the reference's single-GPU simulator never defines: SPEC.md:8 puts multi-GPU
+out of scope): each owner runs the DALI policy over ITS expert shard, with
+the shard's GLOBAL workloads (every rank's tokens) and the shard's slice of
+the next-layer prediction summed over every rank's tokens, on its own CPU
+lane and cache.  ``test_ep_engine_two_ranks`` replays each owner's decision
+log through the oracle driver under exactly those inputs."""
 
 import os
 import socket
@@ -17,19 +27,29 @@ pytestmark = pytest.mark.gpu
 
 G, N, K, D, T = 2, 8, 2, 256, 37
 
+DEVICES = [pytest.param((0, 0), id="one-gpu"), pytest.param((0, 1), id="two-gpus")]
 
-def _worker(rank, port, out_q):
+
+def _need(devs):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    if max(devs) >= torch.cuda.device_count():
+        pytest.skip(f"needs {max(devs) + 1} CUDA devices")
+
+
+def _worker(rank, port, out_q, devs=(0, 0)):
     import torch.distributed as dist
 
     from paper_2602_03495_b200 import _lib
     from paper_2602_03495_b200.engine.ep import EPGroup, PeerExchange
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(devs[rank])
+    dev = torch.device("cuda", devs[rank])
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=G)
     try:
         ep = EPGroup(N)
         NL = ep.NL
-        ex = PeerExchange(ep, T * K, D, torch.device("cuda", 0))
+        ex = PeerExchange(ep, T * K, D, dev)
         sp = torch.cuda.current_stream().cuda_stream
         ok = True
         for epoch_seed in range(3):                  # three layers: flags are monotonic
@@ -101,9 +121,9 @@ def _worker(rank, port, out_q):
         dist.destroy_process_group()
 
 
-def test_peer_exchange_two_processes_one_gpu():
-    if not torch.cuda.is_available():
-        pytest.skip("needs a CUDA device")
+@pytest.mark.parametrize("devs", DEVICES)
+def test_peer_exchange_two_processes(devs):
+    _need(devs)
     import torch.multiprocessing as mp
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -111,7 +131,7 @@ def test_peer_exchange_two_processes_one_gpu():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(G)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, devs)) for r in range(G)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(G))
@@ -120,31 +140,34 @@ def test_peer_exchange_two_processes_one_gpu():
     assert res == {0: True, 1: True}, res
 
 
-def _engine_worker(rank, port, out_q):
+def _engine_worker(rank, port, out_q, devs=(0, 0), resident=False, name="tiny"):
     import torch.distributed as dist
 
+    from oracle import driver as D
+    from oracle import policy as P
     from paper_2602_03495_b200.cost_model import default_cost_model
     from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
     from paper_2602_03495_b200.engine.ep import EPGroup
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(devs[rank])
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=G)
     try:
-        arch = preset("tiny")
+        arch = preset(name)
         cm = default_cost_model(non_moe_layer_time=3.0)
         res = np.random.default_rng(0).standard_normal((arch.num_layers - 1,
                                                         arch.hidden_dim)) * 0.05
-        cfg = dict(cache_slots_per_layer=1, prefetch_size=1, capture=True, seed=3)
+        cfg = (dict(capture=True, seed=3) if resident else
+               dict(cache_slots_per_layer=1, prefetch_size=1, capture=True, seed=3))
         ep = EPGroup(arch.num_experts)
-        w_sh = ModelWeights(arch, seed=9, experts=ep.local_experts)
+        w_sh = ModelWeights(arch, seed=9, experts=ep.local_experts, resident=resident)
         eng = OffloadEngine(arch, w_sh, cm, EngineConfig(**cfg), residuals=res, max_seq=64,
                             ep=ep)
         g = torch.Generator().manual_seed(40 + rank)
         prompt = torch.randint(0, arch.vocab_size, (1, 10), generator=g)
         toks, st = eng.generate(prompt, 6)
         # reference: the single-process engine on this rank's prompt
-        base = OffloadEngine(arch, ModelWeights(arch, seed=9), cm, EngineConfig(**cfg),
-                             residuals=res, max_seq=64)
+        base = OffloadEngine(arch, ModelWeights(arch, seed=9, resident=resident), cm,
+                             EngineConfig(**cfg), residuals=res, max_seq=64)
         tb, sb = base.generate(prompt, 6)
         ok = True
         for la, lb in zip(st.logits, sb.logits):
@@ -160,6 +183,44 @@ def _engine_worker(rank, port, out_q):
                 np.add.at(hist, both[r][key].reshape(-1), 1)
             ok &= bool(np.array_equal(wl, hist[rank * NL:(rank + 1) * NL]))
         ok &= st.cpu_expert_calls + st.gpu_expert_calls > 0
+        if resident:                     # every shard expert on the GPU, no policy state
+            ok &= st.cpu_expert_calls == 0 and eng.resident_mode
+            dist.barrier()
+            ep.peer.close()
+            out_q.put((rank, ok))
+            return
+        # shard semantics, replayed by the oracle driver: N = NL experts, the
+        # shard's global workloads, the shard's slice of the next-layer
+        # prediction summed over both ranks' captured gate inputs
+        L = arch.num_layers
+        hmine = {(s_, l): h.double().numpy() for (s_, l, h) in st.captured}
+        hall = [None] * G
+        dist.all_gather_object(hall, hmine)
+        gates = np.stack([eng.w.router[l].double().cpu().numpy() for l in range(L)])
+        steps = []
+        for s_, (ti, ntok, eos) in enumerate(st.steps_meta):
+            wl = np.stack([st.workloads[(s_, l)] for l in range(L)])
+            pred = np.zeros((L, NL), np.int64)
+            for l in range(L - 1):
+                tot = np.zeros(arch.num_experts, np.int64)
+                for r in range(G):
+                    tot += P.derive_workloads(hall[r][(s_, l)] + res[l], gates[l + 1],
+                                              arch.top_k)
+                pred[l] = tot[rank * NL:(rank + 1) * NL]
+            steps.append(D.StepInput(ti, ntok, wl, None, eos, predicted=pred))
+        dcfg = D.DriverConfig(tables=P.default_tables(non_moe_layer_time=3.0), prefetch_size=1,
+                              cache_capacity=eng.slots_per_layer, w_size=eng.cfg.w_size,
+                              u_size=eng.cfg.u_size, seed=3, initial_on_gpu=st.initial_on_gpu)
+        _, recs = D.run(steps, gates, dcfg, L, NL, arch.top_k)
+        got = eng.policy.decision_log()
+        ok &= len(got) == len(recs)
+        for g_, o in zip(got, recs):
+            ok &= bool(np.array_equal(g_["C"], o.C) and np.array_equal(g_["G"], o.G))
+            ok &= bool(np.array_equal(g_["resident"], o.resident))
+            ok &= g_["hits"] == o.lookups and g_["event"] == o.event
+            ok &= g_["latency"] == o.latency
+            if o.prefetch_set is not None:
+                ok &= g_["pset"] == o.prefetch_set.tolist() and g_["done"] == o.completed
         dist.barrier()
         ep.peer.close()
         out_q.put((rank, ok))
@@ -170,12 +231,17 @@ def _engine_worker(rank, port, out_q):
         dist.destroy_process_group()
 
 
-def test_ep_engine_two_ranks_one_gpu():
-    """The EP engine at world 2 over the peer-memory transport (both ranks on
-    the pool's one GPU): each rank's logits match the single-process engine
-    on its own prompt, and every owner decides on the global workloads."""
-    if not torch.cuda.is_available():
-        pytest.skip("needs a CUDA device")
+@pytest.mark.parametrize("name,resident", [("tiny", False), ("tiny", True),
+                                           ("mixtral-8x22b@L2", True)],
+                         ids=["tiny-cached-shard", "tiny-resident-shard",
+                              "mixtral-8x22b-2layer-resident-shard"])
+@pytest.mark.parametrize("devs", DEVICES)
+def test_ep_engine_two_ranks(devs, resident, name):
+    """The EP engine at world 2 over the peer-memory transport: each rank's
+    logits match the single-process engine on its own prompt, every owner
+    decides on the global workloads, and each owner's decision log equals
+    the oracle driver replaying the shard semantics (module docstring)."""
+    _need(devs)
     import torch.multiprocessing as mp
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -183,7 +249,8 @@ def test_ep_engine_two_ranks_one_gpu():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_engine_worker, args=(r, port, q)) for r in range(G)]
+    procs = [ctx.Process(target=_engine_worker, args=(r, port, q, devs, resident, name))
+             for r in range(G)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(G))
