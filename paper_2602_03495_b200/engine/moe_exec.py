@@ -498,6 +498,8 @@ class MoEExecMixin:
                   cpu_rows.data_ptr() if cpu_rows is not None else None,
                   y_shared.data_ptr() if y_shared is not None else None, T, k, d, splits,
                   R, out.data_ptr(), cs.cuda_stream)
+        if self.cfg.capture_moe_io:
+            self._capture_io(step, l, x, out)
         if tr:
             ev_c = torch.cuda.Event(enable_timing=True)
             ev_c.record(cs)
@@ -509,6 +511,15 @@ class MoEExecMixin:
                 ev_rows=self._ev_rows if cpu_rows is not None else None,
                 ev=(ev_r if ev_r is not None else ev_dec, ev_dec, le["t0"], ev_c)))
         return out
+
+    def _capture_io(self, step: int, l: int, x: torch.Tensor, out: torch.Tensor) -> None:
+        """Stream-ordered host copies of one MoE layer's residual input and
+        output (read by the tests after the request synchronises)."""
+        xi = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        xo = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        xi.copy_(x, non_blocking=True)
+        xo.copy_(out, non_blocking=True)
+        self.stats.moe_io.append((step, l, xi, xo))
 
     def _moe_resident(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int,
                       token_index: int, is_eos: bool) -> torch.Tensor:
@@ -565,6 +576,8 @@ class MoEExecMixin:
                   v["pos"].data_ptr(), v["wts"].data_ptr(), None, None,
                   y_shared.data_ptr() if y_shared is not None else None, T, k, d, splits, R,
                   out.data_ptr(), cs.cuda_stream)
+        if self.cfg.capture_moe_io and not self._in_capture:
+            self._capture_io(step, l, x, out)
         if self.cfg.capture:
             hh = torch.empty((T, d), dtype=torch.bfloat16, pin_memory=True)
             hh.copy_(h, non_blocking=True)

@@ -70,6 +70,8 @@ class EngineConfig:
     cpu_threads: int | None = None
     staging_slots: int | None = None
     capture: bool = False                   # keep gate inputs for oracle replay
+    capture_moe_io: bool = False            # also keep every MoE layer's residual input and
+    #                                         output (per-layer numeric parity tests)
     max_records: int = 16384
     time_ffn: bool = False                  # CUDA events around every expert-FFN launch
     ffn_kernel: str = "tc"                  # "tc" (tcgen05 + TMA) | "simt" (weight streaming)
@@ -98,6 +100,7 @@ class RunStats:
     dali_launches: int = 0
     initial_on_gpu: np.ndarray | None = None
     captured: list = field(default_factory=list)    # (step, layer, h (T,d) bf16 cpu)
+    moe_io: list = field(default_factory=list)      # (step, layer, x_in, out) bf16 cpu pinned
     workloads: dict = field(default_factory=dict)   # (step, layer) -> realised workloads
     topk: dict = field(default_factory=dict)        # (step, layer) -> (T, k) experts (capture)
     logits: list = field(default_factory=list)      # per step (B, V) fp32 (capture)
