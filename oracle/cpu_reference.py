@@ -7,10 +7,11 @@ baseline with no GPU: gating by the reference algorithm
 trace.py:229-265) and every routed expert executed on the CPU, plus the
 same attention.  torch CPU (oneDNN, AMX-bf16) with all host threads.
 
-Bounded sample: ``layers`` of the model's L layers are materialised and
-timed, and times are scaled by L / layers (the layers are identical in
-shape and cost), so a 32-layer Mixtral-8x7B number needs only
-layers x 8 experts of host memory and finishes in seconds.
+Two bounds: ``run_full_depth`` (the ``--impl reference`` arm) materialises
+every layer and times consecutive decode tokens through all of them, with
+no scaling; ``run_sample`` (the GPU arm's in-process ``cpu_baseline``, where
+the engine's own 91 GB host store already occupies host memory) times
+``layers`` of the model's L layers and scales by L / layers.
 """
 
 from __future__ import annotations
@@ -126,6 +127,67 @@ def run_sample(arch_dims: dict, total_layers: int, prefill: int, decode_steps: i
             "sample": f"{sample_layers} of {total_layers} layers (time x{total_layers}/"
                       f"{sample_layers}), prefill {prefill} x B{batch}, {decode_steps} decode "
                       f"steps, all experts on CPU, fp64 reference gating"}
+
+
+def run_full_depth(arch_dims: dict, total_layers: int, prefill: int, decode: int, steps: int,
+                   warmup: int, batch: int = 1, chunk: int = 8, threads=None, seed: int = 0,
+                   log=None):
+    """The reference arm at FULL depth: every one of the model's layers is
+    materialised (Mixtral-8x7B: 90 GB of host weights) and run; nothing is
+    scaled.  One request = a ``prefill``-token prompt, then ``decode`` - 1
+    decode tokens (the first generated token comes from the prefill).  One
+    bench step = the next ``chunk`` decode tokens of the current request; a
+    request that reaches its last decode position is restarted with a new
+    prompt (that prefill is timed into ``prefill_tokens_per_s``).  So K steps
+    time K x chunk consecutive decode tokens across every decode position,
+    each through all layers, and every expert on the host cores."""
+    threads = threads or len(os.sched_getaffinity(0))
+    torch.set_num_threads(threads)
+    t_init = time.perf_counter()
+    m = CpuMoE(layers=total_layers, seed=seed, max_seq=prefill + decode + 1, **arch_dims)
+    t_init = time.perf_counter() - t_init
+    g = torch.Generator().manual_seed(seed)
+    d = arch_dims["d"]
+    pre = []
+
+    def new_request():
+        m.reset(batch)
+        x = torch.randn(batch * prefill, d, generator=g).to(torch.bfloat16)
+        t0 = time.perf_counter()
+        m.step(x, batch, prefill)
+        pre.append(time.perf_counter() - t0)
+        if log:
+            log(f"reference arm: prefill {batch * prefill / pre[-1]:.1f} tok/s")
+
+    new_request()
+    left = max(decode - 1, 1)
+    dec_tokens, dec_time, per_step = 0, 0.0, []
+    for i in range(warmup + steps):
+        n = min(chunk, left)
+        t0 = time.perf_counter()
+        for _ in range(n):
+            x = torch.randn(batch, d, generator=g).to(torch.bfloat16)
+            m.step(x, batch, 1)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            dec_tokens += batch * n
+            dec_time += dt
+            per_step.append(dt)
+        if log:
+            log(f"reference arm step {i}: {batch * n / dt:.2f} decode tok/s")
+        left -= n
+        if left <= 0:
+            new_request()
+            left = max(decode - 1, 1)
+    return {"prefill_tokens_per_s": batch * prefill / float(np.mean(pre)),
+            "decode_tokens_per_s": dec_tokens / dec_time,
+            "step_seconds": per_step, "threads": threads, "init_s": round(t_init, 1),
+            "sample": f"all {total_layers} layers (no scaling); each step = the next {chunk} "
+                      f"decode tokens of a prefill {prefill} + decode {decode} request "
+                      f"(B{batch}), requests restarted at their last position, so {steps} "
+                      f"timed steps cover {dec_tokens} consecutive decode positions; "
+                      f"{len(pre)} full-depth prefills timed; all experts on the CPU "
+                      f"(torch oneDNN bf16), fp64 reference gating"}
 
 
 def policy_layer_timing(d: int, N: int, k: int, capacity: int, prefetch_size: int,

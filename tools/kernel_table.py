@@ -69,8 +69,17 @@ def _bn(mr):
     return 16 if mr <= 16 else 32 if mr <= 32 else 64 if mr <= 64 else 128 if mr <= 128 else 256
 
 
-def cases(which=("mixtral", "dsv2"), Ts=(1, 512, 4096), ffn=True, small=True):
-    """Build the case list (allocates device buffers; call on cuda)."""
+def shape_of(arch) -> dict:
+    """SHAPES entry of an engine MoEArch (bench.py's live table)."""
+    return dict(d=arch.hidden_dim, f=arch.ffn_dim, N=arch.num_experts, k=arch.top_k,
+                qkv=(arch.num_heads + 2 * arch.num_kv_heads) * arch.head_dim,
+                renorm=bool(arch.norm_topk_prob))
+
+
+def cases(which=("mixtral", "dsv2"), Ts=(1, 512, 4096), ffn=True, small=True, shapes=None):
+    """Build the case list (allocates device buffers; call on cuda).
+    ``shapes`` maps a label to a SHAPES-style dict (default: SHAPES)."""
+    shapes = shapes or SHAPES
     from paper_2602_03495_b200.engine.moe_exec import ffn_splits
     from paper_2602_03495_b200.trace import gate_norm2
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -82,7 +91,7 @@ def cases(which=("mixtral", "dsv2"), Ts=(1, 512, 4096), ffn=True, small=True):
         return (torch.randn(*shape, device=dev, generator=g) * 0.5).to(torch.bfloat16)
 
     for m in which:
-        s = SHAPES[m]
+        s = shapes[m]
         d, f, N, k = s["d"], s["f"], s["N"], s["k"]
         gate = (randn_bf16(d, N) * 0.04).contiguous()
         n2 = gate_norm2(gate)
@@ -96,7 +105,7 @@ def cases(which=("mixtral", "dsv2"), Ts=(1, 512, 4096), ffn=True, small=True):
             st = {"i": 0}
 
             def route(hs=hs, idx=idx, wts=wts, wl=wl, gate=gate, n2=n2, T=T, d=d, N=N, k=k,
-                      st=st, renorm=int(m == "mixtral")):
+                      st=st, renorm=int(s.get("renorm", m == "mixtral"))):
                 h = hs[st["i"] % len(hs)]
                 st["i"] += 1
                 _lib.call("dali_route_bf16", h.data_ptr(), None, gate.data_ptr(), n2.data_ptr(),
@@ -137,6 +146,8 @@ def cases(which=("mixtral", "dsv2"), Ts=(1, 512, 4096), ffn=True, small=True):
             # grouped SwiGLU FFN over the routed rows, every expert on the GPU
             cnt = torch.bincount(idx.view(-1).long(), minlength=N).cpu().numpy()
             mr = int(cnt.max())
+            print(f"# {m} T={T} rows per expert: {','.join(str(int(c)) for c in cnt)}",
+                  file=sys.stderr)
             bn = _bn(mr)
             tiles = int(sum((c + bn - 1) // bn for c in cnt if c)) * (d // 128)
             sp = ffn_splits(mr, tiles, f // 64, nsm)
@@ -161,8 +172,10 @@ def cases(which=("mixtral", "dsv2"), Ts=(1, 512, 4096), ffn=True, small=True):
                 hbuf = torch.empty((R, f), dtype=torch.bfloat16, device=dev)
                 yp = torch.empty((sp, R, d), dtype=torch.float32, device=dev)
 
+                # blocks=blocks keeps the weight memory alive: the tensor maps
+                # only hold raw addresses
                 def ffn_launch(maps=maps, xp=xp, offs=offs, N=N, d=d, f=f, R=R, mr=mr, n_on=n_on,
-                               hbuf=hbuf, yp=yp, sp=sp, st={"i": 0}):
+                               hbuf=hbuf, yp=yp, sp=sp, st={"i": 0}, blocks=blocks):
                     mt = maps[st["i"] % len(maps)][1]
                     st["i"] += 1
                     _lib.call("dali_expert_ffn_tc", xp.data_ptr(), offs.data_ptr(), N,
@@ -235,7 +248,7 @@ def _small_cases(m, s, dev):
                       torch.cuda.current_stream().cuda_stream)
         res.append(Case("copy_mapped (kernel copy over UVA-mapped pinned host memory)",
                         f"{m} {what} {nbytes} B", nbytes, cp, 1, bound="pcie-latency"))
-    if m == "mixtral":
+    if s.get("gemv", m == "mixtral"):
         for M, K, what in ((s["qkv"], d, "qkv"), (d, d, "o")):
             nb = _copies(M * K * 2)
             ws = [(torch.randn(M, K, device=dev) * 0.02).to(torch.bfloat16) for _ in range(nb)]

@@ -25,6 +25,9 @@ ap.add_argument("--d", type=int, default=4096)
 ap.add_argument("--f", type=int, default=14336)
 ap.add_argument("--splits", type=int, default=0, help="override the split-K planes")
 ap.add_argument("--counts", default=None, help="RxE: R tokens on each of E experts (e.g. 512x8)")
+ap.add_argument("--count-list", default=None, help="explicit per-expert rows, comma-separated")
+ap.add_argument("--graph", type=int, default=0,
+                help="also replay N back-to-back launches captured in one CUDA graph")
 args = ap.parse_args()
 d, f, N = args.d, args.f, 8
 dev = torch.device("cuda")
@@ -55,9 +58,10 @@ def run(counts, label):
     tiles = sum((c + bn - 1) // bn for c in counts if c) * (d // 128)
     splits = args.splits or ffn_splits(mr, tiles, f // 64, nsm)
     y = torch.empty(splits, rows, d, dtype=torch.float32, device=dev)
-    cs = torch.cuda.current_stream().cuda_stream
+    cs0 = torch.cuda.current_stream().cuda_stream  # noqa: F841
 
     def go():
+        cs = torch.cuda.current_stream().cuda_stream
         if args.kernel == "tc":
             _lib.call("dali_expert_ffn_tc", xp.data_ptr(), offs.data_ptr(), N, maps.data_ptr(), d,
                       f, rows, mr, sum(on), h.data_ptr(), y.data_ptr(), splits, cs)
@@ -76,6 +80,20 @@ def run(counts, label):
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
+    if args.graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(args.graph):
+                go()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        print(f"{label}: graph of {args.graph} launches: {e0.elapsed_time(e1) * 1e3 / args.graph:.1f}"
+              f" us per launch", flush=True)
     byts = sum(on) * 3 * f * d * 2 + rows * (d * 2 + 2 * f * 2 + d * 4 * splits)
     flops = 6.0 * rows * d * f
     print(f"{label}: {args.kernel} splits={splits} bn={bn} median {ms * 1e3:.1f} us, "
@@ -86,6 +104,8 @@ def run(counts, label):
 if args.counts:
     r_, e_ = (int(x) for x in args.counts.split("x"))
     run([r_] * e_ + [0] * (N - e_), f"counts {args.counts}")
+if args.count_list:
+    run([int(x) for x in args.count_list.split(",")], f"count list {args.count_list}")
 if args.mode == "one":
     run([1, 0, 0, 0, 0, 0, 0, 0], "decode 1x1")
 if args.mode in ("decode", "both"):
