@@ -460,6 +460,11 @@ int dali_ep_gather_back(const float* ret, const int32_t* offsets, int32_t N, int
  * SwiGLU intermediate is rounded to bf16 like the GPU kernel's. */
 int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f,
                     const uint16_t* x, int32_t R, float* y, int32_t nthreads);
+/* R > 16 rows (prefill) run on AMX-BF16 tiles when the host has them (1 if
+ * so; DALI_CPU_AMX=0 disables): fp32 accumulation and fp32 outputs, only the
+ * SwiGLU intermediate rounded to bf16 -- the GPU kernel's rounding points.
+ * Without AMX the rows are processed 16 at a time by the AVX-512 kernel. */
+int dali_cpu_expert_amx_available(void);
 
 /* Asynchronous form for the engine: experts i < n (block[i], rows x[i]
  * (rows[i] <= 16, d) bf16 -> y[i] (rows[i], d) f32, [host] pointers as

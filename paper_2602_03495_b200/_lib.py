@@ -107,6 +107,7 @@ SIGNATURES = {
     "dali_decode_attention": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, C.c_float, _P,
                               _P, _P],
     "dali_cpu_expert": [_P, _I32, _I32, _P, _I32, _P, _I32],
+    "dali_cpu_expert_amx_available": [],
     "dali_cpu_expert_submit": [_I32, _P, _P, _P, _P, _I32, _I32, _I32],
     "dali_cpu_expert_wait": [],
     "dali_add_rmsnorm": [_P, _P, _P, C.c_float, _I64, _I32, _P, _P, _P],

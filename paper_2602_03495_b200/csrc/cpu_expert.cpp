@@ -8,7 +8,10 @@
 // Threads: a persistent pool partitions weight rows; phase 1 (W13, SwiGLU
 // into a bf16 intermediate -- the same rounding point as the GPU kernel),
 // barrier, phase 2 (W2 -> fp32 outputs).
+#include <cpuid.h>
 #include <immintrin.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -198,7 +201,144 @@ bool dynamic_chunks() {
 
 bool async_job_busy();
 
+// ---------------------------------------------------------------------------
+// AMX-BF16 path for prefill-sized token batches (R > kMaxRows rows): the same
+// SwiGLU with fp32 accumulators and fp32 outputs, rounding only the SwiGLU
+// intermediate to bf16 -- the rounding points of the GPU tcgen05 kernel and
+// of the AVX-512 decode kernel above, so a prefill row's numerics no longer
+// depend on whether the policy placed its expert on the CPU or the GPU.
+// Weights are the A operand straight from the block (16 rows x 32 k per
+// tile, row stride d or f); tokens are the B operand, packed once per call
+// into the VNNI layout xp[k/2][Tpad][2].  2 A x 2 B -> 4 accumulator tiles
+// (gate/up rows x 32 tokens in phase 1, 32 W2 rows x 32 tokens in phase 2).
+// The SwiGLU intermediate is written straight into the VNNI layout the down
+// projection's B operand needs.  Work units (one per 32 weight rows) are
+// handed out by an atomic counter like the decode kernel's.
+// ---------------------------------------------------------------------------
+struct alignas(64) TileCfg {
+  uint8_t palette = 1, start_row = 0, reserved[14] = {};
+  uint16_t colsb[16] = {};
+  uint8_t rows[16] = {};
+};
+
+bool amx_ok() {
+  static const bool ok = [] {
+    const char* e = getenv("DALI_CPU_AMX");           // A/B switch: 0 = 16-row AVX passes
+    if (e && e[0] == '0') return false;
+    unsigned a, b, c, dx;
+    if (!__get_cpuid_count(7, 0, &a, &b, &c, &dx)) return false;
+    if (!((dx >> 22) & 1u) || !((dx >> 24) & 1u)) return false;     // AMX-BF16, AMX-TILE
+    // Linux: the tile data state must be requested once per process
+    return syscall(SYS_arch_prctl, 0x1023 /* ARCH_REQ_XCOMP_PERM */,
+                   18 /* XFEATURE_XTILEDATA */) == 0;
+  }();
+  return ok;
+}
+
+void tile_config() {
+  TileCfg c;
+  for (int i = 0; i < 8; ++i) {
+    c.colsb[i] = 64;
+    c.rows[i] = 16;
+  }
+  _tile_loadconfig(&c);
+}
+
+// C(0..3) = A(4|5) x B(6|7) over K (multiple of 32); a0/a1: weight rows
+// (stride lda elements), b: VNNI tokens at token t0 (row stride 2 * tpad).
+inline void amx_block(const uint16_t* a0, const uint16_t* a1, int64_t lda, const uint16_t* b,
+                      int64_t tpad, int K, float* c /* [4][16][16] */) {
+  _tile_zero(0);
+  _tile_zero(1);
+  _tile_zero(2);
+  _tile_zero(3);
+  for (int k = 0; k < K; k += 32) {
+    _tile_loadd(4, a0 + k, (int)(lda * 2));
+    _tile_loadd(5, a1 + k, (int)(lda * 2));
+    const uint16_t* bk = b + (int64_t)(k / 2) * tpad * 2;
+    _tile_loadd(6, bk, (int)(tpad * 4));
+    _tile_loadd(7, bk + 32, (int)(tpad * 4));
+    _tile_dpbf16ps(0, 4, 6);
+    _tile_dpbf16ps(1, 4, 7);
+    _tile_dpbf16ps(2, 5, 6);
+    _tile_dpbf16ps(3, 5, 7);
+  }
+  _tile_stored(0, c, 64);
+  _tile_stored(1, c + 256, 64);
+  _tile_stored(2, c + 512, 64);
+  _tile_stored(3, c + 768, 64);
+}
+
+void amx_expert(const uint16_t* block, int d, int f, const uint16_t* x, int R, float* y,
+                Pool* pool) {
+  const int64_t tpad = (R + 31) / 32 * 32;
+  const uint16_t* w13 = block;
+  const uint16_t* w2 = block + (int64_t)2 * f * d;
+  std::vector<uint16_t> xp((size_t)d * tpad), hp((size_t)f * tpad);
+  // phase 0: pack tokens to VNNI (k-pair major), zero padding tokens
+  std::atomic<int> next{0};
+  constexpr int kPackK = 64;
+  pool->run([&](int) {
+    for (int c = next.fetch_add(1); c * kPackK < d; c = next.fetch_add(1)) {
+      const int k0 = c * kPackK, k1 = std::min(d, k0 + kPackK);
+      for (int k = k0; k < k1; k += 2) {
+        uint32_t* row = reinterpret_cast<uint32_t*>(xp.data() + (int64_t)(k / 2) * tpad * 2);
+        for (int t = 0; t < R; ++t)
+          row[t] = *reinterpret_cast<const uint32_t*>(x + (int64_t)t * d + k);
+        for (int64_t t = R; t < tpad; ++t) row[t] = 0;
+      }
+    }
+  });
+  // phase 1: gate/up (rows 128b + 16i and 128b + 64 + 16i) -> SwiGLU -> hp
+  const int units1 = (f / 64) * 4;
+  next.store(0);
+  pool->run([&](int) {
+    tile_config();
+    alignas(64) float c[4 * 256];
+    for (int u = next.fetch_add(1); u < units1; u = next.fetch_add(1)) {
+      const int b = u / 4, i = u % 4;
+      const uint16_t* gr = w13 + (int64_t)(128 * b + 16 * i) * d;
+      const uint16_t* ur = w13 + (int64_t)(128 * b + 64 + 16 * i) * d;
+      for (int64_t t0 = 0; t0 < tpad; t0 += 32) {
+        amx_block(gr, ur, d, xp.data() + t0 * 2, tpad, d, c);
+        for (int r = 0; r < 16; ++r) {
+          const int col = 64 * b + 16 * i + r;
+          uint16_t* hrow = hp.data() + (int64_t)(col / 2) * tpad * 2 + (col & 1);
+          for (int j = 0; j < 32; ++j) {
+            const float g = c[(j < 16 ? 0 : 256) + r * 16 + (j & 15)];
+            const float v = c[(j < 16 ? 512 : 768) + r * 16 + (j & 15)];
+            hrow[(t0 + j) * 2] = f2bf(g / (1.0f + std::exp(-g)) * v);
+          }
+        }
+      }
+    }
+  });
+  // phase 2: y[t, m] = h_t . W2_m, 32 W2 rows per unit, fp32 out
+  const int units2 = d / 32;
+  next.store(0);
+  pool->run([&](int) {
+    tile_config();
+    alignas(64) float c[4 * 256];
+    for (int u = next.fetch_add(1); u < units2; u = next.fetch_add(1)) {
+      const int m0 = 32 * u;
+      for (int64_t t0 = 0; t0 < tpad; t0 += 32) {
+        amx_block(w2 + (int64_t)m0 * f, w2 + (int64_t)(m0 + 16) * f, f, hp.data() + t0 * 2,
+                  tpad, f, c);
+        for (int j = 0; j < 32 && t0 + j < R; ++j) {
+          float* yr = y + (t0 + j) * (int64_t)d + m0;
+          for (int r = 0; r < 16; ++r) {
+            yr[r] = c[(j < 16 ? 0 : 256) + r * 16 + (j & 15)];
+            yr[16 + r] = c[(j < 16 ? 512 : 768) + r * 16 + (j & 15)];
+          }
+        }
+      }
+    }
+  });
+}
+
 }  // namespace
+
+extern "C" int dali_cpu_expert_amx_available(void) { return amx_ok() ? 1 : 0; }
 
 extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, const uint16_t* x,
                                int32_t R, float* y, int32_t nthreads) {
@@ -206,6 +346,10 @@ extern "C" int dali_cpu_expert(const uint16_t* block, int32_t d, int32_t f, cons
   if (R == 0) return DALI_OK;
   if (!cpu_ok()) return DALI_ESIM;
   if (async_job_busy()) return DALI_ESIM;           // the pool is running a submitted job
+  if (R > kMaxRows && amx_ok()) {
+    amx_expert(block, d, f, x, R, y, pool_for(nthreads < 1 ? 1 : nthreads));
+    return DALI_OK;
+  }
   if (R > kMaxRows) {
     for (int r0 = 0; r0 < R; r0 += kMaxRows) {
       const int n = R - r0 < kMaxRows ? R - r0 : kMaxRows;

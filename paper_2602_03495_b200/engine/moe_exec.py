@@ -318,9 +318,9 @@ class MoEExecMixin:
         """Start the CPU-assigned experts on the host worker: decode-sized
         experts (<= NATIVE_MAX_ROWS rows) go to the native pool asynchronously
         (``dali_cpu_expert_submit``) so the caller dispatches the GPU side of
-        the layer meanwhile; prefill-sized ones are returned for the oneDNN
-        path.  Returns the job description for ``_cpu_finish``.  This sits on
-        the decode critical path between the decision and the first CPU byte,
+        the layer meanwhile; prefill-sized ones are returned for the
+        synchronous AMX path.  Returns the job description for
+        ``_cpu_finish``.  This sits on the decode critical path between the decision and the first CPU byte,
         so the submission arrays are preallocated and filled in place."""
         C = np.frombuffer(rec.C, dtype=np.int8, count=self.NL)
         if R == 0 or not C.any():
@@ -373,7 +373,7 @@ class MoEExecMixin:
         d, f = a.hidden_dim, a.ffn_dim
         out = job["out"]
         if job["native"]:
-            _lib.call("dali_cpu_expert_wait")       # join the pool before oneDNN's threads run
+            _lib.call("dali_cpu_expert_wait")       # join the pool before the AMX experts use it
         for e, r0, r1 in job["big"]:
             t0 = time.perf_counter()
             cpu_expert_rows(self._host_block(job["l"], e).view(torch.bfloat16),

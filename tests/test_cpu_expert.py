@@ -65,3 +65,29 @@ def test_cpu_expert_submit_wait_matches_sync(late_ms):
         for r, y, ref in zip(rows, ys, refs):
             if r:
                 assert torch.equal(y[:r], ref[:r])
+
+
+@pytest.mark.skipif(not _has_bf16(), reason="host CPU lacks AVX512-BF16")
+@pytest.mark.parametrize("d,f,R", [(256, 512, 17), (512, 1408, 40), (1024, 2048, 130),
+                                   (4096, 1408, 64)])
+def test_cpu_expert_prefill_rows_keep_fp32_outputs(d, f, R):
+    """Prefill-sized batches (R > 16, the AMX-BF16 path when the host has it)
+    have the decode kernel's rounding points: fp32 gate/up and down outputs,
+    only the SwiGLU intermediate rounded to bf16 (the oneDNN path
+    rounded all three).  Each row must equal the single-row AVX-512 result up
+    to fp32 summation order and rare 1-ulp flips of the bf16 intermediate --
+    far below one bf16 rounding of the output (2^-9 relative)."""
+    g = torch.Generator().manual_seed(7 * d + R)
+    block = (torch.randn(3 * f * d, generator=g) * 0.05).to(torch.bfloat16)
+    x = torch.randn(R, d, generator=g).to(torch.bfloat16)
+    y = torch.empty(R, d, dtype=torch.float32)
+    _lib.call("dali_cpu_expert", block.data_ptr(), d, f, x.data_ptr(), R, y.data_ptr(), 4)
+    ref = torch.empty(R, d, dtype=torch.float32)
+    for r in range(R):
+        _lib.call("dali_cpu_expert", block.data_ptr(), d, f, x[r:r + 1].data_ptr(), 1,
+                  ref[r:r + 1].data_ptr(), 4)
+    err = (y - ref).abs()
+    scale = ref.pow(2).mean(dim=1, keepdim=True).sqrt()
+    assert float((err / scale).max()) < 2e-3, float((err / scale).max())
+    # and the outputs are not bf16-rounded: most values carry more mantissa bits
+    assert float((y != y.to(torch.bfloat16).float()).float().mean()) > 0.9

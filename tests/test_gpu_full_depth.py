@@ -17,8 +17,7 @@ accumulate.  The reference computation is torch fp32 (TF32 off) on the
 engine's bf16 weights.  Bar, per element: |out - ref| <= 2e-2 |ref| + atol,
 atol = 2 bf16 ulps of |x| + |y| (the output is a bf16 residual stream) +
 2^-6 of the row's RMS expert output.  The bf16-rounded SwiGLU intermediate
-(and, for prefill-sized CPU experts, oneDNN's bf16 outputs) perturbs every
-output element by a near-Gaussian error of standard deviation ~2^-9 of the
+perturbs every output element by a near-Gaussian error of standard deviation ~2^-9 of the
 row's scale, which dominates where x + y cancels; measured on Mixtral
 (18.9M elements) the worst element sits at ~5.5 sigma, so the floor is 8
 sigma.
