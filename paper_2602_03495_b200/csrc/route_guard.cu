@@ -24,15 +24,24 @@
 // computes H from the launch geometry; a 1% factor covers the fp32 error of
 // the norms themselves.
 //
-// Two launch shapes (one kernel template):
+// Two launch shapes:
 //  * T <= 16 (decode): one thread-block cluster of C CTAs splits d; partial
 //    logits and norms go to the leader CTA through distributed shared memory
 //    and the leader ranks, writes the histogram directly (no zeroing launch).
+//    The router slices (which do not depend on the previous kernel) are
+//    requested before the PDL wait, so they stream while the predecessor
+//    drains; only the hidden rows wait.
 //  * T > 16 (prefill): one CTA per TB tokens over the whole of d.
 // Operands stream through a 3-stage cp.async ring (raw bf16); each stage is
 // converted once to fp32 in shared memory (residual added in fp64 there, as
 // numpy's `hidden + res`), then every thread accumulates a 4-token x
 // 8-expert register tile.
+// Ranking (rank_tail): at decode sizes (tokens x experts <= 2 x threads)
+// every (token, expert) pair is ranked at once by one thread counting the
+// experts that beat it (logit, then lower index); larger tiles pick the k+1
+// leaders by warp-wide argmax rounds, a warp per token.  Then a warp per
+// token certifies the k+1 leading gaps, finishes the softmax and writes.
+#include <algorithm>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -204,6 +213,190 @@ __device__ void fp64_row_cand(const uint16_t* __restrict__ hrow,
   __syncthreads();
 }
 
+// Shared tail of both launch shapes.  zl: [TB][NP] fp32 logits of this
+// CTA's tokens, xn: [TB] squared token norms, wn: [N] router column norms.
+// Counting ranks, then a warp per token certifies / softmaxes / writes; rows
+// that cannot be certified are recomputed in fp64 (fp64_row_cand).  ring64
+// is scratch for the recompute: >= (d + 1040) doubles, not aliasing zl.
+struct TailSmem {
+  int* hist;                          // [256] per-CTA expert histogram
+  int (*sel)[DALI_MAX_TOPK + 1];      // [TB] leading experts in rank order
+  int* flag;                          // [TB] rows sent to fp64
+  int* nflag;
+  uint32_t (*cmask)[8];               // [TB] candidate masks of those rows
+  int* bad;                           // [TB] non-finite logit seen
+  double* row64;                      // [256]
+  int* cl;                            // [256]
+  int* nc;
+};
+
+template <int TB>
+__device__ void rank_tail(const float* zl, int NP, const float* xn, const float* wn, int tb_n,
+                          int64_t t0, int N, int k, int renorm, float gamma, int force_fp64,
+                          const uint16_t* __restrict__ hidden, const double* __restrict__ residual,
+                          const uint16_t* __restrict__ gate, int d, int32_t* __restrict__ topk_idx,
+                          float* __restrict__ topk_w, double* ring64, const TailSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kk = (k < N) ? k : N - 1;          // last rank whose order must be certain
+  const bool counting = tb_n * N <= 2 * kThreads;
+  // (1) decode sizes: counting ranks, rank(j) = #{i : z_i > z_j or
+  //     (z_i == z_j and i < j)}; only ranks <= kk are kept
+  for (int p = tid; counting && p < tb_n * N; p += kThreads) {
+    const int t = p / N, j = p - t * N;
+    const float* z = zl + t * NP;
+    const float zj = z[j];
+    if (!(fabsf(zj) < 3.0e38f)) {
+      sm.bad[t] = 1;
+      continue;
+    }
+    // NP % 8 == 0, padded logits are never read past N: count in float4s
+    const float4* z4 = reinterpret_cast<const float4*>(z);
+    int r = 0;
+#pragma unroll 4
+    for (int i4 = 0; i4 < N / 4; ++i4) {
+      const float4 v = z4[i4];
+      const int i = 4 * i4;
+      r += (v.x > zj) || (v.x == zj && i < j);
+      r += (v.y > zj) || (v.y == zj && i + 1 < j);
+      r += (v.z > zj) || (v.z == zj && i + 2 < j);
+      r += (v.w > zj) || (v.w == zj && i + 3 < j);
+    }
+    if (r <= kk) sm.sel[t][r] = j;
+  }
+  // (1') larger tiles: k+1 warp-wide argmax rounds over (logit, -index)
+  for (int t = warp; !counting && t < tb_n; t += kThreads / 32) {
+    const float* z = zl + t * NP;
+    float zq[8];
+    unsigned taken = 0;
+    bool nonfin = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = lane + 32 * q;
+      zq[q] = (j < N) ? z[j] : -INFINITY;
+      if (j >= N) taken |= 1u << q;
+      else if (!(fabsf(zq[q]) < 3.0e38f)) nonfin = true;
+    }
+    if (__any_sync(0xffffffffu, nonfin)) {
+      if (lane == 0) sm.bad[t] = 1;
+      continue;
+    }
+    for (int r = 0; r <= kk; ++r) {
+      float bv = -INFINITY;
+      int bj = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = lane + 32 * q;
+        if (!(taken & (1u << q)) && (zq[q] > bv || (zq[q] == bv && j < bj))) {
+          bv = zq[q];
+          bj = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov > bv || (ov == bv && oj < bj)) {
+          bv = ov;
+          bj = oj;
+        }
+      }
+      if (lane == 0) sm.sel[t][r] = bj;
+      if ((bj & 31) == lane) taken |= 1u << (bj >> 5);
+    }
+  }
+  __syncthreads();
+  // (2) certificate, softmax, outputs: one warp per token
+  for (int t = warp; t < tb_n; t += kThreads / 32) {
+    const float* z = zl + t * NP;
+    const int* sel = sm.sel[t];
+    if (sm.bad[t] || force_fp64) {
+      if (lane == 0) {
+        const int f = atomicAdd(sm.nflag, 1);
+        sm.flag[f] = t;
+        for (int q = 0; q < 8; ++q)
+          sm.cmask[f][q] = (32 * q >= N) ? 0u : (N - 32 * q >= 32 ? 0xffffffffu
+                                                                  : ((1u << (N - 32 * q)) - 1u));
+      }
+      __syncwarp();
+      continue;
+    }
+    const float zr = (lane <= kk) ? z[sel[lane]] : 0.f;   // my rank's logit (lane r <= kk)
+    const float z0 = __shfl_sync(0xffffffffu, zr, 0);
+    const float zn = __shfl_down_sync(0xffffffffu, zr, 1);
+    // certificate: every rank r <= kk clear of the fp64 softmax underflow
+    // zone; gaps (r, r+1) for r < kk wider than both bounds
+    int ok = 1;
+    if (lane <= kk) {
+      const int a = sel[lane];
+      ok = (zr - z0 > -600.f);
+      if (lane < kk) {
+        const int b = sel[lane + 1];
+        const float bnd = gamma * sqrtf(xn[t]) * (wn[a] + wn[b]) + 1e-30f;
+        ok = ok && (zr - zn > bnd);
+      }
+    }
+    const bool spread = __any_sync(0xffffffffu, lane <= kk && !(zr - z0 > -600.f));
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok) {
+      // candidates: j with z_j + B_j >= L = min_{r<k} (z_r - B_r); every
+      // expert when the row reaches the fp64 softmax underflow zone
+      const float xnr = gamma * sqrtf(xn[t]);
+      float lo = INFINITY;
+      if (lane < k) lo = zr - (xnr * wn[sel[lane]] + 1e-30f);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      uint32_t words[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = lane + 32 * q;
+        const bool in = j < N && (spread || z[j] + (xnr * wn[j] + 1e-30f) >= lo);
+        words[q] = __ballot_sync(0xffffffffu, in);
+      }
+      if (lane == 0) {
+        const int f = atomicAdd(sm.nflag, 1);
+        sm.flag[f] = t;
+        for (int q = 0; q < 8; ++q) sm.cmask[f][q] = words[q];
+      }
+      __syncwarp();
+      continue;
+    }
+    float sum = 0.f;
+    for (int j = lane; j < N; j += 32) sum += expf(z[j] - z0);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const int64_t tt = t0 + t;
+    const float p = (lane < k) ? expf(zr - z0) / sum : 0.f;
+    float tot = p;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane < k) {
+      const int j = sel[lane];
+      if (topk_idx) topk_idx[tt * k + lane] = j;
+      if (topk_w) topk_w[tt * k + lane] = renorm ? p / tot : p;
+      atomicAdd(&sm.hist[j], 1);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  RG_MARK(7);
+  // (3) fp64 recompute of the uncertified rows (rare)
+  const int nflag = *sm.nflag;
+  for (int f = 0; f < nflag; ++f) {
+    const int t = sm.flag[f];
+    const int64_t tt = t0 + t;
+    fp64_row_cand(hidden + tt * (int64_t)d, residual, gate, d, N, k, renorm, sm.cmask[f],
+                  zl + t * NP, ring64, ring64 + d, sm.row64, sm.cl, sm.nc,
+                  topk_idx ? topk_idx + tt * k : nullptr, topk_w ? topk_w + tt * k : nullptr,
+                  sm.hist);
+  }
+  RG_MARK(8);
+  if (tid == 0) {
+    if (nflag) atomicAdd(&g_route_fires, (unsigned long long)nflag);
+    atomicAdd(&g_route_rows, (unsigned long long)tb_n);
+  }
+  __syncthreads();
+}
+
 template <int TB, int C>
 __global__ void __launch_bounds__(kThreads)
 route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict__ residual,
@@ -211,7 +404,6 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
                    int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
                    unsigned long long* __restrict__ workloads,
                    const float* __restrict__ wnorm2, Geo g, float gamma, int force_fp64) {
-  DALI_PDL_ENTRY();
   RG_MARK(0);
   constexpr int TG = TB / 4;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -227,7 +419,8 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
   __shared__ float sh_xn[TB], sh_wn[256];
   __shared__ float sh_red_xn[(kThreads / 32) * TB];
   __shared__ int sh_hist[256];
-  __shared__ int sh_sel[8][DALI_MAX_TOPK + 1];
+  __shared__ int sh_sel[TB][DALI_MAX_TOPK + 1];
+  __shared__ int sh_bad[TB];
   __shared__ int sh_flag[TB];
   __shared__ int sh_nflag;
   __shared__ double sh_row64[256];
@@ -245,10 +438,11 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
   const int xraw_bytes = TB * g.DC * 2;
 
   for (int i = tid; i < N; i += kThreads) sh_hist[i] = 0;
+  for (int i = tid; i < TB; i += kThreads) sh_bad[i] = 0;
   if (tid == 0) sh_nflag = 0;
 
   // stage issue: raw bf16 x rows [TB][DC] and the contiguous W rows [DC][N]
-  auto issue = [&](int c, int slot) {
+  auto issue_x = [&](int c, int slot) {
     unsigned char* st = ring + slot * kStageBytes;
     const int c0 = d0 + c * g.DC;
     const int upr = g.DC / 8;                        // 16-byte units per x row
@@ -259,6 +453,10 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
       const uint16_t* src = ok ? hidden + (t0 + t) * (int64_t)d + col : hidden;
       cp_async16(st + u * 16, src, ok);
     }
+  };
+  auto issue_w = [&](int c, int slot) {
+    unsigned char* st = ring + slot * kStageBytes;
+    const int c0 = d0 + c * g.DC;
     const int wunits = g.DC * N / 8;
     const int64_t wbase = (int64_t)c0 * N;          // element offset, multiple of 8
     const int64_t wend = (int64_t)d1 * N;
@@ -267,6 +465,10 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
       const bool ok = el < wend;
       cp_async16(st + xraw_bytes + u * 16, ok ? gate + el : gate, ok);
     }
+  };
+  auto issue = [&](int c, int slot) {
+    issue_x(c, slot);
+    issue_w(c, slot);
   };
 
   // register tile: tokens tg + TG*j (j < 4), experts eg*8 .. eg*8+7, d-slice s.
@@ -298,13 +500,17 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
   const int xt = tid % TB, xsub = tid / TB;
   float xn_p = 0.f;
 
+  // the router (and its column norms, for the bound) never depends on the
+  // previous kernel: request the first stages' router rows before the PDL
+  // wait so they stream while the predecessor drains
+  for (int c = 0; c < kStages - 1; ++c)
+    if (c < nchunks) issue_w(c, c);
+  const float wn2v = tid < N ? __ldg(wnorm2 + tid) : 0.f;
+  DALI_PDL_ENTRY();
   for (int c = 0; c < kStages - 1; ++c) {
-    if (c < nchunks) issue(c, c);
+    if (c < nchunks) issue_x(c, c);
     cp_commit();
   }
-  // router column norms (the bound uses ||W_:j||), read after the operand
-  // loads are in flight
-  for (int i = tid; i < N; i += kThreads) sh_wn[i] = sqrtf(wnorm2[i]);
   RG_MARK(1);
   for (int c = 0; c < nchunks; ++c) {
     cp_wait<kStages - 2>();
@@ -451,141 +657,11 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
   }
   __syncthreads();
 
-  // rank, certify, softmax: one warp per token.  The k+1 leading experts are
-  // picked by k+1 warp-wide argmax rounds over (logit, -index) -- ties to the
-  // lower index -- then lane r certifies the gap between ranks r and r+1.
-  const int warp = wid;
-  const int kk = (k < N) ? k : N - 1;          // last rank whose order must be certain
-  for (int t = warp; t < tb_n; t += kThreads / 32) {
-    const float* z = sh_logit + t * g.NP;
-    int* sel = sh_sel[warp];
-    // lane-local candidates: experts lane, lane+32, ... (N <= 256 -> <= 8)
-    float zl[8];
-    unsigned taken = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int j = lane + 32 * q;
-      zl[q] = (j < N) ? z[j] : -INFINITY;
-      if (j >= N) taken |= 1u << q;
-    }
-    // a non-finite logit anywhere in the row: no certificate (fp64 recompute)
-    bool bad = false;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (lane + 32 * q < N && !(fabsf(zl[q]) < 3.0e38f)) bad = true;
-    if (__any_sync(0xffffffffu, bad) || force_fp64) {
-      if (lane == 0) {
-        const int f = atomicAdd(&sh_nflag, 1);
-        sh_flag[f] = t;
-        for (int q = 0; q < 8; ++q)
-          sh_cmask[f][q] = (32 * q >= N) ? 0u : (N - 32 * q >= 32 ? 0xffffffffu
-                                                                 : ((1u << (N - 32 * q)) - 1u));
-      }
-      __syncwarp();
-      continue;
-    }
-    float zr = 0.f;                              // my rank's logit (lane r <= kk)
-    for (int r = 0; r <= kk; ++r) {
-      float bv = -INFINITY;
-      int bj = 0x7fffffff;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int j = lane + 32 * q;
-        if (!(taken & (1u << q)) && (zl[q] > bv || (zl[q] == bv && j < bj))) {
-          bv = zl[q];
-          bj = j;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if (ov > bv || (ov == bv && oj < bj)) {
-          bv = ov;
-          bj = oj;
-        }
-      }
-      if (lane == r) zr = bv;
-      if (lane == 0) sel[r] = bj;
-      if ((bj & 31) == lane) taken |= 1u << (bj >> 5);
-    }
-    __syncwarp();
-    // certificate: every rank r <= kk finite and clear of the fp64 softmax
-    // underflow zone; gaps (r, r+1) for r < kk wider than both bounds
-    const float z0 = __shfl_sync(0xffffffffu, zr, 0);
-    const float zn = __shfl_down_sync(0xffffffffu, zr, 1);
-    int ok = 1;
-    if (lane <= kk) {
-      const int a = sel[lane];
-      ok = fabsf(zr) < 3.0e38f && (zr - z0 > -600.f);
-      if (lane < kk) {
-        const int b = sel[lane + 1];
-        const float bnd = gamma * sqrtf(sh_xn[t]) * (sh_wn[a] + sh_wn[b]) + 1e-30f;
-        ok = ok && (zr - zn > bnd);
-      }
-    }
-    const bool spread = __any_sync(0xffffffffu, lane <= kk && !(zr - z0 > -600.f));
-    ok = __all_sync(0xffffffffu, ok);
-    if (!ok) {
-      // candidates: j with z_j + B_j >= L = min_{r<k} (z_r - B_r); every
-      // expert when the row reaches the fp64 softmax underflow zone
-      const float xnr = gamma * sqrtf(sh_xn[t]);
-      float lo = INFINITY;
-      if (lane < k) lo = zr - (xnr * sh_wn[sel[lane]] + 1e-30f);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      uint32_t words[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int j = lane + 32 * q;
-        const bool in = j < N && (spread || zl[q] + (xnr * sh_wn[j] + 1e-30f) >= lo);
-        words[q] = __ballot_sync(0xffffffffu, in);
-      }
-      if (lane == 0) {
-        const int f = atomicAdd(&sh_nflag, 1);
-        sh_flag[f] = t;
-        for (int q = 0; q < 8; ++q) sh_cmask[f][q] = words[q];
-      }
-      __syncwarp();
-      continue;
-    }
-    float sum = 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (lane + 32 * q < N) sum += expf(zl[q] - z0);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const int64_t tt = t0 + t;
-    const float p = (lane < k) ? expf(zr - z0) / sum : 0.f;
-    float tot = p;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if (lane < k) {
-      const int j = sel[lane];
-      if (topk_idx) topk_idx[tt * k + lane] = j;
-      if (topk_w) topk_w[tt * k + lane] = renorm ? p / tot : p;
-      atomicAdd(&sh_hist[j], 1);
-    }
-    __syncwarp();
-  }
+  if (tid < N) sh_wn[tid] = sqrtf(wn2v);
   __syncthreads();
-  RG_MARK(7);
-  const int nflag = sh_nflag;
-  for (int f = 0; f < nflag; ++f) {
-    const int t = sh_flag[f];
-    const int64_t tt = t0 + t;
-    double* ring64 = reinterpret_cast<double*>(ring);          // [d] x row, then partials
-    fp64_row_cand(hidden + tt * (int64_t)d, residual, gate, d, N, k, renorm, sh_cmask[f],
-                  sh_logit + t * g.NP, ring64, ring64 + d, sh_row64, sh_cl, &sh_nc,
-                  topk_idx ? topk_idx + tt * k : nullptr, topk_w ? topk_w + tt * k : nullptr,
-                  sh_hist);
-  }
-  RG_MARK(8);
-  if (tid == 0) {
-    if (nflag) atomicAdd(&g_route_fires, (unsigned long long)nflag);
-    atomicAdd(&g_route_rows, (unsigned long long)tb_n);
-  }
-  __syncthreads();
+  TailSmem tsm{sh_hist, sh_sel, sh_flag, &sh_nflag, sh_cmask, sh_bad, sh_row64, sh_cl, &sh_nc};
+  rank_tail<TB>(sh_logit, g.NP, sh_xn, sh_wn, tb_n, t0, N, k, renorm, gamma, force_fp64, hidden,
+                residual, gate, d, topk_idx, topk_w, reinterpret_cast<double*>(ring), tsm);
   if (workloads) {
     const bool single = (C > 1) || gridDim.x == 1;
     for (int i = tid; i < N; i += kThreads) {

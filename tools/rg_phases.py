@@ -20,7 +20,7 @@ d, N, k = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (4096, 8, 2)
 Ts = [int(x) for x in (sys.argv[4].split(",") if len(sys.argv) > 4 else ["1", "16", "512"])]
 g = (torch.randn(d, N, device="cuda") * 0.02).to(torch.bfloat16)
 n2 = gate_norm2(g)
-names = ["entry", "issued", "landed", "loop", "reduce", "pre-cl", "post-cl", "rank", "fp64"]
+names = ["entry", "issued", "landed", "loop", "reduce", "pre-cl", "post-cl", "rank", "fp64"]  # tile kernel: 4 = tree done, no 5-6
 for T in Ts:
     h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
     for _ in range(5):
