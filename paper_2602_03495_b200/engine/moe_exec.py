@@ -96,7 +96,10 @@ class MoEExecMixin:
         o_idx = o_off + ((N + 1) * 4 + 7) // 8 * 8
         o_w = o_idx + T * k * 4
         nb = o_w + T * k * 4
-        rblk = self._ws("route", (nb,), torch.uint8)
+        # the all-resident side-stream policy kernel reads this layer's
+        # workloads after the next layer's route ran: one block per layer then
+        side = self.resident_mode and self.cfg.policy_side_stream
+        rblk = self._ws(f"route{l}" if side else "route", (nb,), torch.uint8)
         v = {
             "wl": rblk[:o_off].view(torch.int64),
             "offsets": rblk[o_off:o_off + (N + 1) * 4].view(torch.int32),
@@ -538,13 +541,21 @@ class MoEExecMixin:
         v = self._route(l, h)
         if T == self.kv.k.shape[1] and self.stats.steps_meta:     # decode: device descriptor
             ri = self.policy.n_records + l
+            ps = cs
+            if self.cfg.policy_side_stream:
+                # nothing downstream of the decision reads it here (every expert is
+                # resident, the FFN uses the static map table): the policy kernel
+                # runs beside the layer; _forward joins before the step advances
+                ps = self.policy_stream
+                ps.wait_stream(cs)
+                self._policy_side_used = True
             _lib.call("dali_policy_layer_desc", C.addressof(self.policy.cfg),
                       C.addressof(self.policy.cm_c), l, self.desc_dev.data_ptr(),
                       v["wl"].data_ptr(), None, self.policy.on_gpu.data_ptr(),
                       self.policy.scores.data_ptr(), self.policy.counters.data_ptr(),
                       self.policy.arrived.data_ptr(), self.policy.slot_of.data_ptr(),
                       self.policy.lru_state.data_ptr(), None, 0, self.policy.record_ptr(0),
-                      cs.cuda_stream)
+                      ps.cuda_stream)
             if l == a.num_layers - 1 and not self._in_capture:
                 self.policy.n_records += a.num_layers
         else:

@@ -80,6 +80,10 @@ class EngineConfig:
     ep_transport: str = "p2p"               # expert parallelism: "p2p" (peer-memory kernels,
     #                                         csrc/ep.cu) or "nccl" (all_to_all baseline)
     trace_layers: bool = False              # per-layer host/device timeline (tools/decode_timeline.py)
+    policy_side_stream: bool = os.environ.get("DALI_POLICY_SIDE", "1") != "0"
+    #                                         all-resident decode: the policy kernel (records
+    #                                         only, nothing downstream reads them) runs on a
+    #                                         side stream off the layer's critical path
 
 
 @dataclass
@@ -171,6 +175,8 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
             insert_prefetched=cfg.insert_prefetched, prefetch_kind=cfg.prefetch_kind,
             frequency_table=cfg.frequency_table)
         self.copy_stream = torch.cuda.Stream()       # demand + prefetch expert copies
+        self.policy_stream = torch.cuda.Stream()     # all-resident decode: policy records
+        self._policy_side_used = False
         self.repl_stream = torch.cuda.Stream()       # cache replacement copies (off the
         #                                              demand path: never delays a demand copy)
         # HBM expert cache slots: layer l owns slots [l*slots, (l+1)*slots)
@@ -362,6 +368,9 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
             _lib.call("dali_add_rmsnorm", x.data_ptr(), att.data_ptr(), W.moe_norm[l].data_ptr(),
                       a.rms_eps, T, d, x2.data_ptr(), h.data_ptr(), sp)
             x = self._moe(l, x2, h, step, token_index, is_eos)
+        if self._policy_side_used:              # join the side-stream policy kernels
+            self._cur().wait_stream(self.policy_stream)
+            self._policy_side_used = False
         last = x.view(B, S, -1)[:, -1]
         return rms_norm(last, W.final_norm, a.rms_eps) @ W.lm_head.t()
 
