@@ -517,6 +517,19 @@ gemv_bf16_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w,
 }
 }  // namespace dali
 
+namespace dali {
+int launch_gemv_stream(const uint16_t* x, const uint16_t* w, int Bt, int M, int K, uint16_t* y,
+                       cudaStream_t st);
+// A/B switch: DALI_GEMV_STREAM=0 keeps every GEMV on the row-per-warp kernel
+static bool gemv_stream_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("DALI_GEMV_STREAM");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+}  // namespace dali
+
 extern "C" int dali_gemv_bf16(const uint16_t* x, const uint16_t* w, int32_t Bt, int32_t M,
                               int32_t K, uint16_t* y, void* stream) {
   DALI_REQUIRE(Bt >= 1 && Bt <= dali::kGemvMaxB, DALI_ETRACE, "gemv batch %d outside [1, %d]",
@@ -524,6 +537,10 @@ extern "C" int dali_gemv_bf16(const uint16_t* x, const uint16_t* w, int32_t Bt, 
   DALI_REQUIRE(K % 8 == 0 && M >= 1, DALI_ETRACE, "gemv needs K %% 8 == 0 (K=%d)", K);
   const size_t smem = (size_t)Bt * K * 2;
   DALI_REQUIRE(smem <= 200 * 1024, DALI_ETRACE, "gemv activations exceed shared memory");
+  if (dali::gemv_stream_enabled()) {
+    const int rc = dali::launch_gemv_stream(x, w, Bt, M, K, y, as_stream(stream));
+    if (rc >= 0) return rc;
+  }
   const dim3 grid((unsigned)((M + dali::kGemvWarps - 1) / dali::kGemvWarps));
   const dim3 block(dali::kGemvWarps * 32);
   cudaStream_t st = as_stream(stream);

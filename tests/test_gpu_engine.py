@@ -427,6 +427,36 @@ def test_resident_graph_replay_matches_eager():
             assert np.array_equal(a_["G"], b_["G"])
 
 
+def test_resident_side_stream_policy_matches_inline():
+    """The all-resident decode graph runs the policy kernel on a side stream
+    (EngineConfig.policy_side_stream): every decision record -- workloads,
+    C/G, lookups, window events, virtual-clock latency -- equals the inline
+    (same-stream) launch's, over two requests (graph capture, then replay)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine
+    arch = _mini_mixtral()
+    w = ModelWeights(arch, seed=3, resident=True)
+    cm = default_cost_model(non_moe_layer_time=1.0)
+    side = OffloadEngine(arch, w, cm, EngineConfig(policy_side_stream=True), max_seq=64)
+    inl = OffloadEngine(arch, w, cm, EngineConfig(policy_side_stream=False), max_seq=64)
+    prompt = torch.randint(0, arch.vocab_size, (1, 8), generator=torch.Generator().manual_seed(9))
+    for rep in range(2):
+        ts, ss = side.generate(prompt, 12)
+        ti, si = inl.generate(prompt, 12)
+        assert side._graph is not None and torch.equal(ts, ti), rep
+        ds, di = side.policy.decision_log(), inl.policy.decision_log()
+        assert len(ds) == len(di) == 12 * arch.num_layers
+        for a_, b_ in zip(ds, di):
+            for key in ("C", "G", "resident"):
+                assert np.array_equal(a_[key], b_[key]), (rep, key)
+            for key in ("step", "layer", "hits", "event", "latency", "cpu_busy", "gpu_makespan"):
+                assert a_[key] == b_[key], (rep, key)
+        for key in si.workloads:
+            assert np.array_equal(ss.workloads[key], si.workloads[key]), (rep, key)
+
+
 @pytest.mark.parametrize("name", ["tiny", "tiny-shared"])
 def test_offload_decode_graphs_match_eager(name):
     """Offloaded decode with per-layer CUDA-graph heads (device descriptor for
@@ -640,7 +670,9 @@ def test_full_width_layers_decisions_and_logits(name, slots, psize):
         torch.testing.assert_close(lg[0], ref, rtol=RTOL, atol=RTOL * ref.abs().max().item())
 
 
-@pytest.mark.parametrize("B,M,K", [(1, 6144, 4096), (2, 4096, 4096), (8, 512, 256), (3, 96, 64)])
+@pytest.mark.parametrize("B,M,K", [(1, 6144, 4096), (2, 4096, 4096), (8, 512, 256), (3, 96, 64),
+                                   (1, 10240, 6144), (4, 3072, 2048), (1, 6144, 6144),
+                                   (5, 1000, 4096)])
 def test_decode_gemv_vs_torch(B, M, K):
     """dali_gemv_bf16 (attention projections at decode) vs fp32 torch."""
     if not torch.cuda.is_available():
@@ -654,6 +686,39 @@ def test_decode_gemv_vs_torch(B, M, K):
               torch.cuda.current_stream().cuda_stream)
     ref = x.float() @ w.float().t()
     torch.testing.assert_close(y.float(), ref, rtol=1e-2, atol=1e-2 * ref.abs().max().item())
+
+
+def test_gemv_stream_bit_identical_to_row_kernel():
+    """The persistent TMA-streaming GEMV (csrc/gemv.cu, weights requested
+    before the PDL wait) and the row-per-warp kernel it replaced
+    (DALI_GEMV_STREAM=0) produce bit-identical outputs: same per-lane chunk
+    assignment, FMA order and butterfly reduction."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import os
+    import subprocess
+    import sys
+    code = ("import torch,sys;sys.path.insert(0,%r);from paper_2602_03495_b200 import _lib\n"
+            "out=[]\n"
+            "for (B,M,K) in [(1,6144,4096),(2,4096,4096),(8,1000,4096),(1,10240,6144)]:\n"
+            "  g=torch.Generator(device='cuda').manual_seed(M+B)\n"
+            "  x=torch.randn(B,K,device='cuda',generator=g).to(torch.bfloat16)\n"
+            "  w=(torch.randn(M,K,device='cuda',generator=g)/K**0.5).to(torch.bfloat16)\n"
+            "  y=torch.empty(B,M,dtype=torch.bfloat16,device='cuda')\n"
+            "  _lib.call('dali_gemv_bf16',x.data_ptr(),w.data_ptr(),B,M,K,y.data_ptr(),"
+            "torch.cuda.current_stream().cuda_stream)\n"
+            "  out.append(y.cpu())\n"
+            "torch.save(out,sys.argv[1])\n") % os.path.dirname(os.path.dirname(__file__))
+    res = {}
+    for flag in ("0", "1"):
+        path = f"/tmp/gemv_ab_{flag}_{os.getpid()}.pt"
+        r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True,
+                           env=dict(os.environ, DALI_GEMV_STREAM=flag), timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[flag] = torch.load(path)
+        os.remove(path)
+    for a_, b_ in zip(res["0"], res["1"]):
+        assert torch.equal(a_, b_)
 
 
 def test_tc_ffn_single_cta_wide_path_subprocess():
