@@ -384,6 +384,18 @@ int dali_shared_finish(const float* ys, int32_t splits, int64_t T, int32_t d,
 int dali_gemv_bf16(const uint16_t* x, const uint16_t* w, int32_t B, int32_t M, int32_t K,
                    uint16_t* y, void* stream);
 
+/* Decode GEMV with the attention block's RMSNorms fused in (engine plumbing;
+ * same arithmetic as dali_add_rmsnorm + dali_gemv_bf16, bit for bit):
+ *   norm_in_w != NULL: the GEMV input is RMSNorm(x) * norm_in_w (x is the raw
+ *     residual stream; eps as in dali_add_rmsnorm);
+ *   res != NULL (M == row width): after y, x2_out = res + y and
+ *     h_out = RMSNorm(x2_out) * norm_out_w, computed by the last CTA to
+ *     finish (counter [dev] u32, zero-initialised, left zero).
+ * 1 <= B <= 8, K % 8 == 0, M % 8 == 0, M >= 16. */
+int dali_gemv_norm_bf16(const uint16_t* x, const uint16_t* w, int32_t B, int32_t M, int32_t K,
+                        uint16_t* y, const uint16_t* norm_in_w, float eps, const uint16_t* res,
+                        const uint16_t* norm_out_w, uint16_t* x2_out, uint16_t* h_out,
+                        uint32_t* counter, void* stream);
 /* Engine plumbing: fused residual add + RMSNorm over (T, d) bf16 rows:
  *   x_out = x + a (a may be NULL: x_out untouched, x used as is);
  *   h = bf16(bf16(x_out * rsqrt(mean(x_out^2) + eps)) * w). */

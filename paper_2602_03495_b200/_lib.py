@@ -108,6 +108,7 @@ SIGNATURES = {
                               _P, _P],
     "dali_cpu_expert": [_P, _I32, _I32, _P, _I32, _P, _I32],
     "dali_cpu_expert_amx_available": [],
+    "dali_gemv_norm_bf16": [_P, _P, _I32, _I32, _I32, _P, _P, C.c_float, _P, _P, _P, _P, _P, _P],
     "dali_cpu_expert_submit": [_I32, _P, _P, _P, _P, _I32, _I32, _I32],
     "dali_cpu_expert_wait": [],
     "dali_add_rmsnorm": [_P, _P, _P, C.c_float, _I64, _I32, _P, _P, _P],

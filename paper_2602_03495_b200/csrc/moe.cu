@@ -518,8 +518,11 @@ gemv_bf16_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w,
 }  // namespace dali
 
 namespace dali {
+namespace gemv {
+struct NormArgs;
+}
 int launch_gemv_stream(const uint16_t* x, const uint16_t* w, int Bt, int M, int K, uint16_t* y,
-                       cudaStream_t st);
+                       cudaStream_t st, const gemv::NormArgs* norm);
 // A/B switch: DALI_GEMV_STREAM=0 keeps every GEMV on the row-per-warp kernel
 static bool gemv_stream_enabled() {
   static const bool v = [] {
@@ -538,7 +541,7 @@ extern "C" int dali_gemv_bf16(const uint16_t* x, const uint16_t* w, int32_t Bt, 
   const size_t smem = (size_t)Bt * K * 2;
   DALI_REQUIRE(smem <= 200 * 1024, DALI_ETRACE, "gemv activations exceed shared memory");
   if (dali::gemv_stream_enabled()) {
-    const int rc = dali::launch_gemv_stream(x, w, Bt, M, K, y, as_stream(stream));
+    const int rc = dali::launch_gemv_stream(x, w, Bt, M, K, y, as_stream(stream), nullptr);
     if (rc >= 0) return rc;
   }
   const dim3 grid((unsigned)((M + dali::kGemvWarps - 1) / dali::kGemvWarps));

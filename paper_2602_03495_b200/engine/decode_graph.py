@@ -31,6 +31,19 @@ class DecodeGraphMixin:
                       a.hidden_dim, qkv.data_ptr(), sp)
         else:
             qkv = hn @ W.wqkv[l].t()
+        o = self._attn_core(l, qkv, B)
+        if B <= 8:
+            att = self._ws("att_dec", (B, a.hidden_dim), torch.bfloat16)
+            _lib.call("dali_gemv_bf16", o.data_ptr(), W.wo[l].data_ptr(), B, a.hidden_dim,
+                      H * hd, att.data_ptr(), sp)
+            return att
+        return o @ W.wo[l].t()
+
+    def _attn_core(self, l: int, qkv: torch.Tensor, B: int) -> torch.Tensor:
+        """Fused RoPE + KV append and split-K decode attention -> o (B, H*hd)."""
+        a = self.arch
+        H, KV, hd = a.num_heads, a.num_kv_heads, a.head_dim
+        sp = self._cur().cuda_stream
         q = self._ws("q_dec", (B, H, hd), torch.bfloat16)
         kc, vc = self.kv.k[l], self.kv.v[l]
         _lib.call("dali_rope_append", qkv.data_ptr(), self.rope.cos.data_ptr(),
@@ -42,12 +55,39 @@ class DecodeGraphMixin:
         _lib.call("dali_decode_attention", q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
                   self.desc_dev.data_ptr() + 20, B, H, KV, hd, self.max_seq, splits,
                   1.0 / math.sqrt(hd), ws.data_ptr(), o.data_ptr(), sp)
-        if B <= 8:
-            att = self._ws("att_dec", (B, a.hidden_dim), torch.bfloat16)
-            _lib.call("dali_gemv_bf16", o.data_ptr(), W.wo[l].data_ptr(), B, a.hidden_dim,
-                      H * hd, att.data_ptr(), sp)
-            return att
-        return o @ W.wo[l].t()
+        return o
+
+    def _attn_block(self, l: int, X: torch.Tensor, X2: torch.Tensor, h: torch.Tensor,
+                    B: int) -> None:
+        """Whole decode attention block of layer l: X2 = X + attn(RMSNorm(X)),
+        h = RMSNorm(X2).  With the fused GEMVs (B <= 8) the input norm runs
+        inside the qkv projection and the residual add + MoE norm in the
+        o-projection's last CTA (dali_gemv_norm_bf16): two launches fewer per
+        layer than the separate add_rmsnorm kernels, bit-identical results."""
+        a, W = self.arch, self.w
+        d = a.hidden_dim
+        sp = self._cur().cuda_stream
+        if not (B <= 8 and self.cfg.fused_norm_gemv):
+            hn = self._ws("hn", (B, d), torch.bfloat16)
+            _lib.call("dali_add_rmsnorm", X.data_ptr(), None, W.attn_norm[l].data_ptr(),
+                      a.rms_eps, B, d, None, hn.data_ptr(), sp)
+            att = self._attn_decode(l, hn, B)
+            _lib.call("dali_add_rmsnorm", X.data_ptr(), att.data_ptr(), W.moe_norm[l].data_ptr(),
+                      a.rms_eps, B, d, X2.data_ptr(), h.data_ptr(), sp)
+            return
+        H, KV, hd = a.num_heads, a.num_kv_heads, a.head_dim
+        nqkv = (H + 2 * KV) * hd
+        if self._gemv_ctr is None:
+            self._gemv_ctr = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        qkv = self._ws("qkv_dec", (B, nqkv), torch.bfloat16)
+        _lib.call("dali_gemv_norm_bf16", X.data_ptr(), W.wqkv[l].data_ptr(), B, nqkv, d,
+                  qkv.data_ptr(), W.attn_norm[l].data_ptr(), a.rms_eps, None, None, None, None,
+                  None, sp)
+        o = self._attn_core(l, qkv, B)
+        att = self._ws("att_dec", (B, d), torch.bfloat16)
+        _lib.call("dali_gemv_norm_bf16", o.data_ptr(), W.wo[l].data_ptr(), B, d, H * hd,
+                  att.data_ptr(), None, a.rms_eps, X.data_ptr(), W.moe_norm[l].data_ptr(),
+                  X2.data_ptr(), h.data_ptr(), self._gemv_ctr.data_ptr(), sp)
 
     def _offload_graphable(self) -> bool:
         # the random predictor draws on the host every step: not graph-capturable
@@ -62,13 +102,8 @@ class DecodeGraphMixin:
         a, W = self.arch, self.w
         d = a.hidden_dim
         sp = self._cur().cuda_stream
-        hn = self._ws("hn", (B, d), torch.bfloat16)
         h = self._ws("h", (B, d), torch.bfloat16)
-        _lib.call("dali_add_rmsnorm", X.data_ptr(), None, W.attn_norm[l].data_ptr(), a.rms_eps,
-                  B, d, None, hn.data_ptr(), sp)
-        att = self._attn_decode(l, hn, B)
-        _lib.call("dali_add_rmsnorm", X.data_ptr(), att.data_ptr(), W.moe_norm[l].data_ptr(),
-                  a.rms_eps, B, d, X2.data_ptr(), h.data_ptr(), sp)
+        self._attn_block(l, X, X2, h, B)
         return h, self._moe_head(l, h, 0, 0, False, use_desc=True)
 
     def _decode_offload(self, tok_dev: torch.Tensor, B: int, is_eos: bool) -> torch.Tensor:

@@ -80,6 +80,9 @@ class EngineConfig:
     ep_transport: str = "p2p"               # expert parallelism: "p2p" (peer-memory kernels,
     #                                         csrc/ep.cu) or "nccl" (all_to_all baseline)
     trace_layers: bool = False              # per-layer host/device timeline (tools/decode_timeline.py)
+    fused_norm_gemv: bool = os.environ.get("DALI_FUSED_NORM", "1") != "0"
+    #                                         decode (B <= 8): attention-block RMSNorms fused
+    #                                         into the qkv / o projection GEMVs
     policy_side_stream: bool = os.environ.get("DALI_POLICY_SIDE", "1") != "0"
     #                                         all-resident decode: the policy kernel (records
     #                                         only, nothing downstream reads them) runs on a
@@ -175,6 +178,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
             insert_prefetched=cfg.insert_prefetched, prefetch_kind=cfg.prefetch_kind,
             frequency_table=cfg.frequency_table)
         self.copy_stream = torch.cuda.Stream()       # demand + prefetch expert copies
+        self._gemv_ctr = None                        # fused o-projection + norm counter
         self.policy_stream = torch.cuda.Stream()     # all-resident decode: policy records
         self._policy_side_used = False
         self.repl_stream = torch.cuda.Stream()       # cache replacement copies (off the
@@ -358,15 +362,16 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         h = self._ws("h", (T, d), torch.bfloat16)
         dev_attn = S == 1 and a.head_dim in (64, 128)
         for l in range(a.num_layers):
-            _lib.call("dali_add_rmsnorm", x.data_ptr(), None, W.attn_norm[l].data_ptr(),
-                      a.rms_eps, T, d, None, hn.data_ptr(), sp)
-            if dev_attn:
-                att = self._attn_decode(l, hn, B)
-            else:
-                att = attention(a, hn, W.wqkv[l], W.wo[l], self.rope, self.kv, l, B, S, pos0)
             x2 = torch.empty_like(x)
-            _lib.call("dali_add_rmsnorm", x.data_ptr(), att.data_ptr(), W.moe_norm[l].data_ptr(),
-                      a.rms_eps, T, d, x2.data_ptr(), h.data_ptr(), sp)
+            if dev_attn:
+                self._attn_block(l, x, x2, h, B)
+            else:
+                _lib.call("dali_add_rmsnorm", x.data_ptr(), None, W.attn_norm[l].data_ptr(),
+                          a.rms_eps, T, d, None, hn.data_ptr(), sp)
+                att = attention(a, hn, W.wqkv[l], W.wo[l], self.rope, self.kv, l, B, S, pos0)
+                _lib.call("dali_add_rmsnorm", x.data_ptr(), att.data_ptr(),
+                          W.moe_norm[l].data_ptr(), a.rms_eps, T, d, x2.data_ptr(), h.data_ptr(),
+                          sp)
             x = self._moe(l, x2, h, step, token_index, is_eos)
         if self._policy_side_used:              # join the side-stream policy kernels
             self._cur().wait_stream(self.policy_stream)

@@ -688,6 +688,53 @@ def test_decode_gemv_vs_torch(B, M, K):
     torch.testing.assert_close(y.float(), ref, rtol=1e-2, atol=1e-2 * ref.abs().max().item())
 
 
+@pytest.mark.parametrize("B,d,nqkv,nh", [(1, 4096, 6144, 4096), (3, 2048, 3072, 2048),
+                                         (8, 4096, 6144, 4096), (1, 6144, 10240, 6144)])
+def test_gemv_norm_fusion_bit_identical(B, d, nqkv, nh):
+    """dali_gemv_norm_bf16 (input RMSNorm inside the qkv projection; residual
+    add + RMSNorm in the o projection's last CTA) == dali_add_rmsnorm +
+    dali_gemv_bf16, bit for bit, over repeated launches (the grid counter
+    must come back to zero)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(B + d)
+    bf = torch.bfloat16
+    X = torch.randn(B, d, device="cuda", generator=g).to(bf)
+    wn1 = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).to(bf)
+    wn2 = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).to(bf)
+    Wqkv = (torch.randn(nqkv, d, device="cuda", generator=g) / d ** 0.5).to(bf)
+    Wo = (torch.randn(d, nh, device="cuda", generator=g) / nh ** 0.5).to(bf)
+    O = torch.randn(B, nh, device="cuda", generator=g).to(bf)
+    sp = torch.cuda.current_stream().cuda_stream
+    # reference: separate kernels
+    hn = torch.empty(B, d, dtype=bf, device="cuda")
+    _lib.call("dali_add_rmsnorm", X.data_ptr(), None, wn1.data_ptr(), 1e-5, B, d, None,
+              hn.data_ptr(), sp)
+    q_ref = torch.empty(B, nqkv, dtype=bf, device="cuda")
+    _lib.call("dali_gemv_bf16", hn.data_ptr(), Wqkv.data_ptr(), B, nqkv, d, q_ref.data_ptr(), sp)
+    att = torch.empty(B, d, dtype=bf, device="cuda")
+    _lib.call("dali_gemv_bf16", O.data_ptr(), Wo.data_ptr(), B, d, nh, att.data_ptr(), sp)
+    x2_ref, h_ref = torch.empty_like(X), torch.empty_like(X)
+    _lib.call("dali_add_rmsnorm", X.data_ptr(), att.data_ptr(), wn2.data_ptr(), 1e-5, B, d,
+              x2_ref.data_ptr(), h_ref.data_ptr(), sp)
+    ctr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        q = torch.full((B, nqkv), float("nan"), dtype=bf, device="cuda")
+        _lib.call("dali_gemv_norm_bf16", X.data_ptr(), Wqkv.data_ptr(), B, nqkv, d, q.data_ptr(),
+                  wn1.data_ptr(), 1e-5, None, None, None, None, None, sp)
+        y = torch.empty(B, d, dtype=bf, device="cuda")
+        x2 = torch.full_like(X, float("nan"))
+        h = torch.full_like(X, float("nan"))
+        _lib.call("dali_gemv_norm_bf16", O.data_ptr(), Wo.data_ptr(), B, d, nh, y.data_ptr(),
+                  None, 1e-5, X.data_ptr(), wn2.data_ptr(), x2.data_ptr(), h.data_ptr(),
+                  ctr.data_ptr(), sp)
+        torch.cuda.synchronize()
+        assert torch.equal(q, q_ref)
+        assert torch.equal(y, att) and torch.equal(x2, x2_ref) and torch.equal(h, h_ref)
+        assert int(ctr.item()) == 0
+
+
 def test_gemv_stream_bit_identical_to_row_kernel():
     """The persistent TMA-streaming GEMV (csrc/gemv.cu, weights requested
     before the PDL wait) and the row-per-warp kernel it replaced
