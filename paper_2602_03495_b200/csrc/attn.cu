@@ -85,9 +85,25 @@ decode_attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ 
   float m = -INFINITY, l = 0.f, acc[EL];
 #pragma unroll
   for (int i = 0; i < EL; ++i) acc[i] = 0.f;
+  // one position of look-ahead: the next K/V rows are requested before this
+  // position's dot product and shuffle reduction, so a warp has two rows of
+  // loads in flight instead of one
+  float kn[EL], vn[EL];
+  if (p0 + warp < p1) {
+    load_bf16_lane<EL>(kb + (int64_t)(p0 + warp) * HD + lane * EL, kn);
+    load_bf16_lane<EL>(vb + (int64_t)(p0 + warp) * HD + lane * EL, vn);
+  }
   for (int p = p0 + warp; p < p1; p += kAttnWarps) {
     float kv_[EL], vv[EL];
-    load_bf16_lane<EL>(kb + (int64_t)p * HD + lane * EL, kv_);
+#pragma unroll
+    for (int i = 0; i < EL; ++i) {
+      kv_[i] = kn[i];
+      vv[i] = vn[i];
+    }
+    if (p + kAttnWarps < p1) {
+      load_bf16_lane<EL>(kb + (int64_t)(p + kAttnWarps) * HD + lane * EL, kn);
+      load_bf16_lane<EL>(vb + (int64_t)(p + kAttnWarps) * HD + lane * EL, vn);
+    }
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < EL; ++i) s += qv[i] * kv_[i];
@@ -95,7 +111,6 @@ decode_attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ 
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const float mn = fmaxf(m, s);
     const float corr = __expf(m - mn), ps = __expf(s - mn);
-    load_bf16_lane<EL>(vb + (int64_t)p * HD + lane * EL, vv);
     l = l * corr + ps;
 #pragma unroll
     for (int i = 0; i < EL; ++i) acc[i] = acc[i] * corr + ps * vv[i];
@@ -125,21 +140,38 @@ decode_attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ 
   }
 }
 
+// Split merge.  Every partial of the row is loaded up front (the split count
+// is bounded by kMergeMax) so the merge pays one memory latency instead of one
+// per split; the arithmetic order is unchanged.
+constexpr int kMergeMax = 16;
+
 template <int HD>
 __global__ void attn_merge_kernel(const float* __restrict__ ws, int nsplit,
                                   uint16_t* __restrict__ o) {
   DALI_PDL_ENTRY();
   const int bh = blockIdx.x;
   const float* in = ws + (int64_t)bh * nsplit * (HD + 2);
+  float ms[kMergeMax], ls[kMergeMax];
+#pragma unroll
+  for (int s = 0; s < kMergeMax; ++s) {
+    ms[s] = s < nsplit ? in[s * (HD + 2)] : -INFINITY;
+    ls[s] = s < nsplit ? in[s * (HD + 2) + 1] : 0.f;
+  }
   float M = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, in[s * (HD + 2)]);
+#pragma unroll
+  for (int s = 0; s < kMergeMax; ++s)
+    if (s < nsplit) M = fmaxf(M, ms[s]);
   for (int i = threadIdx.x; i < HD; i += blockDim.x) {
+    float as[kMergeMax];
+#pragma unroll
+    for (int s = 0; s < kMergeMax; ++s) as[s] = s < nsplit ? in[s * (HD + 2) + 2 + i] : 0.f;
     float L = 0.f, A = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float ms = in[s * (HD + 2)];
-      const float c = ms == -INFINITY ? 0.f : __expf(ms - M);
-      L += in[s * (HD + 2) + 1] * c;
-      A += in[s * (HD + 2) + 2 + i] * c;
+#pragma unroll
+    for (int s = 0; s < kMergeMax; ++s) {
+      if (s >= nsplit) break;
+      const float c = ms[s] == -INFINITY ? 0.f : __expf(ms[s] - M);
+      L += ls[s] * c;
+      A += as[s] * c;
     }
     o[(int64_t)bh * HD + i] = f32_to_bf16_bits(A / L);
   }
@@ -165,7 +197,8 @@ extern "C" int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
                                      void* stream) {
   DALI_REQUIRE(hd == 128 || hd == 64, DALI_ETRACE,
                "decode attention kernel supports head_dim 64 or 128, got %d", hd);
-  DALI_REQUIRE(H % KV == 0 && splits >= 1, DALI_ETRACE, "bad attention geometry");
+  DALI_REQUIRE(H % KV == 0 && splits >= 1 && splits <= dali::kMergeMax, DALI_ETRACE,
+               "bad attention geometry (splits %d, at most %d)", splits, dali::kMergeMax);
   cudaStream_t st = dali::as_stream(stream);
   if (hd == 128) {
     dali::launch_pdl(dali::decode_attn_kernel<128>, dim3(dim3(B * H, splits)), dim3(dali::kAttnWarps * 32), 0, st, 
