@@ -171,6 +171,16 @@ int dali_route_bf16(const uint16_t* hidden, const double* residual,
  * last reset) and a test hook scaling the bound (scale < 0: every row takes
  * the fp64 recompute). */
 int dali_route_fire_count(uint64_t* fires, uint64_t* rows, int32_t reset);
+/* dali_route_bf16 (no residual) followed by dali_moe_plan_permute, in ONE
+ * launch for decode-sized batches (T <= 16, T*k + N < 256): the routing
+ * kernel's batch-owning CTA computes the plan and gathers the permuted rows
+ * (derive_workloads + the engine's permute; trace.py:253-265).  Larger
+ * batches run the two as separate launches.  Outputs as the two functions'. */
+int dali_route_plan_bf16(const uint16_t* hidden, const uint16_t* gate, const float* gate_norm2,
+                         int64_t T, int32_t d, int32_t N, int32_t k, int32_t renorm,
+                         int32_t* topk_idx, float* topk_w, int64_t* workloads,
+                         int32_t* offsets, int32_t* perm_token, int32_t* pos, uint16_t* xp,
+                         void* stream);
 int dali_route_guard_scale(double scale);
 
 /* Prefetch-set selection: stable top-P of predicted workloads

@@ -77,6 +77,8 @@ SIGNATURES = {
     "dali_route_bf16": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P],
     "dali_prefetch_select": [_P, _I32, _I32, _P, _P],
     "dali_route_fire_count": [_P, _P, _I32],
+    "dali_route_plan_bf16": [_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P,
+                             _P, _P],
     "dali_route_guard_scale": [C.c_double],
     "dali_greedy": [_P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
     "dali_cost_eval": [_P, _P, _I64, _P, _P, _P],

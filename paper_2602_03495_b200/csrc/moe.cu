@@ -217,24 +217,46 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
                                const float* __restrict__ cpu_rows,
                                const float* __restrict__ extra, int64_t T, int k, int d,
                                int splits, int64_t plane, uint16_t* __restrict__ out) {
-  DALI_PDL_ENTRY();
   // one thread per (token, 8-column chunk): all of a row's chunks load their
-  // k x splits partial rows concurrently (decode: T=1 is latency-bound)
+  // k x splits partial rows concurrently (decode: T=1 is latency-bound).
+  // When the grid covers every item (decode), the routing inputs (top-k ids,
+  // permuted positions, weights, G mask) and the residual row -- all written
+  // by kernels that completed before the predecessor started -- are loaded
+  // before the PDL wait; only the expert outputs (yp, the CPU rows, the
+  // shared-expert rows) wait for the predecessor.
   const int d8 = d >> 3;
   const int64_t items = T * d8;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items; it += stride) {
+  const int64_t it0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int kPreK = 8;                 // top-k held in registers
+  const bool single = items <= stride && k <= kPreK;
+  float g_[kPreK];
+  int64_t r_[kPreK];
+  bool on_[kPreK];
+  uint4 xv0 = make_uint4(0, 0, 0, 0);
+  if (single && it0 < items) {
+    const int64_t t = it0 / d8;
+    const int c = (int)(it0 - t * d8);
+#pragma unroll
+    for (int j = 0; j < kPreK; ++j) {
+      if (j < k) {
+        g_[j] = wts[t * k + j];
+        r_[j] = (int64_t)pos[t * k + j] * d;
+        on_[j] = !mask || mask[idx[t * k + j]];
+      }
+    }
+    xv0 = reinterpret_cast<const uint4*>(x + t * d)[c];
+  }
+  DALI_PDL_ENTRY();
+  for (int64_t it = it0; it < items; it += stride) {
     const int64_t t = it / d8;
     const int c = (int)(it - t * d8);
     {
       float acc[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-      for (int j = 0; j < k; ++j) {
-        const bool on_gpu = !mask || mask[idx[t * k + j]];
-        if (!on_gpu && !cpu_rows) continue;
-        const float g = wts[t * k + j];
-        const int64_t r = (int64_t)pos[t * k + j] * d;
+      auto add_row = [&](bool on_gpu, float g, int64_t r) {
+        if (!on_gpu && !cpu_rows) return;
         float4 a, b;
         if (on_gpu) {
           const float4* src = reinterpret_cast<const float4*>(yp + r) + 2 * c;
@@ -255,6 +277,14 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
         acc[2] = fmaf(g, a.z, acc[2]); acc[3] = fmaf(g, a.w, acc[3]);
         acc[4] = fmaf(g, b.x, acc[4]); acc[5] = fmaf(g, b.y, acc[5]);
         acc[6] = fmaf(g, b.z, acc[6]); acc[7] = fmaf(g, b.w, acc[7]);
+      };
+      if (single) {
+#pragma unroll
+        for (int j = 0; j < kPreK; ++j)
+          if (j < k) add_row(on_[j], g_[j], r_[j]);
+      } else {
+        for (int j = 0; j < k; ++j)
+          add_row(!mask || mask[idx[t * k + j]], wts[t * k + j], (int64_t)pos[t * k + j] * d);
       }
       if (extra) {
         const float4* ex = reinterpret_cast<const float4*>(extra + t * d) + 2 * c;
@@ -262,7 +292,7 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
         acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
         acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
       }
-      const uint4 xv = reinterpret_cast<const uint4*>(x + t * d)[c];
+      const uint4 xv = single ? xv0 : reinterpret_cast<const uint4*>(x + t * d)[c];
       const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xv);
       uint4 ov;
       uint32_t* ow = reinterpret_cast<uint32_t*>(&ov);

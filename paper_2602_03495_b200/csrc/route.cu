@@ -244,7 +244,8 @@ namespace dali {
 int launch_route_guarded(const uint16_t* hidden, const double* residual, const uint16_t* gate,
                          const float* wn2, int64_t T, int d, int N, int k, int renorm,
                          int32_t* idx, float* w, int64_t* workloads, void* stream,
-                         int* launched);
+                         int* launched, const int32_t* const* plan_ptrs = nullptr,
+                         uint16_t* plan_xp = nullptr);
 }
 
 // bf16 engine path: the fp32 certified-margin kernel (route_guard.cu) for
@@ -265,6 +266,34 @@ extern "C" int dali_route_bf16(const uint16_t* hidden, const double* residual,
   if (rc != DALI_OK || launched) return rc;
   return dali::launch_route<uint16_t, uint16_t>(hidden, residual, gate, T, d, N, k, renorm,
                                                 topk_idx, topk_w, workloads, stream);
+}
+
+// Routing + plan + permute in one launch for decode-sized batches (T <= 16,
+// T*k + N < 256): the certified routing kernel's batch-owning CTA also does
+// dali_moe_plan_permute's work; otherwise the two run as separate launches.
+extern "C" int dali_route_plan_bf16(const uint16_t* hidden, const uint16_t* gate,
+                                    const float* gate_norm2, int64_t T, int32_t d, int32_t N,
+                                    int32_t k, int32_t renorm, int32_t* topk_idx, float* topk_w,
+                                    int64_t* workloads, int32_t* offsets, int32_t* perm_token,
+                                    int32_t* pos, uint16_t* xp, void* stream) {
+  DALI_REQUIRE(N >= 1 && N <= DALI_MAX_EXPERTS, DALI_ETRACE,
+               "num experts %d outside [1, %d]", N, DALI_MAX_EXPERTS);
+  DALI_REQUIRE(k >= 1 && k <= N, DALI_ETRACE, "top_k %d out of range for %d experts", k, N);
+  DALI_REQUIRE(workloads && topk_idx && offsets && perm_token && pos && xp, DALI_ETRACE,
+               "route+plan needs every output");
+  const int32_t* plan[3] = {offsets, perm_token, pos};
+  int launched = 0;
+  int rc = dali::launch_route_guarded(hidden, nullptr, gate, gate_norm2, T, d, N, k, renorm,
+                                      topk_idx, topk_w, workloads, stream, &launched, plan, xp);
+  if (rc != DALI_OK) return rc;
+  if (!launched) {
+    rc = dali_route_bf16(hidden, nullptr, gate, gate_norm2, T, d, N, k, renorm, topk_idx, topk_w,
+                         workloads, stream);
+    if (rc != DALI_OK) return rc;
+    return dali_moe_plan_permute(topk_idx, T, k, N, hidden, d, offsets, perm_token, pos, xp,
+                                 stream);
+  }
+  return DALI_OK;
 }
 
 extern "C" int dali_prefetch_select(const int64_t* predicted, int32_t N, int32_t P,

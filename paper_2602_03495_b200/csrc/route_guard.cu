@@ -397,13 +397,63 @@ __device__ void rank_tail(const float* zl, int NP, const float* xn, const float*
   __syncthreads();
 }
 
+// Decode-sized batches: the routing plan and the permute of dali_moe_plan_permute
+// (moe.cu plan_kernel: a stable counting sort of the T*k (token, slot) pairs
+// by expert, then the 128-bit gather of the permuted rows) done by the CTA
+// that owns the whole batch, right after its top-k -- one launch fewer on the
+// decode critical path.  Same outputs: offsets (N+1), perm_token (T*k), pos
+// (T, k), xp (T*k, d).
+struct PlanOut {
+  int32_t* offsets;
+  int32_t* perm;
+  int32_t* pos;
+  uint16_t* xp;
+};
+
+__device__ void plan_gather(const PlanOut& plan, const int32_t* topk_idx,
+                            const uint16_t* __restrict__ hidden, int T, int k, int N, int d,
+                            const int* hist, int* scratch /* >= N + 1 + 256 ints */) {
+  const int tid = threadIdx.x;
+  const int R = T * k;
+  int* offs = scratch;                     // N + 1
+  int* perm = scratch + N + 1;             // R <= 256 - N - 1 by the host's guard
+  if (tid == 0) {
+    int run = 0;
+    for (int e = 0; e < N; ++e) {
+      offs[e] = run;
+      run += hist[e];
+    }
+    offs[N] = run;
+  }
+  __syncthreads();                          // topk_idx rows written by this CTA are visible
+  for (int e = tid; e <= N; e += kThreads) plan.offsets[e] = offs[e];
+  for (int p = tid; p < R; p += kThreads) {
+    const int e = topk_idx[p];
+    int before = 0;                          // earlier pairs routed to the same expert
+    for (int q = 0; q < p; ++q) before += topk_idx[q] == e;
+    const int row = offs[e] + before;
+    plan.pos[p] = row;
+    plan.perm[row] = p / k;
+    perm[row] = p / k;
+  }
+  __syncthreads();
+  const int d8 = d >> 3;
+  const uint4* src = reinterpret_cast<const uint4*>(hidden);
+  uint4* dst = reinterpret_cast<uint4*>(plan.xp);
+  for (int u = tid; u < R * d8; u += kThreads) {
+    const int row = u / d8, c = u - row * d8;
+    dst[u] = src[(int64_t)perm[row] * d8 + c];
+  }
+}
+
 template <int TB, int C>
 __global__ void __launch_bounds__(kThreads)
 route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict__ residual,
                    const uint16_t* __restrict__ gate, int64_t T, int d, int N, int k,
                    int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
                    unsigned long long* __restrict__ workloads,
-                   const float* __restrict__ wnorm2, Geo g, float gamma, int force_fp64) {
+                   const float* __restrict__ wnorm2, Geo g, float gamma, int force_fp64,
+                   PlanOut plan) {
   RG_MARK(0);
   constexpr int TG = TB / 4;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -669,6 +719,7 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
       else if (sh_hist[i]) atomicAdd(workloads + i, (unsigned long long)sh_hist[i]);
     }
   }
+  if (plan.offsets) plan_gather(plan, topk_idx, hidden, tb_n, k, N, d, sh_hist, sh_cl);
 }
 
 static int ilog2(int x) { int r = 0; while ((1 << (r + 1)) <= x) ++r; return r; }
@@ -709,7 +760,8 @@ static double s_guard_scale = 1.0;          // test hook: < 0 forces every row t
 template <int TB, int C>
 static int launch_tb(const uint16_t* hidden, const double* residual, const uint16_t* gate,
                      int64_t T, int d, int N, int k, int renorm, int32_t* idx, float* w,
-                     unsigned long long* wl, const float* wn2, cudaStream_t st, const Geo& g) {
+                     unsigned long long* wl, const float* wn2, cudaStream_t st, const Geo& g,
+                     PlanOut plan = PlanOut{nullptr, nullptr, nullptr, nullptr}) {
   const size_t sm = smem_bytes(g);
   DALI_ONCE_PER_DEVICE(cudaFuncSetAttribute(route_guard_kernel<TB, C>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -742,7 +794,7 @@ static int launch_tb(const uint16_t* hidden, const double* residual, const uint1
   cfg.attrs = attrs;
   cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, route_guard_kernel<TB, C>, hidden, residual, gate, T, d, N, k, renorm,
-                     idx, w, wl, wn2, g, (float)gam, force);
+                     idx, w, wl, wn2, g, (float)gam, force, plan);
   DALI_LAUNCH_CHECK("route_guard_kernel");
   return DALI_OK;
 }
@@ -754,8 +806,16 @@ static int launch_tb(const uint16_t* hidden, const double* residual, const uint1
 int launch_route_guarded(const uint16_t* hidden, const double* residual, const uint16_t* gate,
                          const float* wn2, int64_t T, int d, int N, int k, int renorm,
                          int32_t* idx, float* w, int64_t* workloads, void* stream,
-                         int* launched) {
+                         int* launched, const int32_t* const* plan_ptrs, uint16_t* plan_xp) {
   using namespace rg;
+  PlanOut plan{nullptr, nullptr, nullptr, nullptr};
+  if (plan_ptrs) {
+    // only the single-CTA-owner shape (T <= 16) plans in-kernel, and only
+    // when the pairs fit the scratch; the caller plans separately otherwise
+    if (T > 16 || idx == nullptr || T * k + N + 1 > 256 || (d & 7)) return DALI_OK;
+    plan = PlanOut{const_cast<int32_t*>(plan_ptrs[0]), const_cast<int32_t*>(plan_ptrs[1]),
+                   const_cast<int32_t*>(plan_ptrs[2]), plan_xp};
+  }
   *launched = 0;
   // d <= 8000: the fp64 recompute stages one row (d doubles) in the 72 KB ring
   if (wn2 == nullptr || d > 8000 || N < 4 || N > 256 || (N & 3) || (d & 7) || k > DALI_MAX_TOPK || k > N || T <= 0)
@@ -770,10 +830,10 @@ int launch_route_guarded(const uint16_t* hidden, const double* residual, const u
     const Geo g = make_geo(TB, N, C, d);
     if (g.S < 1 || smem_bytes(g) > 180 * 1024 || (size_t)TB * g.NP > 4096) return DALI_OK;
 #define DALI_RG_SMALL(TBv)                                                              \
-  (C == 8 ? launch_tb<TBv, 8>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g) \
-   : C == 4 ? launch_tb<TBv, 4>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g) \
-   : C == 2 ? launch_tb<TBv, 2>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g) \
-            : launch_tb<TBv, 1>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g))
+  (C == 8 ? launch_tb<TBv, 8>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g, plan) \
+   : C == 4 ? launch_tb<TBv, 4>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g, plan) \
+   : C == 2 ? launch_tb<TBv, 2>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g, plan) \
+            : launch_tb<TBv, 1>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g, plan))
     rc = TB == 4 ? DALI_RG_SMALL(4) : TB == 8 ? DALI_RG_SMALL(8) : DALI_RG_SMALL(16);
 #undef DALI_RG_SMALL
   } else {

@@ -106,14 +106,22 @@ class MoEExecMixin:
             "idx": rblk[o_idx:o_w].view(torch.int32).view(T, k),
             "wts": rblk[o_w:nb].view(torch.float32).view(T, k),
         }
-        route_device(h, self.w.router[l], k, renorm=a.norm_topk_prob,
-                     out=(v["idx"], v["wts"], v["wl"]), norm2=self.w.router_norm2[l])
         perm = self._ws("perm", (T * k,), torch.int32)
         v["pos"] = self._ws("pos", (T, k), torch.int32)
         v["xp"] = self._ws("xp", (T * k, d), torch.bfloat16)
-        _lib.call("dali_moe_plan_permute", v["idx"].data_ptr(), T, k, N, h.data_ptr(), d,
-                  v["offsets"].data_ptr(), perm.data_ptr(), v["pos"].data_ptr(),
-                  v["xp"].data_ptr(), cs.cuda_stream)
+        if T <= 16 and self.cfg.fused_route_plan:
+            # decode: routing, plan and permute in one launch
+            _lib.call("dali_route_plan_bf16", h.data_ptr(), self.w.router[l].data_ptr(),
+                      self.w.router_norm2[l].data_ptr(), T, d, N, k, int(a.norm_topk_prob),
+                      v["idx"].data_ptr(), v["wts"].data_ptr(), v["wl"].data_ptr(),
+                      v["offsets"].data_ptr(), perm.data_ptr(), v["pos"].data_ptr(),
+                      v["xp"].data_ptr(), cs.cuda_stream)
+        else:
+            route_device(h, self.w.router[l], k, renorm=a.norm_topk_prob,
+                         out=(v["idx"], v["wts"], v["wl"]), norm2=self.w.router_norm2[l])
+            _lib.call("dali_moe_plan_permute", v["idx"].data_ptr(), T, k, N, h.data_ptr(), d,
+                      v["offsets"].data_ptr(), perm.data_ptr(), v["pos"].data_ptr(),
+                      v["xp"].data_ptr(), cs.cuda_stream)
         v["blk"], v["layout"], v["perm"] = rblk, (o_off, o_idx, o_w, nb), perm
         return v
 

@@ -80,6 +80,9 @@ class EngineConfig:
     ep_transport: str = "p2p"               # expert parallelism: "p2p" (peer-memory kernels,
     #                                         csrc/ep.cu) or "nccl" (all_to_all baseline)
     trace_layers: bool = False              # per-layer host/device timeline (tools/decode_timeline.py)
+    fused_route_plan: bool = os.environ.get("DALI_FUSED_ROUTE_PLAN", "1") != "0"
+    #                                         decode (T <= 16): routing + plan + permute in
+    #                                         one launch (dali_route_plan_bf16)
     fused_norm_gemv: bool = os.environ.get("DALI_FUSED_NORM", "1") != "0"
     #                                         decode (B <= 8): attention-block RMSNorms fused
     #                                         into the qkv / o projection GEMVs

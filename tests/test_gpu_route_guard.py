@@ -137,3 +137,43 @@ def test_fire_rate_on_realistic_inputs(lib):
         fires, rows = lib.route_fire_count(reset=True)
         assert rows == 2048
         assert fires < 0.05 * rows, (d, N, fires)
+
+
+@pytest.mark.parametrize("d,N,k", [(4096, 8, 2), (2048, 64, 6), (2048, 60, 4), (256, 8, 2)])
+@pytest.mark.parametrize("force", [False, True])
+def test_route_plan_fused_matches_separate(lib, d, N, k, force):
+    """dali_route_plan_bf16 (routing, plan and permute in one launch for
+    decode batches) == dali_route_bf16 + dali_moe_plan_permute, every output
+    bit for bit, for T = 1..16 and the separate-launch fallback (T = 17, 33);
+    force=True sends every row through the fp64 recompute first."""
+    import torch
+    from paper_2602_03495_b200.trace import gate_norm2
+    lib.call("dali_route_guard_scale", -1.0 if force else 1.0)
+    try:
+        for T in (1, 2, 3, 5, 8, 16, 17, 33):
+            h, w = _inputs(T, d, N, seed=T * 13 + N)
+            h, w = h.cuda(), w.cuda()
+            n2 = gate_norm2(w)
+            sp = torch.cuda.current_stream().cuda_stream
+
+            def outs():
+                return (torch.full((T, k), -7, dtype=torch.int32, device="cuda"),
+                        torch.zeros((T, k), dtype=torch.float32, device="cuda"),
+                        torch.zeros((N,), dtype=torch.int64, device="cuda"),
+                        torch.full((N + 1,), -7, dtype=torch.int32, device="cuda"),
+                        torch.full((T * k,), -7, dtype=torch.int32, device="cuda"),
+                        torch.full((T, k), -7, dtype=torch.int32, device="cuda"),
+                        torch.zeros((T * k, d), dtype=torch.bfloat16, device="cuda"))
+            a = outs()
+            lib.call("dali_route_bf16", h.data_ptr(), None, w.data_ptr(), n2.data_ptr(), T, d, N,
+                     k, 1, a[0].data_ptr(), a[1].data_ptr(), a[2].data_ptr(), sp)
+            lib.call("dali_moe_plan_permute", a[0].data_ptr(), T, k, N, h.data_ptr(), d,
+                     a[3].data_ptr(), a[4].data_ptr(), a[5].data_ptr(), a[6].data_ptr(), sp)
+            b = outs()
+            lib.call("dali_route_plan_bf16", h.data_ptr(), w.data_ptr(), n2.data_ptr(), T, d, N,
+                     k, 1, *[t.data_ptr() for t in b], sp)
+            torch.cuda.synchronize()
+            for x_, y_ in zip(a, b):
+                assert torch.equal(x_, y_), (T, d, N, k)
+    finally:
+        lib.call("dali_route_guard_scale", 1.0)
