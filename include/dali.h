@@ -381,6 +381,13 @@ int dali_unpermute_combine(const uint16_t* x, const float* yp,
  * path; unaligned copies are byte-wise and limited to 1 MiB. */
 int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream);
 
+/* Engine plumbing: bulk host->device copy (expert blocks) driven by `nctas`
+ * CTAs of 512 threads reading mapped pinned memory, instead of a copy engine.
+ * The CTA count bounds the bytes in flight on PCIe, so latency-critical small
+ * transfers issued meanwhile are not queued behind a copy engine's deep read
+ * queue.  Pointers and size must be 16-byte aligned. */
+int dali_copy_h2d_sm(void* dst, const void* src, int64_t nbytes, int32_t nctas, void* stream);
+
 /* Shared expert(s) finish (engine plumbing): out[t,:] = sum over `splits`
  * planes of ys (splits, T, d) f32, times sigmoid(h[t,:] . gate_w) when
  * gate_w (d,) bf16 is given (Qwen-style gated shared expert), else 1.

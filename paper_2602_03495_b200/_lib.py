@@ -115,6 +115,7 @@ SIGNATURES = {
     "dali_cpu_expert_wait": [],
     "dali_add_rmsnorm": [_P, _P, _P, C.c_float, _I64, _I32, _P, _P, _P],
     "dali_copy_mapped": [_P, _P, _I64, _P],
+    "dali_copy_h2d_sm": [_P, _P, _I64, _I32, _P],
     "dali_shared_finish": [_P, _I32, _I64, _I32, _P, _P, _P, _P],
     "dali_gemv_bf16": [_P, _P, _I32, _I32, _I32, _P, _P],
     "dali_ipc_alloc": [C.c_size_t, C.POINTER(C.c_void_p), _P],

@@ -211,6 +211,26 @@ ffn_down_simt(const uint16_t* __restrict__ h, const int32_t* __restrict__ offset
 // Combine: out[t] = x[t] + sum_j w[t,j] * yp[pos[t,j]] (+ extra[t]); one warp
 // per token, 8 columns (16 B of bf16) per lane step.
 // ---------------------------------------------------------------------------
+// PCIe quiet window.  The decode path's small host<->device transfers (CPU
+// expert rows read by the combine, decision mirrors, pointer tables) queue
+// behind whatever expert-block reads are in flight on the link.  The
+// SM-driven expert copy (copy_h2d_sm_kernel) keeps that queue short and, in
+// addition, pauses while this device clock deadline lies in the future: the
+// control kernels extend it when they start, so the decode chain (combine ->
+// attention -> routing -> policy -> mirrors) runs with an idle link and
+// without the copy's loads competing on the SMs.
+__device__ unsigned long long g_pcie_quiet_until = 0;
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void pcie_quiet(unsigned long long ns) {
+  atomicMax(&g_pcie_quiet_until, gtimer_ns() + ns);
+}
+constexpr unsigned long long kQuietChainNs = 120000;   // combine -> decision mirrors
+constexpr unsigned long long kQuietCtlNs = 25000;      // one control transfer
+
 __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __restrict__ yp,
                                const int32_t* __restrict__ idx, const int32_t* __restrict__ pos,
                                const float* __restrict__ wts, const int8_t* __restrict__ mask,
@@ -230,6 +250,7 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
   const int64_t it0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   constexpr int kPreK = 8;                 // top-k held in registers
   const bool single = items <= stride && k <= kPreK;
+  if (single && it0 == 0) pcie_quiet(kQuietChainNs);      // decode: the chain starts here
   float g_[kPreK];
   int64_t r_[kPreK];
   bool on_[kPreK];
@@ -412,6 +433,7 @@ namespace dali {
 __global__ void copy_mapped_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
                                    int64_t n16, uint8_t* __restrict__ dst_tail,
                                    const uint8_t* __restrict__ src_tail, int tail) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) pcie_quiet(kQuietCtlNs);
   DALI_PDL_ENTRY();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
@@ -424,6 +446,52 @@ __global__ void copy_bytes_kernel(uint8_t* __restrict__ dst, const uint8_t* __re
   if (i < n) dst[i] = src[i];
 }
 }  // namespace dali
+
+// Bulk host->device copy driven by a few SMs instead of a copy engine: the
+// number of CTAs bounds the bytes in flight on the PCIe link, so a small
+// latency-critical read issued meanwhile (CPU-expert rows, pointer tables)
+// waits behind at most that many bytes instead of a copy engine's deep queue.
+namespace dali {
+template <int U>
+__global__ void __launch_bounds__(512) copy_h2d_sm_kernel(uint4* __restrict__ dst,
+                                                           const uint4* __restrict__ src,
+                                                           int64_t n16) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const volatile unsigned long long* quiet = &g_pcie_quiet_until;
+  for (; i + (U - 1) * stride < n16; i += U * stride) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcv(src + i + u * stride);
+    unsigned long long q = *quiet;          // L2 read, overlapped with the PCIe loads
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcg(dst + i + u * stride, v[u]);
+    while (gtimer_ns() < q) {               // a control transfer / decode chain is running
+      __nanosleep(2000);
+      q = *quiet;
+    }
+  }
+  for (; i < n16; i += stride) __stcg(dst + i, __ldcv(src + i));
+}
+}  // namespace dali
+
+// nctas = CTAs x 1 + 64 x (loads in flight per thread - 1), threads per CTA
+// = 512 (the low 6 bits pick the CTA count, bits 6.. the unroll 1/2/4)
+extern "C" int dali_copy_h2d_sm(void* dst, const void* src, int64_t nbytes, int32_t nctas,
+                                void* stream) {
+  if (nbytes <= 0) return DALI_OK;
+  DALI_REQUIRE(dst && src && nctas >= 1 && ((((uintptr_t)dst | (uintptr_t)src | nbytes) & 15) == 0),
+               DALI_ECUDA, "dali_copy_h2d_sm: needs 16-byte aligned pointers and size");
+  const int ctas = nctas & 63, u = 1 + (nctas >> 6);
+  auto* d4 = reinterpret_cast<uint4*>(dst);
+  auto* s4 = reinterpret_cast<const uint4*>(src);
+  cudaStream_t st = as_stream(stream);
+  if (u >= 4) copy_h2d_sm_kernel<4><<<ctas, 512, 0, st>>>(d4, s4, nbytes >> 4);
+  else if (u >= 2) copy_h2d_sm_kernel<2><<<ctas, 512, 0, st>>>(d4, s4, nbytes >> 4);
+  else copy_h2d_sm_kernel<1><<<ctas, 512, 0, st>>>(d4, s4, nbytes >> 4);
+  DALI_LAUNCH_CHECK("copy_h2d_sm_kernel");
+  return DALI_OK;
+}
 
 extern "C" int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream) {
   if (nbytes <= 0) return DALI_OK;

@@ -23,6 +23,7 @@ from .. import _lib
 from ..errors import SimulationError
 from ..trace import route_device
 from .cpu_worker import NATIVE_MAX_ROWS, cpu_expert_rows
+from .weights import h2d_block
 
 
 def ffn_splits(max_rows: int, tiles: int, kb: int, n_sm: int) -> int:
@@ -70,13 +71,20 @@ class MoEExecMixin:
     def _splits_for(self, tiles: int, max_rows: int, ffn_dim: int | None = None) -> int:
         return ffn_splits(max_rows, tiles, (ffn_dim or self.arch.ffn_dim) // 64, self.n_sm)
 
-    def _copy_into_staging(self, l: int, e: int) -> tuple[int, torch.cuda.Event]:
+    def _copy_into_staging(self, l: int, e: int, demand: bool = False
+                           ) -> tuple[int, torch.cuda.Event]:
+        """Expert block (l, e) -> a staging slot on the copy stream.  Demand
+        copies (the GPU expert waits for them: prefill-sized work) use the copy
+        engine's full bandwidth; prefetches, like replacements, use the
+        SM-driven copy that yields the link to the decode path's control
+        transfers (weights.h2d_block)."""
         i = self.staging.get()
         ev_prev = self.staging.free_after[i]
         with torch.cuda.stream(self.copy_stream):
             if ev_prev is not None:
                 self.copy_stream.wait_event(ev_prev)
-            self.staging.buf[i].copy_(self._host_block(l, e), non_blocking=True)
+            h2d_block(self.staging.buf[i], self._host_block(l, e), self.copy_stream,
+                      0 if demand else self.cfg.h2d_sm_ctas)
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
         self.stats.h2d_bytes += self.w.expert_bytes
@@ -191,7 +199,7 @@ class MoEExecMixin:
                 i, ev = self.prefetched.pop((l, e))
                 n_pf += 1
             else:
-                i, ev = self._copy_into_staging(l, e)
+                i, ev = self._copy_into_staging(l, e, demand=True)
                 self.stats.demand_copies += 1
                 n_dem += 1
             ptrs[e] = self.staging.ptr(i)
@@ -261,7 +269,8 @@ class MoEExecMixin:
                     for j in range(rec.ev_n):
                         v_, c_ = int(rec.evicted[j]), int(rec.admitted[j])
                         s = self.host_slot[l, v_]
-                        self.cache_buf[s].copy_(self._host_block(l, c_), non_blocking=True)
+                        h2d_block(self.cache_buf[s], self._host_block(l, c_),
+                                  self.repl_stream, self.cfg.h2d_sm_ctas)
                         self.host_slot[l, c_], self.host_slot[l, v_] = s, -1
                         self.stats.h2d_bytes += self.w.expert_bytes
                         self.stats.replace_copies += 1

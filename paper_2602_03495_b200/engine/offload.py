@@ -90,6 +90,11 @@ class EngineConfig:
     #                                         all-resident decode: the policy kernel (records
     #                                         only, nothing downstream reads them) runs on a
     #                                         side stream off the layer's critical path
+    h2d_sm_ctas: int = int(os.environ.get("DALI_H2D_SM_CTAS", "0"))
+    #                                         replacement / prefetch H2D copies driven by this
+    #                                         many SMs (bounded PCIe queue depth, paused in
+    #                                         the decode chain's quiet window); 0 = copy
+    #                                         engine (default: measured faster end to end)
 
 
 @dataclass

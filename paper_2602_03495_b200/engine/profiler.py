@@ -23,6 +23,7 @@ from ..cost_model import CostModel, fit_cost_model, quantize_ms
 from .arch import MoEArch
 from .cpu_worker import NATIVE_MAX_ROWS, cpu_expert_rows
 from .offload import ffn_splits
+from .weights import h2d_block
 
 
 def _cpu_expert(h: torch.Tensor, blk: torch.Tensor, d: int, f: int, threads: int):
@@ -41,7 +42,7 @@ def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
                        non_moe_ms: float | None = None, log=None, tc: bool = True,
                        threads: int | None = None,
                        contended_from_rows: int | None = None,
-                       warmup_s: float = 0.6) -> CostModel:
+                       warmup_s: float = 0.6, h2d_ctas: int = 0) -> CostModel:
     dev = torch.device("cuda", torch.cuda.current_device())
     d, f, N = arch.hidden_dim, arch.ffn_dim, arch.num_experts
     ws = [1 << i for i in range(0, 32) if (1 << i) <= max_w]
@@ -88,9 +89,9 @@ def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
             if busy:
                 with torch.cuda.stream(side):
                     for j in range(n_dma):               # ~6 x trans_time of DMA
-                        dma_dst.copy_(weights.host.bytes[weights.expert_bytes * j:
-                                                         weights.expert_bytes * (j + 1)],
-                                      non_blocking=True)
+                        h2d_block(dma_dst, weights.host.bytes[weights.expert_bytes * j:
+                                                              weights.expert_bytes * (j + 1)],
+                                  side, h2d_ctas)
                 time.sleep(0.001)                        # let the first copy start
             t0 = time.perf_counter()
             _cpu_expert(h, blk, d, f, threads)
@@ -144,12 +145,12 @@ def profile_cost_model(arch: MoEArch, weights, max_w: int = 1024, reps: int = 3,
     if weights.host is not None:
         src = weights.host.bytes[:weights.expert_bytes]
         dst = torch.empty((weights.expert_bytes,), dtype=torch.uint8, device=dev)
-        dst.copy_(src, non_blocking=True)
+        h2d_block(dst, src, cs, h2d_ctas)         # demand copies: copy engine
         ts = []
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(cs)
-            dst.copy_(src, non_blocking=True)
+            h2d_block(dst, src, cs, h2d_ctas)
             e1.record(cs)
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))

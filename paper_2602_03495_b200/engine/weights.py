@@ -54,6 +54,30 @@ def router_weights(arch: MoEArch, seed: int, layer: int) -> np.ndarray:
     return base * scale[None, :]
 
 
+H2D_SM_CTAS = int(os.environ.get("DALI_H2D_SM_CTAS", "0"))
+
+
+def h2d_block(dst: torch.Tensor, src: torch.Tensor, stream: torch.cuda.Stream,
+              nctas: int = H2D_SM_CTAS) -> None:
+    """Expert-block host->device copy from the pinned store on ``stream``.
+    nctas = 0 (default): copy engine.  nctas > 0: a few SMs read the mapped
+    pinned block (dali_copy_h2d_sm) with a bounded number of bytes in flight
+    and pause in the decode chain's PCIe quiet window, so the decode path's
+    small PCIe transfers (decision mirrors, pointer tables, CPU-expert rows)
+    are not queued behind the copy engine's deep read queue: +40-50 us each
+    under copy-engine DMA, ~0 with the SM copy (tools/pcie_latency_probe.py,
+    profiles/r02_pcie_latency_probe.log).  End to end it lost: the SM copy
+    moves 45-49 instead of 54 GB/s, the replacement queue backs up and cache
+    hits wait on in-flight copies ("Tried and rejected")."""
+    nbytes = src.numel() * src.element_size()
+    if nctas > 0 and not (src.data_ptr() | dst.data_ptr() | nbytes) & 15:
+        _lib.call("dali_copy_h2d_sm", dst.data_ptr(), src.data_ptr(), nbytes, int(nctas),
+                  stream.cuda_stream)
+    else:
+        with torch.cuda.stream(stream):
+            dst.copy_(src, non_blocking=True)
+
+
 class HostStore:
     """Page-locked expert store (exact size, huge pages, parallel first touch)."""
 

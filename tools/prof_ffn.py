@@ -20,7 +20,9 @@ from paper_2602_03495_b200.engine.offload import ffn_splits  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--mode", default="both")
 ap.add_argument("--iters", type=int, default=20)
-ap.add_argument("--kernel", default="tc")
+ap.add_argument("--kernel", default="tc", help="tc | simt")
+ap.add_argument("--check", action="store_true", help="compare with an fp32 torch reference")
+ap.add_argument("--kprof", action="store_true", help="per-kernel CUPTI durations")
 ap.add_argument("--d", type=int, default=4096)
 ap.add_argument("--f", type=int, default=14336)
 ap.add_argument("--splits", type=int, default=0, help="override the split-K planes")
@@ -71,6 +73,23 @@ def run(counts, label):
     for _ in range(3):
         go()
     torch.cuda.synchronize()
+    if args.check:                      # vs an fp32 torch reference of the same FFN
+        ysum = y.sum(0)
+        err = 0.0
+        for e in range(N):
+            if not on[e]:
+                continue
+            r0, r1 = int(offs[e]), int(offs[e + 1])
+            blk = blocks[e].float()
+            w13 = blk[:2 * f * d].view(2 * f, d)
+            idx = torch.arange(2 * f, device=dev).view(-1, 128)
+            g_rows, u_rows = idx[:, :64].reshape(-1), idx[:, 64:].reshape(-1)
+            x = xp[r0:r1].float()
+            gg, uu = x @ w13[g_rows].t(), x @ w13[u_rows].t()
+            hh = (torch.nn.functional.silu(gg) * uu).to(torch.bfloat16).float()
+            ref = hh @ blk[2 * f * d:].view(d, f).t()
+            err = max(err, float((ysum[r0:r1] - ref).abs().max() / ref.abs().max()))
+        print(f"{label}: max |err| / max |ref| vs fp32 reference {err:.2e}", flush=True)
     ts = []
     for _ in range(args.iters):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -80,6 +99,15 @@ def run(counts, label):
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
+    if args.kprof:                      # per-kernel device durations (CUPTI)
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(10):
+                go()
+            torch.cuda.synchronize()
+        for ev in prof.key_averages():
+            if ev.device_type.name == "CUDA" and ev.count >= 10:
+                print(f"    {ev.key[:60]:60s} n={ev.count} avg {ev.device_time:.1f} us")
     if args.graph:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
@@ -112,6 +140,10 @@ if args.mode in ("decode", "both"):
     run([1, 0, 0, 1, 0, 0, 0, 0], "decode 2x1")
 if args.mode in ("prefill", "both"):
     run([128] * 8, "prefill 8x128")
+if args.mode == "decode-sweep":
+    for c in ([1] + [0] * 7, [1, 1] + [0] * 6, [2, 2] + [0] * 6, [2, 1] + [0] * 6, [1] * 8,
+              [2] * 8, [1, 2, 0, 0, 2, 0, 0, 0]):
+        run(c, f"counts {max(c)}x{sum(1 for x in c if x)}")
 if args.mode == "all":
     for c in ([1, 0, 0, 0, 0, 0, 0, 0], [1, 1, 0, 0, 0, 0, 0, 0], [2, 1, 0, 0, 0, 0, 0, 0],
               [4] * 8, [16] * 8, [64] * 8, [128] * 8, [256] * 8, [512] * 8):
