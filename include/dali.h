@@ -374,6 +374,21 @@ int dali_unpermute_combine(const uint16_t* x, const float* yp,
                            int32_t k, int32_t d, int32_t splits, int64_t rows,
                            uint16_t* out, void* stream);
 
+/* Same as dali_unpermute_combine, launchable before the host worker has
+ * produced the CPU experts' rows: every CTA first waits until the mapped
+ * pinned word *rows_ready (stored by the worker's last unit, see
+ * dali_cpu_submit_layer) is >= rows_want.  rows_ready NULL = no wait.  The
+ * wait is bounded (4 s of device time; dali_host_wait_timeouts counts
+ * expiries).  CPU rows are read with ld.global.cv (never a stale L2 line). */
+int dali_unpermute_combine_wait(const uint16_t* x, const float* yp,
+                                const int32_t* topk_idx, const int32_t* pos,
+                                const float* topk_w, const int8_t* gpu_mask,
+                                const float* cpu_rows, const float* extra, int64_t T,
+                                int32_t k, int32_t d, int32_t splits, int64_t rows,
+                                uint16_t* out, const uint64_t* rows_ready,
+                                uint64_t rows_want, void* stream);
+int dali_host_wait_timeouts(uint64_t* out, int32_t reset);
+
 /* Engine plumbing: copy nbytes between UVA addresses (device memory and/or
  * mapped pinned host memory, either direction) with a kernel instead of a
  * copy engine, so small per-layer control transfers and per-token reads never
@@ -507,6 +522,21 @@ int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const uint64_t* xs
                            const int32_t* rows, const uint64_t* ys, int32_t d,
                            int32_t f, int32_t nthreads);
 int dali_cpu_expert_wait(void);
+
+/* One decode layer's CPU experts in one call (engine hot path): the experts e
+ * with C[e] != 0 (the decision record's C vector) and rows offsets[e] ..
+ * offsets[e+1] of the permuted activations xp (R, d) bf16 are started on the
+ * worker pool, results into out (R, d) f32 (rows of other experts untouched).
+ * blocks (N,) = host address of each expert's weight block.  When the job's
+ * last work unit finishes (at once if there is none), done_value is stored
+ * to *done_flag (release) -- the word dali_unpermute_combine_wait polls.
+ * *n_experts = experts started, or -1 if an expert has more than 16 rows
+ * (nothing started, flag untouched: prefill-sized work goes through
+ * dali_cpu_expert).  Join with dali_cpu_expert_wait. */
+int dali_cpu_submit_layer(const int8_t* C, const int32_t* offsets, int32_t N,
+                          const uint64_t* blocks, const uint16_t* xp, float* out,
+                          int32_t d, int32_t f, int32_t nthreads, uint64_t* done_flag,
+                          uint64_t done_value, int32_t* n_experts);
 
 /* Deterministic counter-hash weight init (uniform, given std):
  * out[i] = bf16(std * sqrt(3) * (2*u(seed, offset+i) - 1)). */

@@ -97,6 +97,10 @@ SIGNATURES = {
     "dali_expert_ffn_simt": [_P, _P, _I32, _P, _I32, _I32, _P, _P, _P],
     "dali_unpermute_combine": [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I64, _P,
                                _P],
+    "dali_unpermute_combine_wait": [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I64,
+                                    _P, _P, C.c_uint64, _P],
+    "dali_host_wait_timeouts": [_P, _I32],
+    "dali_cpu_submit_layer": [_P, _P, _I32, _P, _P, _P, _I32, _I32, _I32, _P, C.c_uint64, _P],
     "dali_expert_ffn_tc": [_P, _P, _I32, _P, _I32, _I32, _I64, _I32, _I32, _P, _P, _I32, _P],
     "dali_expert_maps": [_P, _I32, _I32, _P],
     "dali_init_uniform_bf16": [_P, _I64, C.c_uint64, C.c_uint64, C.c_float, _P],

@@ -443,6 +443,12 @@ struct StageJob {
   std::function<void(int)> fn;
   Pool* pool = nullptr;
   bool busy = false;
+  // completion word: the thread that finishes the job's last unit stores
+  // flag_value there (release), for a device kernel polling it over UVA (the
+  // decode layer's combine, launched before the join)
+  std::atomic<int> left{0};
+  uint64_t* flag = nullptr;
+  uint64_t flag_value = 0;
 
   void unit(const Stage& st, int u) {
     const int e = st.expert, R = rows[e];
@@ -477,6 +483,8 @@ struct StageJob {
            u = st.next.fetch_add(1, std::memory_order_relaxed)) {
         unit(st, u);
         st.done.fetch_add(1, std::memory_order_release);
+        if (left.fetch_sub(1, std::memory_order_acq_rel) == 1 && flag)
+          __atomic_store_n(flag, flag_value, __ATOMIC_RELEASE);
       }
     }
   }
@@ -489,9 +497,45 @@ StageJob& stage_job() {
 bool async_job_busy() { return stage_job().busy; }
 }  // namespace
 
+static int submit_job(int32_t n, const uint64_t* blocks, const uint64_t* xs, const int32_t* rows,
+                      const uint64_t* ys, int32_t d, int32_t f, int32_t nthreads, uint64_t* flag,
+                      uint64_t flag_value);
+
 extern "C" int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const uint64_t* xs,
                                       const int32_t* rows, const uint64_t* ys, int32_t d,
                                       int32_t f, int32_t nthreads) {
+  return submit_job(n, blocks, xs, rows, ys, d, f, nthreads, nullptr, 0);
+}
+
+extern "C" int dali_cpu_submit_layer(const int8_t* C, const int32_t* offsets, int32_t N,
+                                     const uint64_t* blocks, const uint16_t* xp, float* out,
+                                     int32_t d, int32_t f, int32_t nthreads, uint64_t* done_flag,
+                                     uint64_t done_value, int32_t* n_experts) {
+  if (!C || !offsets || !blocks || !xp || !out || !n_experts || N < 1 || N > 4096)
+    return DALI_ETRACE;
+  uint64_t bl[256], xs[256], ys[256];
+  int32_t rows[256];
+  int n = 0;
+  for (int e = 0; e < N; ++e) {
+    const int r0 = offsets[e], r1 = offsets[e + 1];
+    if (!C[e] || r1 <= r0) continue;
+    if (r1 - r0 > kMaxRows || n == 256) {           // prefill-sized: the caller's AMX path
+      *n_experts = -1;
+      return DALI_OK;
+    }
+    bl[n] = blocks[e];
+    xs[n] = reinterpret_cast<uint64_t>(xp + (int64_t)r0 * d);
+    ys[n] = reinterpret_cast<uint64_t>(out + (int64_t)r0 * d);
+    rows[n] = r1 - r0;
+    ++n;
+  }
+  *n_experts = n;
+  return submit_job(n, bl, xs, rows, ys, d, f, nthreads, done_flag, done_value);
+}
+
+static int submit_job(int32_t n, const uint64_t* blocks, const uint64_t* xs, const int32_t* rows,
+                      const uint64_t* ys, int32_t d, int32_t f, int32_t nthreads, uint64_t* flag,
+                      uint64_t flag_value) {
   if (n < 0 || (n > 0 && (!blocks || !xs || !rows || !ys)) || d % 32 || f % 64)
     return DALI_ETRACE;
   if (n > 0 && !cpu_ok()) return DALI_ESIM;
@@ -522,6 +566,15 @@ extern "C" int dali_cpu_expert_submit(int32_t n, const uint64_t* blocks, const u
     dn.down = 1;
     dn.dep = i;
     dn.units = rows[i] > 0 ? (d + kDownRows - 1) / kDownRows : 0;
+  }
+  int total = 0;
+  for (int i = 0; i < 2 * n; ++i) total += j.stages[i].units;
+  j.flag = flag;
+  j.flag_value = flag_value;
+  j.left.store(total, std::memory_order_relaxed);
+  if (total == 0) {                                 // nothing to run, nothing to join
+    if (flag) __atomic_store_n(flag, flag_value, __ATOMIC_RELEASE);
+    return DALI_OK;
   }
   j.pool = pool_for(nthreads < 1 ? 1 : nthreads);
   j.fn = [&j](int) { j.work(); };

@@ -231,19 +231,51 @@ __device__ __forceinline__ void pcie_quiet(unsigned long long ns) {
 constexpr unsigned long long kQuietChainNs = 120000;   // combine -> decision mirrors
 constexpr unsigned long long kQuietCtlNs = 25000;      // one control transfer
 
+// Host completion word.  The offloaded decode launches a layer's combine
+// before the host worker has produced the CPU experts' rows: thread 0 of each
+// CTA polls the mapped pinned word that the worker's last work unit stores
+// (dali_cpu_submit_layer) until it reaches `want`, then the CTA reads the rows.
+// One poller per CTA with a ~0.5 us back-off keeps the PCIe read traffic
+// negligible (per-thread polling of the rows themselves was measured to slow
+// the host worker down).  ld.global.cv on every read: a System Memory line
+// the GPU L2 holds is discarded and re-fetched (ld.volatile was measured to
+// return a stale line for seconds now and then, tools/stress_launch_ahead.py).
+// Bounded: after kHostWaitNs the CTA gives up, counts a timeout
+// (dali_host_wait_timeouts) and proceeds.
+__device__ unsigned long long g_host_wait_timeouts = 0;
+constexpr unsigned long long kHostWaitNs = 4000000000ull;
+__device__ __forceinline__ void wait_host_word(const unsigned long long* w, unsigned long long want) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = gtimer_ns();
+    while (__ldcv(w) < want) {
+      if (gtimer_ns() - t0 > kHostWaitNs) {
+        atomicAdd(&g_host_wait_timeouts, 1ull);
+        break;
+      }
+      __nanosleep(500);
+    }
+    __threadfence_system();
+  }
+  __syncthreads();
+}
+
 __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __restrict__ yp,
                                const int32_t* __restrict__ idx, const int32_t* __restrict__ pos,
                                const float* __restrict__ wts, const int8_t* __restrict__ mask,
                                const float* __restrict__ cpu_rows,
                                const float* __restrict__ extra, int64_t T, int k, int d,
-                               int splits, int64_t plane, uint16_t* __restrict__ out) {
+                               int splits, int64_t plane, uint16_t* __restrict__ out,
+                               const unsigned long long* __restrict__ rows_ready,
+                               unsigned long long rows_want) {
   // one thread per (token, 8-column chunk): all of a row's chunks load their
   // k x splits partial rows concurrently (decode: T=1 is latency-bound).
   // When the grid covers every item (decode), the routing inputs (top-k ids,
-  // permuted positions, weights, G mask) and the residual row -- all written
-  // by kernels that completed before the predecessor started -- are loaded
-  // before the PDL wait; only the expert outputs (yp, the CPU rows, the
-  // shared-expert rows) wait for the predecessor.
+  // permuted positions, weights) and the residual row -- all written by
+  // kernels that completed before the predecessor started -- are loaded
+  // before the PDL wait.  The G mask is not: it lives in the layer's pointer
+  // table, whose upload kernel is the direct predecessor when a layer has no
+  // GPU expert.  The expert outputs (yp, the CPU rows, the shared-expert rows)
+  // and the mask are read after the wait.
   const int d8 = d >> 3;
   const int64_t items = T * d8;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -253,7 +285,7 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
   if (single && it0 == 0) pcie_quiet(kQuietChainNs);      // decode: the chain starts here
   float g_[kPreK];
   int64_t r_[kPreK];
-  bool on_[kPreK];
+  int on_[kPreK];
   uint4 xv0 = make_uint4(0, 0, 0, 0);
   if (single && it0 < items) {
     const int64_t t = it0 / d8;
@@ -263,12 +295,18 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
       if (j < k) {
         g_[j] = wts[t * k + j];
         r_[j] = (int64_t)pos[t * k + j] * d;
-        on_[j] = !mask || mask[idx[t * k + j]];
+        on_[j] = idx[t * k + j];              // expert id; the mask is applied after the wait
       }
     }
     xv0 = reinterpret_cast<const uint4*>(x + t * d)[c];
   }
   DALI_PDL_ENTRY();
+  if (rows_ready) wait_host_word(rows_ready, rows_want);  // CPU experts' rows complete
+  if (single && it0 < items) {
+#pragma unroll
+    for (int j = 0; j < kPreK; ++j)
+      if (j < k) on_[j] = !mask || mask[on_[j]];
+  }
   for (int64_t it = it0; it < items; it += stride) {
     const int64_t t = it / d8;
     const int c = (int)(it - t * d8);
@@ -291,8 +329,8 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
           }
         } else {                                       // row computed by the CPU worker
           const float4* src = reinterpret_cast<const float4*>(cpu_rows + r) + 2 * c;
-          a = src[0];
-          b = src[1];
+          a = __ldcv(src);                             // host memory: never a stale L2 line
+          b = __ldcv(src + 1);
         }
         acc[0] = fmaf(g, a.x, acc[0]); acc[1] = fmaf(g, a.y, acc[1]);
         acc[2] = fmaf(g, a.z, acc[2]); acc[3] = fmaf(g, a.w, acc[3]);
@@ -405,12 +443,43 @@ extern "C" int dali_expert_ffn_simt(const uint16_t* xp, const int32_t* offsets, 
   return DALI_OK;
 }
 
+extern "C" int dali_unpermute_combine_wait(const uint16_t* x, const float* yp,
+                                           const int32_t* topk_idx, const int32_t* pos,
+                                           const float* topk_w, const int8_t* gpu_mask,
+                                           const float* cpu_rows, const float* extra, int64_t T,
+                                           int32_t k, int32_t d, int32_t splits, int64_t rows,
+                                           uint16_t* out, const uint64_t* rows_ready,
+                                           uint64_t rows_want, void* stream);
+
 extern "C" int dali_unpermute_combine(const uint16_t* x, const float* yp, const int32_t* topk_idx,
                                       const int32_t* pos, const float* topk_w,
                                       const int8_t* gpu_mask, const float* cpu_rows,
                                       const float* extra, int64_t T, int32_t k, int32_t d,
                                       int32_t splits, int64_t rows, uint16_t* out,
                                       void* stream) {
+  return dali_unpermute_combine_wait(x, yp, topk_idx, pos, topk_w, gpu_mask, cpu_rows, extra, T, k,
+                                     d, splits, rows, out, nullptr, 0, stream);
+}
+
+extern "C" int dali_host_wait_timeouts(uint64_t* out, int32_t reset) {
+  unsigned long long v = 0;
+  DALI_REQUIRE(out && cudaMemcpyFromSymbol(&v, g_host_wait_timeouts, sizeof(v)) == cudaSuccess,
+               DALI_ECUDA, "dali_host_wait_timeouts: read failed");
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_host_wait_timeouts, &z, sizeof(z));
+  }
+  *out = v;
+  return DALI_OK;
+}
+
+extern "C" int dali_unpermute_combine_wait(const uint16_t* x, const float* yp,
+                                           const int32_t* topk_idx, const int32_t* pos,
+                                           const float* topk_w, const int8_t* gpu_mask,
+                                           const float* cpu_rows, const float* extra, int64_t T,
+                                           int32_t k, int32_t d, int32_t splits, int64_t rows,
+                                           uint16_t* out, const uint64_t* rows_ready,
+                                           uint64_t rows_want, void* stream) {
   DALI_REQUIRE(d % 8 == 0, DALI_ETRACE, "hidden dim %d must be a multiple of 8", d);
   if (T <= 0) return DALI_OK;
   const int64_t blocks = std::min<int64_t>((T * (d / 8) + 255) / 256, (int64_t)sm_count() * 8);
@@ -418,7 +487,9 @@ extern "C" int dali_unpermute_combine(const uint16_t* x, const float* yp, const 
                                                                   gpu_mask, cpu_rows, extra, T, k,
                                                                   d,
                                                                   splits < 1 ? 1 : splits,
-                                                                  rows * (int64_t)d, out);
+                                                                  rows * (int64_t)d, out,
+                                                                  reinterpret_cast<const unsigned long long*>(rows_ready),
+                                                                  (unsigned long long)rows_want);
   DALI_LAUNCH_CHECK("combine_kernel");
   return DALI_OK;
 }
@@ -436,9 +507,12 @@ __global__ void copy_mapped_kernel(uint4* __restrict__ dst, const uint4* __restr
   if (blockIdx.x == 0 && threadIdx.x == 0) pcie_quiet(kQuietCtlNs);
   DALI_PDL_ENTRY();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // .cv loads: the source is often mapped pinned host memory the host rewrites
+  // between launches (pointer tables, descriptors) -- never serve it from L2
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
-    dst[i] = src[i];
-  if (blockIdx.x == 0 && threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
+    dst[i] = __ldcv(src + i);
+  if (blockIdx.x == 0 && threadIdx.x < tail)
+    dst_tail[threadIdx.x] = *reinterpret_cast<const volatile uint8_t*>(src_tail + threadIdx.x);
 }
 __global__ void copy_bytes_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
                                   int64_t n) {

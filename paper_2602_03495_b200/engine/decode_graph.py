@@ -14,6 +14,7 @@ import torch
 from .. import _lib
 from ..errors import SimulationError
 from .layers import rms_norm
+_DEBUG_WS = __import__("os").environ.get("DALI_DEBUG_WS", "0") == "1"
 
 
 class DecodeGraphMixin:
@@ -128,12 +129,28 @@ class DecodeGraphMixin:
         torch.index_select(W.embed, 0, tok_dev.reshape(-1), out=X)
         heads = self._heads
         capture = self._heads_warm and not heads
+        # launch-ahead: layer l's combine is queued before its CPU experts are
+        # joined (it polls their completion word on the device), then layer
+        # l+1's head graph, and only then does this thread join layer l's CPU
+        # work -- the device chain starts the moment the last CPU row lands
+        ahead = self._launch_ahead and self._cpu_async and self.policy.prefetch_kind != "random"
+        try:
+            self._decode_layers(L, X, X2, B, step, heads, capture, ahead)
+        finally:
+            self._join_pending()
+        self._heads_warm = True
+        self.policy.n_records = base + L
+        return rms_norm(X, W.final_norm, a.rms_eps) @ W.lm_head.t()
+
+    def _decode_layers(self, L: int, X: torch.Tensor, X2: torch.Tensor, B: int, step: int,
+                       heads: dict, capture: bool, ahead: bool) -> None:
+        cs = self._cur()
         for l in range(L):
             ev_r = None
             if self.cfg.trace_layers:
                 ev_r = torch.cuda.Event(enable_timing=True)
                 ev_r.record(cs)
-            tp0 = time.perf_counter()
+            tq = time.perf_counter()
             if l in heads:
                 g, h, views, nk = heads[l]
                 g.replay()
@@ -148,15 +165,18 @@ class DecodeGraphMixin:
                 finally:
                     self._capturing = False
                 nk = _lib.launch_count() - k0         # our kernels in the graph body
+                if _DEBUG_WS:
+                    print(f"[ws] captured head {l} step {step} h={h.data_ptr():#x}", flush=True)
                 g.replay()
                 self.graph_kernels += nk
                 heads[l] = (g, h, views, nk)
             else:
                 h, views = self._decode_head(l, X, X2, B)
-            self._moe_tail(l, X2, h, step, views, tp0, ev_r, X)
-        self._heads_warm = True
-        self.policy.n_records = base + L
-        return rms_norm(X, W.final_norm, a.rms_eps) @ W.lm_head.t()
+            tl = time.perf_counter()
+            self._join_pending()                     # layer l-1's CPU experts
+            # launch time of the head, excluding the join (accounted as CPU time)
+            tp0 = time.perf_counter() - (tl - tq)
+            self._moe_tail(l, X2, h, step, views, tp0, ev_r, X, ahead=ahead)
 
     def _set_desc(self, step: int, token_index: int, eos_at: int, rec_index: int, pos: int):
         """Write the device step descriptor (stream-ordered kernel copy from

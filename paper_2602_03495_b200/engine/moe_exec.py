@@ -25,6 +25,8 @@ from ..trace import route_device
 from .cpu_worker import NATIVE_MAX_ROWS, cpu_expert_rows
 from .weights import h2d_block
 
+_REC_C_OFF = _lib.LayerRecordC.C.offset          # C vector inside dali_layer_record
+
 
 def ffn_splits(max_rows: int, tiles: int, kb: int, n_sm: int) -> int:
     """Split-K planes of the down projection for dali_expert_ffn_tc: the
@@ -384,6 +386,50 @@ class MoEExecMixin:
                        "dali_cpu_expert_submit")
         return dict(out=out, native=n > 0, big=big, lo=lo, hi=hi, l=l, rows=rows_host)
 
+    def _cpu_submit_layer(self, l: int, rows_host: torch.Tensor, offs_host: torch.Tensor, rec,
+                          R: int):
+        """Decode fast path of ``_cpu_submit``: one native call reads the
+        record's C vector and the offsets mirror, starts the layer's CPU
+        experts and arms the completion word the launched-ahead combine polls
+        (dali_cpu_submit_layer).  Returns the job (None: no CPU expert) or
+        False when an expert is prefill-sized (nothing started)."""
+        a = self.arch
+        d = a.hidden_dim
+        ent = self._sub_args.get(l)
+        if ent is None:
+            if self._blk_tab is None:
+                self._blk_tab = np.array([[self.w.expert_host_ptr(ll, e) for e in range(self.NL)]
+                                          for ll in range(a.num_layers)], dtype=np.uint64)
+            n = C.c_int32()
+            ent = (_lib.load().dali_cpu_submit_layer, n, C.byref(n),
+                   self._blk_tab[l].ctypes.data)
+            self._sub_args[l] = ent
+        fn, n, n_ref, tab_p = ent
+        out = self._ws("cpu_rows_h", (R, d), torch.float32, pinned=True)   # grow-only: re-fetch
+        self._rows_seq += 1
+        _lib.check(fn(C.addressof(rec) + _REC_C_OFF, offs_host.data_ptr(), self.NL, tab_p,
+                      rows_host.data_ptr(), out.data_ptr(), d, a.ffn_dim, self.cpu_threads,
+                      self._rows_flag_p, self._rows_seq, n_ref), "dali_cpu_submit_layer")
+        if n.value < 0:
+            return False
+        if n.value == 0:
+            return None
+        self.stats.cpu_expert_calls += n.value
+        return dict(out=out, native=True, big=[], seq=self._rows_seq)
+
+    def _join_pending(self) -> None:
+        """Join the previous decode layer's CPU experts (this thread takes the
+        remaining work units).  Its combine was launched ahead and waits on
+        the completion word, so nothing else is left to do here."""
+        job = self._pending_cpu
+        if job is None:
+            return
+        self._pending_cpu = None
+        t0 = time.perf_counter()
+        _lib.call("dali_cpu_expert_wait")
+        pr = self.stats.host_ms
+        pr["cpu_experts"] = pr.get("cpu_experts", 0.0) + (time.perf_counter() - t0) * 1e3
+
     def _cpu_finish(self, job, R: int) -> torch.Tensor | None:
         """Run the prefill-sized CPU experts and join the asynchronous ones;
         returns the pinned (R, d) f32 rows, which device kernels read over UVA."""
@@ -471,10 +517,17 @@ class MoEExecMixin:
         return dict(v=v, hv=hv, xp_host=xp_host, h_host=h_host, ri=ri, T=T)
 
     def _moe_tail(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, views: dict,
-                  tp0: float, ev_r, out: torch.Tensor) -> torch.Tensor:
+                  tp0: float, ev_r, out: torch.Tensor, ahead: bool = False) -> torch.Tensor:
         """Host half: wait for the decision record, execute it (GPU experts
         from cache / staging / demand copy, prefetch + replacement copies, CPU
-        experts on the host worker) and queue the Eq. (2) combine into ``out``."""
+        experts on the host worker) and queue the Eq. (2) combine into ``out``.
+
+        ahead=True (offloaded decode): the CPU experts start through
+        dali_cpu_submit_layer and the combine is launched at once, polling the
+        worker's completion word on the device; the join is left to the
+        caller (``_join_pending`` after it queued the next layer's head), so
+        the device runs combine -> next attention -> routing -> policy as soon
+        as the last CPU row lands, with no host round trip in between."""
         a = self.arch
         N, k, d = a.num_experts, a.top_k, a.hidden_dim
         v, hv, xp_host, T = views["v"], views["hv"], views["xp_host"], views["T"]
@@ -493,7 +546,13 @@ class MoEExecMixin:
         # dispatches the GPU experts and copies of the same layer; _cpu_finish
         # then joins the pool (this thread takes the remaining work units).
         # DALI_CPU_ASYNC=0: GPU work first, then the CPU experts synchronously.
-        job = self._cpu_submit(l, xp_host, offs_np, rec, R) if self._cpu_async else None
+        job = None
+        if ahead:
+            job = self._cpu_submit_layer(l, xp_host, hv["offsets"], rec, R)
+            if job is False:                        # prefill-sized expert: generic path
+                ahead, job = False, None
+        if not ahead and self._cpu_async:
+            job = self._cpu_submit(l, xp_host, offs_np, rec, R)
         tp_sub = time.perf_counter()
         try:
             wl_np = hv["wl"].numpy().copy()
@@ -508,16 +567,21 @@ class MoEExecMixin:
                 _lib.load().dali_cpu_expert_wait()     # never leave a job in flight
             raise
         tp3 = time.perf_counter()
-        if not self._cpu_async:
-            job = self._cpu_submit(l, xp_host, offs_np, rec, R)
-        cpu_rows = self._cpu_finish(job, R)
+        if ahead:
+            cpu_rows = job["out"] if job is not None else None
+            self._pending_cpu = job
+        else:
+            if not self._cpu_async:
+                job = self._cpu_submit(l, xp_host, offs_np, rec, R)
+            cpu_rows = self._cpu_finish(job, R)
         tp4 = time.perf_counter()
         self._acct(tp0, tp1, tp2, tp3, tp4)
-        _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
+        _lib.call("dali_unpermute_combine_wait", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
                   v["pos"].data_ptr(), v["wts"].data_ptr(), gmask_p,
                   cpu_rows.data_ptr() if cpu_rows is not None else None,
                   y_shared.data_ptr() if y_shared is not None else None, T, k, d, splits,
-                  R, out.data_ptr(), cs.cuda_stream)
+                  R, out.data_ptr(), self._rows_flag_p if (ahead and job is not None) else None,
+                  job["seq"] if (ahead and job is not None) else 0, cs.cuda_stream)
         if self.cfg.capture_moe_io:
             self._capture_io(step, l, x, out)
         if tr:
@@ -528,7 +592,7 @@ class MoEExecMixin:
                 step=step, layer=l, T=T, nC=int(sum(1 for e in range(N) if rec.C[e] and wl_np[e])),
                 hit=le["hit"], pf=le["pf"], dem=le["dem"], rep=le["rep"], done=le["done"],
                 host=(tp0, tp1, tp2, tp3, tp4, time.perf_counter()), tp_sub=tp_sub,
-                ev_rows=self._ev_rows if cpu_rows is not None else None,
+                ev_rows=self._ev_rows if (cpu_rows is not None and not ahead) else None,
                 ev=(ev_r if ev_r is not None else ev_dec, ev_dec, le["t0"], ev_c)))
         return out
 

@@ -48,6 +48,8 @@ from .moe_exec import MoEExecMixin, ffn_splits  # noqa: F401  (ffn_splits re-exp
 from .weights import ModelWeights
 
 
+_DEBUG_WS = os.environ.get("DALI_DEBUG_WS", "0") == "1"
+
 @dataclass
 class EngineConfig:
     cache_slots_per_layer: int = 0          # 0 = no cache (every GPU expert demand-fetched)
@@ -210,6 +212,17 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         # dispatch first, then run them synchronously -- A/B switch)
         self._cpu_async = os.environ.get("DALI_CPU_ASYNC", "1") == "1"
         self._cpu_sub = None                  # preallocated submission arrays (_cpu_submit)
+        # offloaded decode: a layer's combine is launched before its CPU experts
+        # finish and polls this pinned word (dali_unpermute_combine_wait), which
+        # the worker's last unit sets to the layer's sequence number; the join
+        # is deferred past the next layer's head
+        self._launch_ahead = os.environ.get("DALI_LAUNCH_AHEAD", "1") == "1"
+        self._rows_flag = torch.zeros(2, dtype=torch.int64).pin_memory()
+        self._rows_flag_p = self._rows_flag.data_ptr()
+        self._rows_seq = 0
+        self._pending_cpu = None              # deferred join of the previous layer
+        self._blk_tab = None                  # (L, N) host block addresses (dali_cpu_submit_layer)
+        self._sub_args = {}                   # layer -> prebuilt submission arguments
         self._ev_rows = None                  # trace: event before the CPU-row upload
         torch.set_num_threads(self.cpu_threads)
         # per-layer pinned scratch for pointer table + G mask
@@ -301,6 +314,9 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         t = self._wsd.get(key)
         if t is None or t.numel() < n:
             if t is not None:
+                if _DEBUG_WS:
+                    print(f"[ws] {name} grows {t.numel()} -> {n} (capturing={self._capturing})",
+                          flush=True)
                 if self._capturing:
                     raise SimulationError(f"workspace {name!r} grew during graph capture")
                 self._ws_retired.append(t)
@@ -312,6 +328,8 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
 
     def _drop_graphs(self) -> None:
         """Forget the captured decode graphs (re-captured on demand)."""
+        if _DEBUG_WS:
+            print(f"[ws] drop graphs ({len(self._heads)} heads)", flush=True)
         self._graph = None
         self._graph_warm = False
         self._heads, self._heads_warm = {}, False
