@@ -452,18 +452,6 @@ int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
                           int32_t splits, float scale, float* workspace,
                           uint16_t* out, void* stream);
 
-/* dali_rope_append + dali_decode_attention in one launch, bit for bit:
- * every CTA rotates its query head from qkv, the CTA holding position *pos
- * computes the new rotated K / V row itself (and the first query head of each
- * KV group appends it to the caches), the last CTA of each (b, h) row merges
- * the split partials.  counters: (B*H,) u32, zero-initialised, left zeroed. */
-int dali_decode_attention_fused(const uint16_t* qkv, const float* cos_t, const float* sin_t,
-                                const int32_t* pos, const int32_t* len, int32_t B, int32_t H,
-                                int32_t KV, int32_t hd, int32_t max_len, int32_t splits,
-                                float scale, uint16_t* k_cache, uint16_t* v_cache,
-                                float* workspace, uint32_t* counters, uint16_t* out,
-                                void* stream);
-
 /* ---- expert-parallel exchange over peer memory ---------------------------
  * The EP MoE layer's dispatch and return all-to-alls, fused with the permute
  * / unpermute around them: ranks store rows straight into each other's

@@ -110,8 +110,6 @@ SIGNATURES = {
                                _P],
     "dali_step_advance": [_P, _P],
     "dali_rope_append": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P],
-    "dali_decode_attention_fused": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32,
-                                    C.c_float, _P, _P, _P, _P, _P, _P],
     "dali_decode_attention": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, C.c_float, _P,
                               _P, _P],
     "dali_cpu_expert": [_P, _I32, _I32, _P, _I32, _P, _I32],

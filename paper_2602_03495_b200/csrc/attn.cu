@@ -177,164 +177,6 @@ __global__ void attn_merge_kernel(const float* __restrict__ ws, int nsplit,
   }
 }
 
-// Fused decode attention: RoPE + KV append + split-K attention + split merge
-// in one launch (the three kernels above, bit for bit):
-//  * every CTA (b, h, split) rotates its own query head from the qkv row
-//    (rope_append's arithmetic, q rounded to bf16 as it was stored);
-//  * the CTA whose split holds the new position computes that position's
-//    rotated K and V row itself and uses them from registers (the first query
-//    head of each KV group also writes them to the caches for later steps),
-//    so no CTA reads a cache row another CTA is writing;
-//  * the last CTA of a (b, h) row to finish (a per-row counter, reset by that
-//    CTA for the next launch) merges the split partials exactly as
-//    attn_merge_kernel does.
-template <int HD>
-__global__ void __launch_bounds__(kAttnWarps * 32)
-decode_attn_fused_kernel(const uint16_t* __restrict__ qkv, const float* __restrict__ cos_t,
-                         const float* __restrict__ sin_t, const int32_t* __restrict__ pos_p,
-                         const int32_t* __restrict__ len_p, int H, int KV, int max_len,
-                         float scale, uint16_t* __restrict__ kc, uint16_t* __restrict__ vc,
-                         float* __restrict__ ws, unsigned int* __restrict__ counters,
-                         uint16_t* __restrict__ o) {
-  DALI_PDL_ENTRY();
-  constexpr int EL = HD / 32, HALF = HD / 2;
-  const int bh = blockIdx.x, b = bh / H, h = bh % H;
-  const int grp = H / KV, kvh = h / grp;
-  const int split = blockIdx.y, nsplit = gridDim.y;
-  const int pos = *pos_p, len = *len_p;
-  const int chunk = (len + nsplit - 1) / nsplit;
-  const int p0 = split * chunk, p1 = min(len, p0 + chunk);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint16_t* row = qkv + (int64_t)b * (H + 2 * KV) * HD;
-  // rotated (bf16-rounded) element i of head `head` of the qkv row
-  auto rot = [&](int head, int i) -> uint16_t {
-    const uint16_t* src = row + (int64_t)head * HD;
-    const int j = i < HALF ? i : i - HALF;
-    const float x0 = bf16_bits_to_f32(src[j]), x1 = bf16_bits_to_f32(src[j + HALF]);
-    const float c = cos_t[(int64_t)pos * HALF + j], sn = sin_t[(int64_t)pos * HALF + j];
-    return i < HALF ? f32_to_bf16_bits(x0 * c - x1 * sn) : f32_to_bf16_bits(x1 * c + x0 * sn);
-  };
-  float qv[EL];
-#pragma unroll
-  for (int i = 0; i < EL; ++i) qv[i] = bf16_bits_to_f32(rot(h, lane * EL + i)) * scale;
-  const bool has_new = pos >= p0 && pos < p1;
-  float knew[EL], vnew[EL];
-  if (has_new) {
-    uint16_t kb16[EL], vb16[EL];
-#pragma unroll
-    for (int i = 0; i < EL; ++i) {
-      kb16[i] = rot(H + kvh, lane * EL + i);
-      vb16[i] = row[(int64_t)(H + KV + kvh) * HD + lane * EL + i];
-      knew[i] = bf16_bits_to_f32(kb16[i]);
-      vnew[i] = bf16_bits_to_f32(vb16[i]);
-    }
-    if (h % grp == 0 && warp == 0) {                        // one writer per KV head
-      uint16_t* kd = kc + (((int64_t)b * KV + kvh) * max_len + pos) * HD + lane * EL;
-      uint16_t* vd = vc + (((int64_t)b * KV + kvh) * max_len + pos) * HD + lane * EL;
-#pragma unroll
-      for (int i = 0; i < EL; ++i) {
-        kd[i] = kb16[i];
-        vd[i] = vb16[i];
-      }
-    }
-  }
-  const uint16_t* kb = kc + ((int64_t)b * KV + kvh) * max_len * HD;
-  const uint16_t* vb = vc + ((int64_t)b * KV + kvh) * max_len * HD;
-  auto load_kv = [&](int p, float* kk, float* vv) {
-    if (p == pos) {
-#pragma unroll
-      for (int i = 0; i < EL; ++i) {
-        kk[i] = knew[i];
-        vv[i] = vnew[i];
-      }
-    } else {
-      load_bf16_lane<EL>(kb + (int64_t)p * HD + lane * EL, kk);
-      load_bf16_lane<EL>(vb + (int64_t)p * HD + lane * EL, vv);
-    }
-  };
-  float m = -INFINITY, l = 0.f, acc[EL];
-#pragma unroll
-  for (int i = 0; i < EL; ++i) acc[i] = 0.f;
-  float kn[EL], vn[EL];
-  if (p0 + warp < p1) load_kv(p0 + warp, kn, vn);
-  for (int p = p0 + warp; p < p1; p += kAttnWarps) {
-    float kv_[EL], vv[EL];
-#pragma unroll
-    for (int i = 0; i < EL; ++i) {
-      kv_[i] = kn[i];
-      vv[i] = vn[i];
-    }
-    if (p + kAttnWarps < p1) load_kv(p + kAttnWarps, kn, vn);
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < EL; ++i) s += qv[i] * kv_[i];
-#pragma unroll
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    const float mn = fmaxf(m, s);
-    const float corr = __expf(m - mn), ps = __expf(s - mn);
-    l = l * corr + ps;
-#pragma unroll
-    for (int i = 0; i < EL; ++i) acc[i] = acc[i] * corr + ps * vv[i];
-    m = mn;
-  }
-  __shared__ float sm[kAttnWarps], sl[kAttnWarps], sacc[kAttnWarps][HD];
-  __shared__ bool last;
-  if (lane == 0) { sm[warp] = m; sl[warp] = l; }
-#pragma unroll
-  for (int i = 0; i < EL; ++i) sacc[warp][lane * EL + i] = acc[i];
-  __syncthreads();
-  float* part = ws + (int64_t)bh * nsplit * (HD + 2);
-  if (warp == 0) {
-    float M = -INFINITY;
-    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm[w]);
-    float L = 0.f, A[EL];
-#pragma unroll
-    for (int i = 0; i < EL; ++i) A[i] = 0.f;
-    for (int w = 0; w < kAttnWarps; ++w) {
-      const float c = sm[w] == -INFINITY ? 0.f : __expf(sm[w] - M);
-      L += sl[w] * c;
-#pragma unroll
-      for (int i = 0; i < EL; ++i) A[i] += sacc[w][lane * EL + i] * c;
-    }
-    float* out = part + (int64_t)split * (HD + 2);
-    if (lane == 0) { out[0] = M; out[1] = L; }
-#pragma unroll
-    for (int i = 0; i < EL; ++i) out[2 + lane * EL + i] = A[i];
-  }
-  // last CTA of the row merges (attn_merge_kernel's arithmetic)
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counters + bh, 1u) == (unsigned)(nsplit - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  float ms[kMergeMax], ls[kMergeMax];
-#pragma unroll
-  for (int s = 0; s < kMergeMax; ++s) {
-    ms[s] = s < nsplit ? __ldcg(part + s * (HD + 2)) : -INFINITY;
-    ls[s] = s < nsplit ? __ldcg(part + s * (HD + 2) + 1) : 0.f;
-  }
-  float M = -INFINITY;
-#pragma unroll
-  for (int s = 0; s < kMergeMax; ++s)
-    if (s < nsplit) M = fmaxf(M, ms[s]);
-  for (int i = threadIdx.x; i < HD; i += blockDim.x) {
-    float as[kMergeMax];
-#pragma unroll
-    for (int s = 0; s < kMergeMax; ++s) as[s] = s < nsplit ? __ldcg(part + s * (HD + 2) + 2 + i) : 0.f;
-    float L = 0.f, A = 0.f;
-#pragma unroll
-    for (int s = 0; s < kMergeMax; ++s) {
-      if (s >= nsplit) break;
-      const float c = ms[s] == -INFINITY ? 0.f : __expf(ms[s] - M);
-      L += ls[s] * c;
-      A += as[s] * c;
-    }
-    o[(int64_t)bh * HD + i] = f32_to_bf16_bits(A / L);
-  }
-  if (threadIdx.x == 0) counters[bh] = 0u;                 // ready for the next launch
-}
-
 }  // namespace dali
 
 extern "C" int dali_rope_append(const uint16_t* qkv, const float* cos_t, const float* sin_t,
@@ -370,29 +212,5 @@ extern "C" int dali_decode_attention(const uint16_t* q, const uint16_t* k_cache,
     dali::launch_pdl(dali::attn_merge_kernel<64>, dim3(B * H), dim3(64), 0, st, workspace, splits, out);
   }
   DALI_LAUNCH_CHECK("attn_merge_kernel");
-  return DALI_OK;
-}
-
-extern "C" int dali_decode_attention_fused(const uint16_t* qkv, const float* cos_t,
-                                           const float* sin_t, const int32_t* pos,
-                                           const int32_t* len, int32_t B, int32_t H, int32_t KV,
-                                           int32_t hd, int32_t max_len, int32_t splits,
-                                           float scale, uint16_t* k_cache, uint16_t* v_cache,
-                                           float* workspace, uint32_t* counters, uint16_t* out,
-                                           void* stream) {
-  DALI_REQUIRE(hd == 128 || hd == 64, DALI_ETRACE,
-               "decode attention kernel supports head_dim 64 or 128, got %d", hd);
-  DALI_REQUIRE(H % KV == 0 && splits >= 1 && splits <= dali::kMergeMax && counters, DALI_ETRACE,
-               "bad attention geometry (splits %d, at most %d)", splits, dali::kMergeMax);
-  cudaStream_t st = dali::as_stream(stream);
-  if (hd == 128)
-    dali::launch_pdl(dali::decode_attn_fused_kernel<128>, dim3(B * H, splits),
-                     dim3(dali::kAttnWarps * 32), 0, st, qkv, cos_t, sin_t, pos, len, H, KV,
-                     max_len, scale, k_cache, v_cache, workspace, counters, out);
-  else
-    dali::launch_pdl(dali::decode_attn_fused_kernel<64>, dim3(B * H, splits),
-                     dim3(dali::kAttnWarps * 32), 0, st, qkv, cos_t, sin_t, pos, len, H, KV,
-                     max_len, scale, k_cache, v_cache, workspace, counters, out);
-  DALI_LAUNCH_CHECK("decode_attn_fused_kernel");
   return DALI_OK;
 }

@@ -15,9 +15,6 @@ from .. import _lib
 from ..errors import SimulationError
 from .layers import rms_norm
 _DEBUG_WS = __import__("os").environ.get("DALI_DEBUG_WS", "0") == "1"
-# decode attention as one fused launch (dali_decode_attention_fused); 0 = rope /
-# split-K / merge as three launches (A/B switch, bit-identical results)
-_FUSED_ATTN = __import__("os").environ.get("DALI_FUSED_ATTN", "1") != "0"
 
 
 class DecodeGraphMixin:
@@ -48,26 +45,14 @@ class DecodeGraphMixin:
         a = self.arch
         H, KV, hd = a.num_heads, a.num_kv_heads, a.head_dim
         sp = self._cur().cuda_stream
-        kc, vc = self.kv.k[l], self.kv.v[l]
-        splits = 16
-        ws = self._ws("attn_ws", (B * H * splits * (hd + 2),), torch.float32)
-        o = self._ws("o_dec", (B, H * hd), torch.bfloat16)
-        if _FUSED_ATTN:
-            # RoPE + KV append + split-K attention + merge in one launch
-            ctr = self._attn_ctr
-            if ctr is None or ctr.numel() < B * H:
-                ctr = self._attn_ctr = torch.zeros(max(B, self.max_batch) * H, dtype=torch.int32,
-                                                   device=self.dev)
-            _lib.call("dali_decode_attention_fused", qkv.data_ptr(), self.rope.cos.data_ptr(),
-                      self.rope.sin.data_ptr(), self.desc_dev.data_ptr() + 16,
-                      self.desc_dev.data_ptr() + 20, B, H, KV, hd, self.max_seq, splits,
-                      1.0 / math.sqrt(hd), kc.data_ptr(), vc.data_ptr(), ws.data_ptr(),
-                      ctr.data_ptr(), o.data_ptr(), sp)
-            return o
         q = self._ws("q_dec", (B, H, hd), torch.bfloat16)
+        kc, vc = self.kv.k[l], self.kv.v[l]
         _lib.call("dali_rope_append", qkv.data_ptr(), self.rope.cos.data_ptr(),
                   self.rope.sin.data_ptr(), self.desc_dev.data_ptr() + 16, B, H, KV, hd,
                   self.max_seq, q.data_ptr(), kc.data_ptr(), vc.data_ptr(), sp)
+        splits = 16
+        ws = self._ws("attn_ws", (B * H * splits * (hd + 2),), torch.float32)
+        o = self._ws("o_dec", (B, H * hd), torch.bfloat16)
         _lib.call("dali_decode_attention", q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
                   self.desc_dev.data_ptr() + 20, B, H, KV, hd, self.max_seq, splits,
                   1.0 / math.sqrt(hd), ws.data_ptr(), o.data_ptr(), sp)

@@ -221,7 +221,6 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         self._rows_flag_p = self._rows_flag.data_ptr()
         self._rows_seq = 0
         self._pending_cpu = None              # deferred join of the previous layer
-        self._attn_ctr = None                 # split-merge counters of the fused decode attention
         self._blk_tab = None                  # (L, N) host block addresses (dali_cpu_submit_layer)
         self._sub_args = {}                   # layer -> prebuilt submission arguments
         self._ev_rows = None                  # trace: event before the CPU-row upload
