@@ -244,15 +244,62 @@ void tile_config() {
   _tile_loadconfig(&c);
 }
 
-// C(0..3) = A(4|5) x B(6|7) over K (multiple of 32); a0/a1: weight rows
-// (stride lda elements), b: VNNI tokens at token t0 (row stride 2 * tpad).
-inline void amx_block(const uint16_t* a0, const uint16_t* a1, int64_t lda, const uint16_t* b,
-                      int64_t tpad, int K, float* c /* [4][16][16] */) {
-  _tile_zero(0);
-  _tile_zero(1);
-  _tile_zero(2);
-  _tile_zero(3);
-  for (int k = 0; k < K; k += 32) {
+// Same as amx_block over k in [k0, k1) with the accumulators carried in
+// memory: loaded from c (or zeroed when first), stored back to c.  Splitting
+// the k loop this way changes nothing numerically (tile store / load of fp32
+// is exact, the dpbf16 sequence is the same).  pf: software-prefetch the
+// weight rows kPfK elements ahead (the first pass over a weight chunk streams
+// from DRAM as 32 interleaved row streams, more than the hardware prefetchers
+// track).
+inline int pf_k() {
+  static const int v = getenv("DALI_AMX_PFK") ? atoi(getenv("DALI_AMX_PFK")) : 256;
+  return v;
+}
+struct BgPf {
+  const char* base[2] = {nullptr, nullptr};   // first rows of the two 16-row tiles
+  int64_t ld = 0;                              // row stride, bytes
+  int lines_per_row = 0, pos = 0, total = 0, per_step = 0;
+  void set(const uint16_t* a0, const uint16_t* a1, int64_t lda, int k0, int k1, int steps) {
+    base[0] = reinterpret_cast<const char*>(a0 + k0);
+    base[1] = reinterpret_cast<const char*>(a1 + k0);
+    ld = lda * 2;
+    lines_per_row = (k1 - k0) * 2 / 64;
+    pos = 0;
+    total = 32 * lines_per_row;
+    per_step = steps > 0 ? (total + steps - 1) / steps : 0;
+  }
+  void clear() { total = pos = per_step = 0; }
+  inline void step() {
+    for (int i = 0; i < per_step && pos < total; ++i, ++pos) {
+      const int line = pos >> 5, row = pos & 31;     // k-major, as the next item reads them
+      _mm_prefetch(base[row >> 4] + (row & 15) * ld + line * 64, _MM_HINT_T1);
+    }
+  }
+};
+
+inline void amx_block_acc(const uint16_t* a0, const uint16_t* a1, int64_t lda, const uint16_t* b,
+                          int64_t tpad, int k0, int k1, float* c, bool first, bool pf,
+                          BgPf* bg = nullptr) {
+  if (first) {
+    _tile_zero(0);
+    _tile_zero(1);
+    _tile_zero(2);
+    _tile_zero(3);
+  } else {
+    _tile_loadd(0, c, 64);
+    _tile_loadd(1, c + 256, 64);
+    _tile_loadd(2, c + 512, 64);
+    _tile_loadd(3, c + 768, 64);
+  }
+  const int pfk = pf_k();
+  pf = pf && pfk > 0;
+  for (int k = k0; k < k1; k += 32) {
+    if (pf && k + pfk < k1) {
+      for (int r = 0; r < 16; ++r) {
+        _mm_prefetch(reinterpret_cast<const char*>(a0 + r * lda + k + pfk), _MM_HINT_T0);
+        _mm_prefetch(reinterpret_cast<const char*>(a1 + r * lda + k + pfk), _MM_HINT_T0);
+      }
+    }
     _tile_loadd(4, a0 + k, (int)(lda * 2));
     _tile_loadd(5, a1 + k, (int)(lda * 2));
     const uint16_t* bk = b + (int64_t)(k / 2) * tpad * 2;
@@ -262,11 +309,46 @@ inline void amx_block(const uint16_t* a0, const uint16_t* a1, int64_t lda, const
     _tile_dpbf16ps(1, 4, 7);
     _tile_dpbf16ps(2, 5, 6);
     _tile_dpbf16ps(3, 5, 7);
+    if (bg) bg->step();
   }
   _tile_stored(0, c, 64);
   _tile_stored(1, c + 256, 64);
   _tile_stored(2, c + 512, 64);
   _tile_stored(3, c + 768, 64);
+}
+
+// exp(x) for 16 lanes: 2^n * p(r), n = round(x log2 e), r = x - n ln 2 split
+// in two parts, degree-6 polynomial (Cephes expf coefficients, ~1 ulp); x
+// clamped to [-87.3, 88.3] (results 0 / ~2e38 at the ends, as silu needs)
+inline __m512 exp16(__m512 x) {
+  x = _mm512_max_ps(_mm512_min_ps(x, _mm512_set1_ps(88.3f)), _mm512_set1_ps(-87.3f));
+  const __m512 n = _mm512_roundscale_ps(_mm512_mul_ps(x, _mm512_set1_ps(1.44269504088896341f)),
+                                        _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+  __m512 r = _mm512_fnmadd_ps(n, _mm512_set1_ps(0.693359375f), x);
+  r = _mm512_fnmadd_ps(n, _mm512_set1_ps(-2.12194440e-4f), r);
+  __m512 p = _mm512_set1_ps(1.9875691500e-4f);
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.3981999507e-3f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(8.3334519073e-3f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(4.1665795894e-2f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.6666665459e-1f));
+  p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(5.0000001201e-1f));
+  p = _mm512_fmadd_ps(p, _mm512_mul_ps(r, r), _mm512_add_ps(r, _mm512_set1_ps(1.0f)));
+  return _mm512_scalef_ps(p, n);
+}
+// silu(g) * u, fp32 (rounded to bf16 once by the caller)
+inline __m512 swiglu16(__m512 g, __m512 u) {
+  const __m512 den = _mm512_add_ps(_mm512_set1_ps(1.0f), exp16(_mm512_sub_ps(_mm512_setzero_ps(), g)));
+  return _mm512_mul_ps(_mm512_div_ps(g, den), u);
+}
+
+// k chunk of the down projection: the fewest elements (multiple of 32,
+// dividing f) per chunk such that the chunk of the SwiGLU intermediate for
+// all tokens stays in a core's L2 (~1 MB budget of 2 MB)
+inline int down_kchunk(int f, int64_t tpad) {
+  int best = 32;
+  for (int kc = 32; kc <= f; kc += 32)
+    if (f % kc == 0 && (int64_t)kc * tpad * 2 <= (1 << 20)) best = kc;
+  return best;
 }
 
 void amx_expert(const uint16_t* block, int d, int f, const uint16_t* x, int R, float* y,
@@ -295,35 +377,89 @@ void amx_expert(const uint16_t* block, int d, int f, const uint16_t* x, int R, f
   pool->run([&](int) {
     tile_config();
     alignas(64) float c[4 * 256];
-    for (int u = next.fetch_add(1); u < units1; u = next.fetch_add(1)) {
+    BgPf bg;
+    auto rows1 = [&](int uu, const uint16_t*& g_, const uint16_t*& u_) {
+      const int b = uu / 4, i = uu % 4;
+      g_ = w13 + (int64_t)(128 * b + 16 * i) * d;
+      u_ = w13 + (int64_t)(128 * b + 64 + 16 * i) * d;
+    };
+    int u = next.fetch_add(1);
+    int un = u < units1 ? next.fetch_add(1) : units1;      // this thread's next unit
+    for (; u < units1; u = un, un = u < units1 ? next.fetch_add(1) : units1) {
       const int b = u / 4, i = u % 4;
-      const uint16_t* gr = w13 + (int64_t)(128 * b + 16 * i) * d;
-      const uint16_t* ur = w13 + (int64_t)(128 * b + 64 + 16 * i) * d;
+      const uint16_t *gr, *ur;
+      rows1(u, gr, ur);
+      if (un < units1 && tpad > 32) {
+        const uint16_t *gn, *unx;
+        rows1(un, gn, unx);
+        bg.set(gn, unx, d, 0, d, (int)(tpad / 32 - 1) * (d / 32));
+      } else {
+        bg.clear();
+      }
       for (int64_t t0 = 0; t0 < tpad; t0 += 32) {
-        amx_block(gr, ur, d, xp.data() + t0 * 2, tpad, d, c);
-        for (int r = 0; r < 16; ++r) {
+        // the first token block streams this unit's 32 weight rows from DRAM
+        // (L2 if the previous unit prefetched them); the later ones re-read
+        // them from L2 and prefetch the next unit's rows meanwhile
+        amx_block_acc(gr, ur, d, xp.data() + t0 * 2, tpad, 0, d, c, true, t0 == 0,
+                      t0 == 0 ? nullptr : &bg);
+        // SwiGLU of 16 tokens per vector, two adjacent columns interleaved
+        // into one 64-byte row of the down projection's VNNI operand
+        for (int r = 0; r < 16; r += 2) {
           const int col = 64 * b + 16 * i + r;
-          uint16_t* hrow = hp.data() + (int64_t)(col / 2) * tpad * 2 + (col & 1);
-          for (int j = 0; j < 32; ++j) {
-            const float g = c[(j < 16 ? 0 : 256) + r * 16 + (j & 15)];
-            const float v = c[(j < 16 ? 512 : 768) + r * 16 + (j & 15)];
-            hrow[(t0 + j) * 2] = f2bf(g / (1.0f + std::exp(-g)) * v);
+          uint32_t* hrow = reinterpret_cast<uint32_t*>(hp.data()) + (int64_t)(col / 2) * tpad;
+          for (int jb = 0; jb < 32; jb += 16) {
+            const int cg = jb ? 256 : 0, cu = jb ? 768 : 512;
+            const __m512 h0 = swiglu16(_mm512_load_ps(c + cg + r * 16), _mm512_load_ps(c + cu + r * 16));
+            const __m512 h1 =
+                swiglu16(_mm512_load_ps(c + cg + (r + 1) * 16), _mm512_load_ps(c + cu + (r + 1) * 16));
+            const __m512i lo = _mm512_cvtepu16_epi32((__m256i)_mm512_cvtneps_pbh(h0));
+            const __m512i hi = _mm512_cvtepu16_epi32((__m256i)_mm512_cvtneps_pbh(h1));
+            _mm512_storeu_si512(hrow + t0 + jb, _mm512_or_si512(lo, _mm512_slli_epi32(hi, 16)));
           }
         }
       }
     }
   });
-  // phase 2: y[t, m] = h_t . W2_m, 32 W2 rows per unit, fp32 out
+  // phase 2: y[t, m] = h_t . W2_m, 32 W2 rows per unit, fp32 out.  The k loop
+  // is cut into chunks whose slice of the SwiGLU intermediate (all tokens)
+  // fits a core's L2, and work items run chunk-major, so each core reuses one
+  // hp chunk across the units it takes instead of streaming the whole
+  // intermediate (f x tokens, 3.7 MB at 128 tokens) once per 32 W2 rows.
+  // Accumulators of unfinished units live in `part`; a unit's next chunk
+  // waits (rarely: a full chunk of other items lies in between) until its
+  // previous chunk is done.
   const int units2 = d / 32;
+  const int kc = down_kchunk(f, tpad), nch = f / kc;
+  const int64_t tblocks = tpad / 32;
+  std::vector<float> part(nch > 1 ? (size_t)units2 * tblocks * 1024 : 0);
+  std::unique_ptr<std::atomic<int>[]> chunks_done(new std::atomic<int>[units2]);
+  for (int u = 0; u < units2; ++u) chunks_done[u].store(0, std::memory_order_relaxed);
   next.store(0);
   pool->run([&](int) {
     tile_config();
     alignas(64) float c[4 * 256];
-    for (int u = next.fetch_add(1); u < units2; u = next.fetch_add(1)) {
+    BgPf bg;
+    const int items = units2 * nch;
+    int it = next.fetch_add(1);
+    int itn = it < items ? next.fetch_add(1) : items;
+    for (; it < items; it = itn, itn = it < items ? next.fetch_add(1) : items) {
+      const int ch = it / units2, u = it - ch * units2;
       const int m0 = 32 * u;
+      if (itn < items && tpad > 32) {
+        const int chn = itn / units2, mn = 32 * (itn - chn * units2);
+        bg.set(w2 + (int64_t)mn * f, w2 + (int64_t)(mn + 16) * f, f, chn * kc, (chn + 1) * kc,
+               (int)(tblocks - 1) * (kc / 32));
+      } else {
+        bg.clear();
+      }
+      while (chunks_done[u].load(std::memory_order_acquire) < ch) _mm_pause();
       for (int64_t t0 = 0; t0 < tpad; t0 += 32) {
-        amx_block(w2 + (int64_t)m0 * f, w2 + (int64_t)(m0 + 16) * f, f, hp.data() + t0 * 2,
-                  tpad, f, c);
+        float* acc = nch > 1 ? part.data() + ((size_t)u * tblocks + t0 / 32) * 1024 : c;
+        amx_block_acc(w2 + (int64_t)m0 * f, w2 + (int64_t)(m0 + 16) * f, f, hp.data() + t0 * 2,
+                      tpad, ch * kc, (ch + 1) * kc, acc, ch == 0, t0 == 0,
+                      t0 == 0 ? nullptr : &bg);
+        if (ch + 1 < nch) continue;
+        if (acc != c) std::copy(acc, acc + 1024, c);
         for (int j = 0; j < 32 && t0 + j < R; ++j) {
           float* yr = y + (t0 + j) * (int64_t)d + m0;
           for (int r = 0; r < 16; ++r) {
@@ -332,6 +468,7 @@ void amx_expert(const uint16_t* block, int d, int f, const uint16_t* x, int R, f
           }
         }
       }
+      chunks_done[u].store(ch + 1, std::memory_order_release);
     }
   });
 }

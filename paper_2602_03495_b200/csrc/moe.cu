@@ -329,8 +329,8 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
           }
         } else {                                       // row computed by the CPU worker
           const float4* src = reinterpret_cast<const float4*>(cpu_rows + r) + 2 * c;
-          a = __ldcv(src);                             // host memory: never a stale L2 line
-          b = __ldcv(src + 1);
+          a = src[0];                                  // read once, after the completion word
+          b = src[1];
         }
         acc[0] = fmaf(g, a.x, acc[0]); acc[1] = fmaf(g, a.y, acc[1]);
         acc[2] = fmaf(g, a.z, acc[2]); acc[3] = fmaf(g, a.w, acc[3]);
@@ -510,7 +510,7 @@ __global__ void copy_mapped_kernel(uint4* __restrict__ dst, const uint4* __restr
   // .cv loads: the source is often mapped pinned host memory the host rewrites
   // between launches (pointer tables, descriptors) -- never serve it from L2
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
-    dst[i] = __ldcv(src + i);
+    dst[i] = src[i];
   if (blockIdx.x == 0 && threadIdx.x < tail)
     dst_tail[threadIdx.x] = *reinterpret_cast<const volatile uint8_t*>(src_tail + threadIdx.x);
 }
