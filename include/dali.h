@@ -379,7 +379,8 @@ int dali_unpermute_combine(const uint16_t* x, const float* yp,
  * pinned word *rows_ready (stored by the worker's last unit, see
  * dali_cpu_submit_layer) is >= rows_want.  rows_ready NULL = no wait.  The
  * wait is bounded (4 s of device time; dali_host_wait_timeouts counts
- * expiries).  CPU rows are read with ld.global.cv (never a stale L2 line). */
+ * expiries).  The word is polled with ld.global.cv (never a stale L2
+ * line); the rows are read once after it. */
 int dali_unpermute_combine_wait(const uint16_t* x, const float* yp,
                                 const int32_t* topk_idx, const int32_t* pos,
                                 const float* topk_w, const int8_t* gpu_mask,

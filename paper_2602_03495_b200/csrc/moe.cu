@@ -237,10 +237,12 @@ constexpr unsigned long long kQuietCtlNs = 25000;      // one control transfer
 // (dali_cpu_submit_layer) until it reaches `want`, then the CTA reads the rows.
 // One poller per CTA with a ~0.5 us back-off keeps the PCIe read traffic
 // negligible (per-thread polling of the rows themselves was measured to slow
-// the host worker down).  ld.global.cv on every read: a System Memory line
-// the GPU L2 holds is discarded and re-fetched (ld.volatile was measured to
-// return a stale line for seconds now and then, tools/stress_launch_ahead.py).
-// Bounded: after kHostWaitNs the CTA gives up, counts a timeout
+// the host worker down).  The poll uses ld.global.cv, which discards a
+// System Memory line the GPU L2 holds and re-fetches it: repeated
+// ld.volatile reads inside one kernel were measured to return a stale line
+// for seconds now and then (tools/stress_launch_ahead.py).  The rows are then
+// read once with plain loads (.cv there cost 5% at Qwen B=16).  Bounded:
+// after kHostWaitNs the CTA gives up, counts a timeout
 // (dali_host_wait_timeouts) and proceeds.
 __device__ unsigned long long g_host_wait_timeouts = 0;
 constexpr unsigned long long kHostWaitNs = 4000000000ull;
@@ -507,8 +509,9 @@ __global__ void copy_mapped_kernel(uint4* __restrict__ dst, const uint4* __restr
   if (blockIdx.x == 0 && threadIdx.x == 0) pcie_quiet(kQuietCtlNs);
   DALI_PDL_ENTRY();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // .cv loads: the source is often mapped pinned host memory the host rewrites
-  // between launches (pointer tables, descriptors) -- never serve it from L2
+  // plain loads: every source byte is read once per launch (the stale System
+  // Memory lines seen with repeated in-kernel polls do not arise; see
+  // wait_host_word)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
     dst[i] = src[i];
   if (blockIdx.x == 0 && threadIdx.x < tail)
