@@ -30,6 +30,7 @@ the MoE layer lives in ``moe_exec.py``, the decode steps / CUDA graphs in
 
 from __future__ import annotations
 
+import ctypes as C
 import os
 from dataclasses import dataclass, field
 
@@ -219,7 +220,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         self._launch_ahead = os.environ.get("DALI_LAUNCH_AHEAD", "1") == "1"
         self._rows_flag = torch.zeros(2, dtype=torch.int64).pin_memory()
         self._rows_flag_p = self._rows_flag.data_ptr()
-        self._rows_seq = 0
+        self._rows_seq = self._rows_seq_checked = 0
         self._pending_cpu = None              # deferred join of the previous layer
         self._blk_tab = None                  # (L, N) host block addresses (dali_cpu_submit_layer)
         self._sub_args = {}                   # layer -> prebuilt submission arguments
@@ -529,6 +530,15 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
                 self.stats.logits.append(logits.float().cpu())
         e2.record(cs)
         e2.synchronize()
+        if self._rows_seq != self._rows_seq_checked:
+            # a launched-ahead combine that gave up waiting for its CPU rows
+            # (4 s of device time) proceeded with whatever the rows held
+            self._rows_seq_checked = self._rows_seq
+            tmo = C.c_uint64()
+            _lib.call("dali_host_wait_timeouts", C.byref(tmo), 1)
+            if tmo.value:
+                raise SimulationError(f"{tmo.value} decode combines timed out waiting for the "
+                                      "host worker's CPU-expert rows")
         if self.ep is not None and self.ep.peer is not None:
             # a peer lost during the last layers' return exchange only sets the
             # mapped error flag; never hand back rows it left half-written
