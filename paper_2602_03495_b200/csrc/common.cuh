@@ -105,6 +105,52 @@ __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
   return *reinterpret_cast<uint16_t*>(&h);
 }
 
+// Eq. (2) combine arithmetic for one 8-column chunk c of a token row, shared
+// by combine_kernel (moe.cu) and the decode GEMV's fused combine prologue
+// (gemv.cu) so the two produce the same bits: acc += g * (split-K planes of
+// expert-output row r, summed in plane order); then + extra; out = bf16(x + acc).
+__device__ __forceinline__ void combine_add_planes(float (&acc)[8], const float* yp, int splits,
+                                                   int64_t plane, int64_t r, int c, float g) {
+  const float4* src = reinterpret_cast<const float4*>(yp + r) + 2 * c;
+  float4 a = src[0], b = src[1];
+  for (int s = 1; s < splits; ++s) {                     // split-K planes, fixed order
+    const float4* q = reinterpret_cast<const float4*>(yp + s * plane + r) + 2 * c;
+    const float4 a2 = q[0], b2 = q[1];
+    a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
+    b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
+  }
+  acc[0] = fmaf(g, a.x, acc[0]); acc[1] = fmaf(g, a.y, acc[1]);
+  acc[2] = fmaf(g, a.z, acc[2]); acc[3] = fmaf(g, a.w, acc[3]);
+  acc[4] = fmaf(g, b.x, acc[4]); acc[5] = fmaf(g, b.y, acc[5]);
+  acc[6] = fmaf(g, b.z, acc[6]); acc[7] = fmaf(g, b.w, acc[7]);
+}
+__device__ __forceinline__ void combine_add_row(float (&acc)[8], const float* row, int c, float g) {
+  const float4* src = reinterpret_cast<const float4*>(row) + 2 * c;
+  const float4 a = src[0], b = src[1];
+  acc[0] = fmaf(g, a.x, acc[0]); acc[1] = fmaf(g, a.y, acc[1]);
+  acc[2] = fmaf(g, a.z, acc[2]); acc[3] = fmaf(g, a.w, acc[3]);
+  acc[4] = fmaf(g, b.x, acc[4]); acc[5] = fmaf(g, b.y, acc[5]);
+  acc[6] = fmaf(g, b.z, acc[6]); acc[7] = fmaf(g, b.w, acc[7]);
+}
+__device__ __forceinline__ void combine_add_extra(float (&acc)[8], const float* row, int c) {
+  const float4* ex = reinterpret_cast<const float4*>(row) + 2 * c;
+  const float4 a = ex[0], b = ex[1];
+  acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+  acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+}
+__device__ __forceinline__ uint4 combine_finish(const uint4& xv, const float (&acc)[8]) {
+  const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xv);
+  uint4 ov;
+  uint32_t* ow = reinterpret_cast<uint32_t*>(&ov);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float lo = __uint_as_float(xw[q] << 16) + acc[2 * q];
+    const float hi = __uint_as_float(xw[q] & 0xffff0000u) + acc[2 * q + 1];
+    ow[q] = (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
+  }
+  return ov;
+}
+
 template <typename T> __device__ __forceinline__ double to_f64(T v);
 template <> __device__ __forceinline__ double to_f64<double>(double v) { return v; }
 template <> __device__ __forceinline__ double to_f64<uint16_t>(uint16_t v) { return bf16_bits_to_f64(v); }

@@ -317,27 +317,10 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.f;
       auto add_row = [&](bool on_gpu, float g, int64_t r) {
-        if (!on_gpu && !cpu_rows) return;
-        float4 a, b;
-        if (on_gpu) {
-          const float4* src = reinterpret_cast<const float4*>(yp + r) + 2 * c;
-          a = src[0];
-          b = src[1];
-          for (int s = 1; s < splits; ++s) {           // split-K planes, fixed order
-            const float4* q = reinterpret_cast<const float4*>(yp + s * plane + r) + 2 * c;
-            const float4 a2 = q[0], b2 = q[1];
-            a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
-            b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
-          }
-        } else {                                       // row computed by the CPU worker
-          const float4* src = reinterpret_cast<const float4*>(cpu_rows + r) + 2 * c;
-          a = src[0];                                  // read once, after the completion word
-          b = src[1];
-        }
-        acc[0] = fmaf(g, a.x, acc[0]); acc[1] = fmaf(g, a.y, acc[1]);
-        acc[2] = fmaf(g, a.z, acc[2]); acc[3] = fmaf(g, a.w, acc[3]);
-        acc[4] = fmaf(g, b.x, acc[4]); acc[5] = fmaf(g, b.y, acc[5]);
-        acc[6] = fmaf(g, b.z, acc[6]); acc[7] = fmaf(g, b.w, acc[7]);
+        if (on_gpu)
+          combine_add_planes(acc, yp, splits, plane, r, c, g);
+        else if (cpu_rows)                             // row computed by the CPU worker,
+          combine_add_row(acc, cpu_rows + r, c, g);    // read once after the completion word
       };
       if (single) {
 #pragma unroll
@@ -347,22 +330,9 @@ __global__ void combine_kernel(const uint16_t* __restrict__ x, const float* __re
         for (int j = 0; j < k; ++j)
           add_row(!mask || mask[idx[t * k + j]], wts[t * k + j], (int64_t)pos[t * k + j] * d);
       }
-      if (extra) {
-        const float4* ex = reinterpret_cast<const float4*>(extra + t * d) + 2 * c;
-        const float4 a = ex[0], b = ex[1];
-        acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
-        acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
-      }
+      if (extra) combine_add_extra(acc, extra + t * d, c);
       const uint4 xv = single ? xv0 : reinterpret_cast<const uint4*>(x + t * d)[c];
-      const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xv);
-      uint4 ov;
-      uint32_t* ow = reinterpret_cast<uint32_t*>(&ov);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float lo = __uint_as_float(xw[q] << 16) + acc[2 * q];
-        const float hi = __uint_as_float(xw[q] & 0xffff0000u) + acc[2 * q + 1];
-        ow[q] = (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
-      }
+      const uint4 ov = combine_finish(xv, acc);
       reinterpret_cast<uint4*>(out + t * d)[c] = ov;
     }
   }
