@@ -18,7 +18,7 @@ from paper_2602_03495_b200 import _lib  # noqa: E402
 from paper_2602_03495_b200.engine.offload import ffn_splits  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--mode", default="both")
+ap.add_argument("--mode", default="both", help="both | decode | prefill | one | all | decode-sweep | none")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--kernel", default="tc", help="tc | simt")
 ap.add_argument("--check", action="store_true", help="compare with an fp32 torch reference")
@@ -27,11 +27,15 @@ ap.add_argument("--d", type=int, default=4096)
 ap.add_argument("--f", type=int, default=14336)
 ap.add_argument("--splits", type=int, default=0, help="override the split-K planes")
 ap.add_argument("--counts", default=None, help="RxE: R tokens on each of E experts (e.g. 512x8)")
+ap.add_argument("--n", type=int, default=8, help="experts (weight blocks allocated)")
+ap.add_argument("--zipf", default=None,
+                help="TxK: T tokens routed top-K over the n experts with a seeded skewed "
+                     "distribution (DeepSeek-V2-Lite prefill: 4096x6 with --n 64)")
 ap.add_argument("--count-list", default=None, help="explicit per-expert rows, comma-separated")
 ap.add_argument("--graph", type=int, default=0,
                 help="also replay N back-to-back launches captured in one CUDA graph")
 args = ap.parse_args()
-d, f, N = args.d, args.f, 8
+d, f, N = args.d, args.f, args.n
 dev = torch.device("cuda")
 blocks = torch.empty((N, 3 * f * d), dtype=torch.bfloat16, device=dev)
 for e in range(N):
@@ -129,6 +133,15 @@ def run(counts, label):
           f"{flops / ms / 1e9:.1f} TFLOP/s, bytes {byts}")
 
 
+if args.zipf:
+    T_, K_ = (int(x) for x in args.zipf.split("x"))
+    rng = np.random.default_rng(5)
+    pr = 1.0 / np.arange(1, N + 1) ** 0.6
+    pr = rng.permutation(pr / pr.sum())
+    cnt = np.zeros(N, dtype=np.int64)
+    for _ in range(T_):
+        cnt[rng.choice(N, size=K_, replace=False, p=pr)] += 1
+    run(cnt.tolist(), f"zipf {args.zipf} (max {cnt.max()}, min {cnt.min()})")
 if args.counts:
     r_, e_ = (int(x) for x in args.counts.split("x"))
     run([r_] * e_ + [0] * (N - e_), f"counts {args.counts}")
