@@ -14,7 +14,6 @@ import torch
 from .. import _lib
 from ..errors import SimulationError
 from .layers import rms_norm
-_DEBUG_WS = __import__("os").environ.get("DALI_DEBUG_WS", "0") == "1"
 
 
 class DecodeGraphMixin:
@@ -165,8 +164,6 @@ class DecodeGraphMixin:
                 finally:
                     self._capturing = False
                 nk = _lib.launch_count() - k0         # our kernels in the graph body
-                if _DEBUG_WS:
-                    print(f"[ws] captured head {l} step {step} h={h.data_ptr():#x}", flush=True)
                 g.replay()
                 self.graph_kernels += nk
                 heads[l] = (g, h, views, nk)

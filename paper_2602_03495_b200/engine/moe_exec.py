@@ -76,10 +76,10 @@ class MoEExecMixin:
     def _copy_into_staging(self, l: int, e: int, demand: bool = False
                            ) -> tuple[int, torch.cuda.Event]:
         """Expert block (l, e) -> a staging slot on the copy stream.  Demand
-        copies (the GPU expert waits for them: prefill-sized work) use the copy
-        engine's full bandwidth; prefetches, like replacements, use the
-        SM-driven copy that yields the link to the decode path's control
-        transfers (weights.h2d_block)."""
+        copies (the GPU expert waits for them) always use the copy engine;
+        prefetches, like replacements, follow ``EngineConfig.h2d_sm_ctas``
+        (default 0 = copy engine; > 0 = the SM-driven copy of
+        weights.h2d_block)."""
         i = self.staging.get()
         ev_prev = self.staging.free_after[i]
         with torch.cuda.stream(self.copy_stream):

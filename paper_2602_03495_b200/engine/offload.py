@@ -49,8 +49,6 @@ from .moe_exec import MoEExecMixin, ffn_splits  # noqa: F401  (ffn_splits re-exp
 from .weights import ModelWeights
 
 
-_DEBUG_WS = os.environ.get("DALI_DEBUG_WS", "0") == "1"
-
 @dataclass
 class EngineConfig:
     cache_slots_per_layer: int = 0          # 0 = no cache (every GPU expert demand-fetched)
@@ -315,9 +313,6 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         t = self._wsd.get(key)
         if t is None or t.numel() < n:
             if t is not None:
-                if _DEBUG_WS:
-                    print(f"[ws] {name} grows {t.numel()} -> {n} (capturing={self._capturing})",
-                          flush=True)
                 if self._capturing:
                     raise SimulationError(f"workspace {name!r} grew during graph capture")
                 self._ws_retired.append(t)
@@ -329,8 +324,6 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
 
     def _drop_graphs(self) -> None:
         """Forget the captured decode graphs (re-captured on demand)."""
-        if _DEBUG_WS:
-            print(f"[ws] drop graphs ({len(self._heads)} heads)", flush=True)
         self._graph = None
         self._graph_warm = False
         self._heads, self._heads_warm = {}, False
