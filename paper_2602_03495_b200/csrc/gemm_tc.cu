@@ -767,7 +767,8 @@ static int launch_bn(const int32_t* offs, const uint64_t* maps, int N, int d, in
     cudaFuncSetAttribute(ffn_tc_kernel<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
   });
-  const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;   // sum_e ceil(n_e / BN) <= this
+  // sum_e ceil(n_e / BN) <= n + (rows - n) / BN for n >= the experts with rows
+  const int64_t ntile_bound = n_gpu + std::max<int64_t>(rows - n_gpu, 0) / BN;
   const int m_up = (2 * f) / BM, m_dn = d / BM;
   const int64_t g_up = ntile_bound * m_up;
   launch_pdl(ffn_tc_kernel<BN, 0>, dim3((unsigned)g_up), dim3(kThreads), S::BYTES, st, xmap, offs,
@@ -807,7 +808,7 @@ static int launch_persistent(const int32_t* offs, const uint64_t* maps, int N, i
     cudaFuncSetAttribute(ffn_tc_persistent<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
   });
-  const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;
+  const int64_t ntile_bound = n_gpu + std::max<int64_t>(rows - n_gpu, 0) / BN;
   const int m_up = (2 * f) / BM, m_dn = d / BM;
   const unsigned g_up = (unsigned)std::min<int64_t>(ntile_bound * m_up, n_sm);
   const unsigned g_dn = (unsigned)std::min<int64_t>(ntile_bound * m_dn * splits, n_sm);
@@ -850,7 +851,7 @@ static int launch_pair(const int32_t* offs, const uint64_t* maps, int N, int d, 
     cudaFuncSetAttribute(ffn_tc_pair<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)S::BYTES);
   });
-  const int64_t ntile_bound = n_gpu + (rows + BN - 1) / BN;
+  const int64_t ntile_bound = n_gpu + std::max<int64_t>(rows - n_gpu, 0) / BN;
   const int m_up = (2 * f) / BM, m_dn = d / BM;
   const int max_ctas = (n_sm / 2) * 2;
   const unsigned g_up = (unsigned)std::min<int64_t>(2 * ntile_bound * (m_up / 2), max_ctas);
