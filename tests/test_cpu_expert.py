@@ -91,3 +91,59 @@ def test_cpu_expert_prefill_rows_keep_fp32_outputs(d, f, R):
     assert float((err / scale).max()) < 2e-3, float((err / scale).max())
     # and the outputs are not bf16-rounded: most values carry more mantissa bits
     assert float((y != y.to(torch.bfloat16).float()).float().mean()) > 0.9
+
+
+@pytest.mark.skipif(not _has_bf16(), reason="host CPU lacks AVX512-BF16")
+def test_cpu_submit_layer_from_record_and_completion_word():
+    """dali_cpu_submit_layer (launch-ahead decode): the experts the C vector
+    marks, with rows from the offsets, run on the pool and give the rows
+    dali_cpu_expert gives; the completion word receives the sequence number
+    when the last unit ends (at once when no expert has rows); a prefill-sized
+    expert starts nothing and leaves the word alone."""
+    import ctypes as C
+
+    import numpy as np
+
+    d, f, N = 256, 512, 8
+    g = torch.Generator().manual_seed(11)
+    blocks = [(torch.randn(3 * f * d, generator=g) * 0.05).to(torch.bfloat16) for _ in range(N)]
+    tab = np.array([b.data_ptr() for b in blocks], dtype=np.uint64)
+    counts = np.array([1, 0, 2, 1, 0, 3, 1, 0], dtype=np.int32)
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    R = int(offs[-1])
+    x = torch.randn(R, d, generator=g).to(torch.bfloat16)
+    cmask = np.array([1, 1, 0, 1, 0, 1, 0, 0], dtype=np.int8)      # expert 1 has no rows
+    flag = np.zeros(2, dtype=np.uint64)
+    out = torch.full((R, d), 7.0, dtype=torch.float32)
+    n = C.c_int32()
+    _lib.call("dali_cpu_submit_layer", cmask.ctypes.data, offs.ctypes.data, N, tab.ctypes.data,
+              x.data_ptr(), out.data_ptr(), d, f, 4, flag.ctypes.data, 41, C.byref(n))
+    assert n.value == 3                                               # experts 0, 3, 5
+    _lib.call("dali_cpu_expert_wait")
+    assert int(flag[0]) == 41
+    for e in range(N):
+        r0, r1 = int(offs[e]), int(offs[e + 1])
+        if r1 == r0:
+            continue
+        if cmask[e]:
+            ref = torch.empty(r1 - r0, d, dtype=torch.float32)
+            _lib.call("dali_cpu_expert", blocks[e].data_ptr(), d, f, x[r0:r1].data_ptr(),
+                      r1 - r0, ref.data_ptr(), 4)
+            assert torch.equal(out[r0:r1], ref), e
+        else:
+            assert bool((out[r0:r1] == 7.0).all()), e                # GPU experts' rows untouched
+    # no CPU expert with rows: the word is stored at once, nothing to join
+    zero = np.zeros(N, dtype=np.int8)
+    _lib.call("dali_cpu_submit_layer", zero.ctypes.data, offs.ctypes.data, N, tab.ctypes.data,
+              x.data_ptr(), out.data_ptr(), d, f, 4, flag.ctypes.data, 42, C.byref(n))
+    assert n.value == 0 and int(flag[0]) == 42
+    _lib.call("dali_cpu_expert_wait")
+    # a prefill-sized expert (> 16 rows): nothing started, the word untouched
+    big = np.array([0, 17] + [17] * (N - 1), dtype=np.int32)
+    xb = torch.randn(int(big[-1]), d, generator=g).to(torch.bfloat16)
+    outb = torch.empty(int(big[-1]), d, dtype=torch.float32)
+    one = np.zeros(N, dtype=np.int8)
+    one[0] = 1
+    _lib.call("dali_cpu_submit_layer", one.ctypes.data, big.ctypes.data, N, tab.ctypes.data,
+              xb.data_ptr(), outb.data_ptr(), d, f, 4, flag.ctypes.data, 43, C.byref(n))
+    assert n.value == -1 and int(flag[0]) == 42
