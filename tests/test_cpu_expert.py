@@ -18,7 +18,9 @@ def _has_bf16():
 @pytest.mark.skipif(not _has_bf16(), reason="host CPU lacks AVX512-BF16")
 @pytest.mark.parametrize("d,f,R", [(256, 512, 1), (512, 1408, 3), (1024, 2048, 16),
                                    (256, 512, 21), (512, 1408, 64), (256, 512, 100),
-                                   (1024, 2048, 130)])
+                                   (1024, 2048, 130),
+                                   # wide f: the AMX down projection runs in 2 / 7 k chunks
+                                   (256, 14336, 40), (256, 14336, 130)])
 def test_cpu_expert_matches_fp32_reference(d, f, R):
     g = torch.Generator().manual_seed(d + R)
     block = (torch.randn(3 * f * d, generator=g) * 0.05).to(torch.bfloat16)
