@@ -61,3 +61,34 @@ def test_launch_ahead_stress_no_poll_timeouts():
         x = eng._wsd[("dec_X", torch.bfloat16, False)]
         assert bool(torch.isfinite(x).all()), it
     assert _timeouts() == t0
+
+
+def test_sm_driven_h2d_copy_and_engine_option():
+    """Opt-in SM-driven expert copies (EngineConfig.h2d_sm_ctas > 0,
+    dali_copy_h2d_sm): byte-exact against the source for several CTA / unroll
+    settings, and an engine using them for replacements and prefetches makes
+    the same decisions and tokens as the copy-engine default."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200 import _lib
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, build_engine
+    src = torch.randint(0, 256, (3 << 20,), dtype=torch.uint8).pin_memory()
+    st = torch.cuda.current_stream()
+    for nctas in (1, 4, 8 + 64, 16 + 192):
+        dst = torch.zeros(src.numel(), dtype=torch.uint8, device="cuda")
+        _lib.call("dali_copy_h2d_sm", dst.data_ptr(), src.data_ptr(), src.numel(), nctas,
+                  st.cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(dst.cpu(), src), nctas
+    cm = default_cost_model(non_moe_layer_time=3.0)
+    prompt = torch.randint(0, 512, (1, 20), generator=torch.Generator().manual_seed(3))
+    outs = []
+    for n in (0, 4):
+        eng = build_engine("tiny", EngineConfig(cache_slots_per_layer=2, prefetch_size=2, seed=3,
+                                                h2d_sm_ctas=n), seed=5, cost_model=cm, max_seq=96)
+        toks, _ = eng.generate(prompt, 24)
+        outs.append((toks.cpu(), [(r["C"].tolist(), r["G"].tolist(), r["event"])
+                                  for r in eng.policy.decision_log()]))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
