@@ -182,6 +182,9 @@ int dali_route_plan_bf16(const uint16_t* hidden, const uint16_t* gate, const flo
                          int32_t* offsets, int32_t* perm_token, int32_t* pos, uint16_t* xp,
                          void* stream);
 int dali_route_guard_scale(double scale);
+/* A/B hook for T > 16 batches: 0 picks by shape, 1 forces the round-1
+   d-chunked kernel, 2 the fixed-geometry prefill kernel (same outputs). */
+int dali_route_prefill_variant(int32_t variant);
 
 /* Prefetch-set selection: stable top-P of predicted workloads
  * (prefetch.py:153-156).  predicted [dev] (N,) int64 -> set [dev] (P,) i32 */

@@ -80,6 +80,7 @@ SIGNATURES = {
     "dali_route_plan_bf16": [_P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P,
                              _P, _P],
     "dali_route_guard_scale": [C.c_double],
+    "dali_route_prefill_variant": [C.c_int32],
     "dali_greedy": [_P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
     "dali_cost_eval": [_P, _P, _I64, _P, _P, _P],
     "dali_cache_record": [_P, _P, _P, _I32, _I32, _I32, _P, _I32, _P, _P],

@@ -722,6 +722,244 @@ route_guard_kernel(const uint16_t* __restrict__ hidden, const double* __restrict
   if (plan.offsets) plan_gather(plan, topk_idx, hidden, tb_n, k, N, d, sh_hist, sh_cl);
 }
 
+// ---------------------------------------------------------------------------
+// Prefill shape (T > 16, N <= 64): compile-time geometry.  CTA = TB tokens x
+// NP (8 or 64, padded) experts over the whole of d; thread tile 4 tokens x
+// 8 experts, S = 256 / (NP/8 * TB/4) d-slices.  Per chunk of DC router rows
+// (2-stage cp.async ring of raw bf16) the CTA converts the router rows once
+// to fp32 in a [half][row][expert-group][4] layout and the token rows to a
+// transposed fp32 [row][token] tile, so the inner step is three 16-byte
+// shared loads and 32 FFMAs with no per-step conversion or runtime index
+// math.  Summation: KQ-term blocks per chunk flushed into an outer
+// accumulator, pairwise slice tree -- the same certified-height argument
+// and rank_tail as the decode shape.
+template <int TB, int NP>
+struct PCfg {
+  static constexpr int EG = NP / 8, TG = TB / 4, TT = EG * TG, S = kThreads / TT;
+  static constexpr int row_bytes = (NP + TB) * 2;
+  static constexpr int KQ = (S * 16 * row_bytes <= 24576) ? 16
+                            : (S * 8 * row_bytes <= 24576) ? 8 : 4;
+  static constexpr int DC = S * KQ;
+  static constexpr int STG = DC * row_bytes;            // raw: W [DC][N] then x [DC/8][TB][8]
+  static constexpr int WF = DC * NP * 4, XF = DC * TB * 4;
+  static constexpr int UNITS = TB * DC / 8;             // x 16-byte units per chunk
+  static constexpr int XR = (UNITS + kThreads - 1) / kThreads;
+  static constexpr int TILE = TB * NP;
+  static constexpr int RED = S * TILE * 4;
+  static constexpr int MAIN = (2 * STG + WF + XF) > RED ? (2 * STG + WF + XF) : RED;
+  static constexpr int SMEM = MAIN + TILE * 4 + kThreads * 4;
+  static_assert(TT <= kThreads && S * TT == kThreads, "tile threads");
+  static_assert(KQ <= 32, "block height");
+};
+
+template <int TB, int NP>
+__global__ void __launch_bounds__(kThreads, 2)
+route_prefill_kernel(const uint16_t* __restrict__ hidden, const double* __restrict__ residual,
+                     const uint16_t* __restrict__ gate, int64_t T, int d, int N, int k,
+                     int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                     unsigned long long* __restrict__ workloads,
+                     const float* __restrict__ wnorm2, float gamma, int force_fp64) {
+  using P = PCfg<TB, NP>;
+  constexpr int DC = P::DC, S = P::S, EG = P::EG, TG = P::TG, KQ = P::KQ;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* ring = smem;                                   // 2 x STG raw stages
+  float* wF = reinterpret_cast<float*>(smem + 2 * P::STG);     // [2][DC][EG][4]
+  float* xT = wF + DC * NP;                                     // [DC][TB]
+  float* logit = reinterpret_cast<float*>(smem + P::MAIN);      // [TB][NP]
+  float* xnu = logit + P::TILE;                                 // [kThreads] norm partials
+
+  __shared__ float sh_xn[TB], sh_wn[256];
+  __shared__ int sh_hist[256];
+  __shared__ int sh_sel[TB][DALI_MAX_TOPK + 1];
+  __shared__ int sh_bad[TB];
+  __shared__ int sh_flag[TB];
+  __shared__ int sh_nflag;
+  __shared__ double sh_row64[256];
+  __shared__ int sh_cl[256];
+  __shared__ int sh_nc;
+  __shared__ uint32_t sh_cmask[TB][8];
+
+  const int tid = threadIdx.x;
+  const int64_t t0 = (int64_t)blockIdx.x * TB;
+  const int tb_n = (int)((T - t0 < TB) ? (T - t0) : TB);
+  const int nchunks = (d + DC - 1) / DC;
+  for (int i = tid; i < N; i += kThreads) sh_hist[i] = 0;
+  for (int i = tid; i < TB; i += kThreads) sh_bad[i] = 0;
+  if (tid == 0) sh_nflag = 0;
+
+  auto issue_w = [&](int c) {
+    unsigned char* st = ring + (c & 1) * P::STG;
+    const int64_t wbase = (int64_t)c * DC * N, wend = (int64_t)d * N;
+    for (int u = tid; u < DC * N / 8; u += kThreads) {
+      const int64_t el = wbase + (int64_t)u * 8;
+      cp_async16(st + u * 16, el < wend ? gate + el : gate, el < wend);
+    }
+  };
+  auto issue_x = [&](int c) {
+    unsigned char* st = ring + (c & 1) * P::STG + DC * N * 2;
+    for (int u = tid; u < P::UNITS; u += kThreads) {
+      const int t = u % TB, q8 = u / TB;                    // unit-major: [q8][t]
+      const int col = c * DC + q8 * 8;
+      const bool ok = t < tb_n && col < d;
+      cp_async16(st + u * 16, ok ? hidden + (t0 + t) * (int64_t)d + col : hidden, ok);
+    }
+  };
+
+  const int eg = tid % EG, tg = (tid / EG) % TG, s = tid / P::TT;
+  float acc[4][8], blk[4][8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[j][e] = 0.f;
+  float xn_p = 0.f;                                 // token tid % TB (units u = tid + 256 r)
+
+  issue_w(0);                                       // the router does not depend on the predecessor
+  const float wn2v = tid < N ? __ldg(wnorm2 + tid) : 0.f;
+  DALI_PDL_ENTRY();
+  issue_x(0);
+  cp_commit();
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      issue_w(c + 1);
+      issue_x(c + 1);
+    }
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();                                // chunk c landed everywhere; fp32 tiles free
+    const unsigned char* st = ring + (c & 1) * P::STG;
+    {   // router rows -> fp32 [half][row][eg][4], padded experts zero
+      const uint16_t* wr = reinterpret_cast<const uint16_t*>(st);
+      if ((N & 7) == 0) {
+        for (int u = tid; u < DC * N / 8; u += kThreads) {
+          const int i = u / (N / 8), g8 = u - i * (N / 8);
+          const uint4 raw = *reinterpret_cast<const uint4*>(wr + u * 8);
+          float v[8];
+          bf16x2_to_f32(raw.x, v[0], v[1]);
+          bf16x2_to_f32(raw.y, v[2], v[3]);
+          bf16x2_to_f32(raw.z, v[4], v[5]);
+          bf16x2_to_f32(raw.w, v[6], v[7]);
+          *reinterpret_cast<float4*>(wF + (i * EG + g8) * 4) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(wF + ((DC + i) * EG + g8) * 4) =
+              make_float4(v[4], v[5], v[6], v[7]);
+        }
+        if (N < NP) {
+          for (int u = tid; u < DC * (NP - N) / 8; u += kThreads) {
+            const int i = u / ((NP - N) / 8), g8 = N / 8 + u % ((NP - N) / 8);
+            *reinterpret_cast<float4*>(wF + (i * EG + g8) * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(wF + ((DC + i) * EG + g8) * 4) =
+                make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      } else if ((N & 3) == 0) {                    // 4-element units never straddle rows
+        for (int u = tid; u < DC * N / 4; u += kThreads) {
+          const int i = u / (N / 4), j = (u - i * (N / 4)) * 4;
+          const uint2 raw = *reinterpret_cast<const uint2*>(wr + u * 4);
+          float v[4];
+          bf16x2_to_f32(raw.x, v[0], v[1]);
+          bf16x2_to_f32(raw.y, v[2], v[3]);
+          *reinterpret_cast<float4*>(wF + (((j >> 2) & 1) * DC + i) * (NP / 2) + (j >> 3) * 4) =
+              make_float4(v[0], v[1], v[2], v[3]);
+        }
+        for (int u = tid; u < DC * (NP - N) / 4; u += kThreads) {
+          const int i = u / ((NP - N) / 4), j = N + (u % ((NP - N) / 4)) * 4;
+          *reinterpret_cast<float4*>(wF + (((j >> 2) & 1) * DC + i) * (NP / 2) + (j >> 3) * 4) =
+              make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else {
+        for (int u = tid; u < DC * NP; u += kThreads) {
+          const int i = u / NP, j = u - i * NP;
+          const float v = j < N ? __uint_as_float((uint32_t)wr[i * N + j] << 16) : 0.f;
+          wF[(((j >> 2) & 1) * DC + i) * NP / 2 + (j >> 3) * 4 + (j & 3)] = v;
+        }
+      }
+    }
+    {   // token rows -> fp32 transposed [row][token] (+ residual in fp64), norms
+      const uint16_t* xr = reinterpret_cast<const uint16_t*>(st + DC * N * 2);
+#pragma unroll
+      for (int r = 0; r < P::XR; ++r) {
+        const int u = tid + r * kThreads;
+        if (u < P::UNITS) {
+          const int t = u % TB, q8 = u / TB;
+          const uint4 raw = *reinterpret_cast<const uint4*>(xr + u * 8);
+          float v[8];
+          bf16x2_to_f32(raw.x, v[0], v[1]);
+          bf16x2_to_f32(raw.y, v[2], v[3]);
+          bf16x2_to_f32(raw.z, v[4], v[5]);
+          bf16x2_to_f32(raw.w, v[6], v[7]);
+          const int col = c * DC + q8 * 8;
+          if (residual && col < d) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = (float)__dadd_rn((double)v[q], residual[col + q]);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            xn_p = fmaf(v[q], v[q], xn_p);
+            xT[(q8 * 8 + q) * TB + t] = v[q];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // KQ-term block: rows i = s + q*S of this chunk
+    const float* wa = wF + eg * 4;
+    const float* wb = wF + DC * NP / 2 + eg * 4;
+    const float* xa = xT + tg * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) blk[j][e] = 0.f;
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const int i = s + q * S;
+      const float4 w0 = *reinterpret_cast<const float4*>(wa + i * (NP / 2));
+      const float4 w1 = *reinterpret_cast<const float4*>(wb + i * (NP / 2));
+      const float4 xv = *reinterpret_cast<const float4*>(xa + i * TB);
+      const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      const float x[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) blk[j][e] = fmaf(x[j], w[e], blk[j][e]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[j][e] += blk[j][e];
+  }
+  cp_wait<0>();
+  __syncthreads();                                  // ring + fp32 tiles free: slice partials
+  float* red = reinterpret_cast<float*>(smem);      // [S][TB][NP]
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float* dst = red + s * P::TILE + (tg * 4 + j) * NP + eg * 8;
+    *reinterpret_cast<float4*>(dst) = make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
+    *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[j][4], acc[j][5], acc[j][6], acc[j][7]);
+  }
+  xnu[tid] = xn_p;
+  __syncthreads();
+  for (int half = S >> 1; half >= 1; half >>= 1) {  // pairwise slice tree
+    for (int i = tid; i < half * P::TILE; i += kThreads) red[i] += red[i + half * P::TILE];
+    __syncthreads();
+  }
+  for (int i = tid; i < P::TILE; i += kThreads) logit[i] = red[i];
+  if (tid < TB) {
+    float v = 0.f;
+    for (int q = tid; q < kThreads; q += TB) v += xnu[q];
+    sh_xn[tid] = v;
+  }
+  if (tid < N) sh_wn[tid] = sqrtf(wn2v);
+  __syncthreads();
+  TailSmem tsm{sh_hist, sh_sel, sh_flag, &sh_nflag, sh_cmask, sh_bad, sh_row64, sh_cl, &sh_nc};
+  rank_tail<TB>(logit, NP, sh_xn, sh_wn, tb_n, t0, N, k, renorm, gamma, force_fp64, hidden,
+                residual, gate, d, topk_idx, topk_w, reinterpret_cast<double*>(smem), tsm);
+  if (workloads) {
+    for (int i = tid; i < N; i += kThreads) {
+      if (gridDim.x == 1) workloads[i] = (unsigned long long)sh_hist[i];
+      else if (sh_hist[i]) atomicAdd(workloads + i, (unsigned long long)sh_hist[i]);
+    }
+  }
+}
+
 static int ilog2(int x) { int r = 0; while ((1 << (r + 1)) <= x) ++r; return r; }
 
 static Geo make_geo(int TB, int N, int C, int d) {
@@ -756,6 +994,7 @@ static size_t smem_bytes(const Geo& g) {
 }
 
 static double s_guard_scale = 1.0;          // test hook: < 0 forces every row to fp64
+static int s_prefill_variant = 0;           // A/B hook: 0 auto, 1 chunked, 2 fixed-geometry
 
 template <int TB, int C>
 static int launch_tb(const uint16_t* hidden, const double* residual, const uint16_t* gate,
@@ -799,6 +1038,31 @@ static int launch_tb(const uint16_t* hidden, const double* residual, const uint1
   return DALI_OK;
 }
 
+template <int TB, int NP>
+static int launch_prefill(const uint16_t* hidden, const double* residual, const uint16_t* gate,
+                          int64_t T, int d, int N, int k, int renorm, int32_t* idx, float* w,
+                          unsigned long long* wl, const float* wn2, cudaStream_t st) {
+  using P = PCfg<TB, NP>;
+  if ((size_t)(d + 1040) * 8 > (size_t)P::MAIN) return 1;     // fp64 scratch: chunked kernel
+  DALI_ONCE_PER_DEVICE(cudaFuncSetAttribute(route_prefill_kernel<TB, NP>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            P::SMEM));
+  // summation height: a KQ-term block per chunk, one flush per chunk, the
+  // slice tree, and one for a rounded (residual-shifted) input
+  const int nch = (d + P::DC - 1) / P::DC;
+  const int H = P::KQ + nch + ilog2(P::S) + 1;
+  const double u = 1.0 / (1 << 24);
+  double gam = H * u / (1.0 - H * u) + (residual ? 2 * u : 0.0) + 1e-12;
+  gam *= 1.01 * (s_guard_scale > 0 ? s_guard_scale : 1.0);
+  const int force = s_guard_scale < 0;
+  const unsigned grid = (unsigned)((T + TB - 1) / TB);
+  if (wl && grid > 1) cudaMemsetAsync(wl, 0, sizeof(int64_t) * N, st);
+  launch_pdl(route_prefill_kernel<TB, NP>, dim3(grid), dim3(kThreads), (size_t)P::SMEM, st,
+             hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, (float)gam, force);
+  DALI_LAUNCH_CHECK("route_prefill_kernel");
+  return DALI_OK;
+}
+
 }  // namespace rg
 
 // Returns 1 if launched (or T == 0 handled), 0 if the shape is not eligible
@@ -822,7 +1086,7 @@ int launch_route_guarded(const uint16_t* hidden, const double* residual, const u
     return DALI_OK;
   cudaStream_t st = as_stream(stream);
   auto* wl = reinterpret_cast<unsigned long long*>(workloads);
-  int rc;
+  int rc = 1;                                   // 1: not launched yet
   if (T <= 16) {
     int C = 8;
     while (C > 1 && (d % (C * 8) || d / C < 256)) C >>= 1;
@@ -836,7 +1100,22 @@ int launch_route_guarded(const uint16_t* hidden, const double* residual, const u
             : launch_tb<TBv, 1>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st, g, plan))
     rc = TB == 4 ? DALI_RG_SMALL(4) : TB == 8 ? DALI_RG_SMALL(8) : DALI_RG_SMALL(16);
 #undef DALI_RG_SMALL
-  } else {
+  } else if (N <= 64 && s_prefill_variant != 1 &&
+             (s_prefill_variant == 2 || T >= ((N <= 8 || (N & 7)) ? 2048 : 1024))) {
+    // measured (tools/prof_route.py, profiles/r02_route_prefill.txt): 10-25%
+    // faster from ~1k tokens (2k at N <= 8, where each token element feeds
+    // only 8 FMAs and the fp32 staging costs about what it saves, and at
+    // N % 8 != 0, whose router rows convert in 4-element units); below that
+    // the chunked kernel's shorter chunk chain per CTA wins
+    int TB = 4;
+    while (TB < 32 && (T + TB - 1) / TB > 2 * 148) TB <<= 1;   // up to 2 CTAs per SM
+#define DALI_RG_PRE(TBv) (N <= 8 ? launch_prefill<TBv, 8>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st) \
+                         : launch_prefill<TBv, 64>(hidden, residual, gate, T, d, N, k, renorm, idx, w, wl, wn2, st))
+    rc = TB == 4 ? DALI_RG_PRE(4) : TB == 8 ? DALI_RG_PRE(8) : TB == 16 ? DALI_RG_PRE(16)
+                                                               : DALI_RG_PRE(32);
+#undef DALI_RG_PRE
+  }
+  if (T > 16 && rc == 1) {
     int TB = 4;
     while (TB < 32 && (T + TB - 1) / TB > 2 * 148) TB <<= 1;   // up to 2 CTAs per SM
     const Geo g = make_geo(TB, N, 1, d);
@@ -857,6 +1136,11 @@ int launch_route_guarded(const uint16_t* hidden, const double* residual, const u
 
 extern "C" int dali_route_guard_scale(double scale) {
   dali::rg::s_guard_scale = scale;
+  return DALI_OK;
+}
+
+extern "C" int dali_route_prefill_variant(int32_t variant) {
+  dali::rg::s_prefill_variant = variant;
   return DALI_OK;
 }
 

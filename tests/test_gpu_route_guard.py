@@ -177,3 +177,45 @@ def test_route_plan_fused_matches_separate(lib, d, N, k, force):
                 assert torch.equal(x_, y_), (T, d, N, k)
     finally:
         lib.call("dali_route_guard_scale", 1.0)
+
+
+@pytest.mark.parametrize("d,N,k", [(4096, 8, 2), (2048, 64, 6), (2048, 60, 4), (6144, 8, 2),
+                                   (256, 16, 4), (1024, 32, 4)])
+def test_prefill_kernel_matches_chunked_kernel_and_oracle(lib, d, N, k):
+    """T > 16 with N <= 64: the fixed-geometry prefill kernel (4..32 tokens
+    per CTA, fp32 operand tiles; dali_route_prefill_variant(2) forces it at
+    every T) against the round-1 d-chunked kernel (variant 1).  Indices and workloads equal each other
+    and the fp64 oracle, weights to fp32 rounding, at every token-tile size;
+    the forced-fp64 path too."""
+    import torch
+    for T in (17, 100, 300, 700, 1300, 2100, 4096):
+        h, w = _inputs(T, d, N, seed=T * 3 + d + N)
+        res = None
+        if T == 700:
+            res = np.random.default_rng(T).normal(size=d) * 0.1
+        lib.call("dali_route_prefill_variant", 2)
+        try:
+            new = _route(h, w, k, res=res)
+            lib.call("dali_route_prefill_variant", 1)
+            old = _route(h, w, k, res=res)
+        finally:
+            lib.call("dali_route_prefill_variant", 0)
+        o_idx, o_sc, o_wl = _oracle(h, w, k, res=res)
+        assert np.array_equal(new[0], o_idx), (T, d, N)
+        assert np.array_equal(new[2], o_wl), (T, d, N)
+        assert np.array_equal(new[0], old[0]) and np.array_equal(new[2], old[2])
+        np.testing.assert_allclose(new[1], old[1], rtol=2e-6, atol=1e-7)
+        if T in (100, 1300):
+            lib.route_fire_count(reset=True)
+            lib.call("dali_route_guard_scale", -1.0)
+            lib.call("dali_route_prefill_variant", 2)
+            try:
+                f = _route(h, w, k, res=res)
+            finally:
+                lib.call("dali_route_guard_scale", 1.0)
+                lib.call("dali_route_prefill_variant", 0)
+            fires, rows = lib.route_fire_count(reset=True)
+            assert fires == rows == T
+            assert np.array_equal(f[0], o_idx) and np.array_equal(f[2], o_wl)
+            np.testing.assert_allclose(f[1], new[1], rtol=2e-6, atol=1e-7)
+    torch.cuda.synchronize()

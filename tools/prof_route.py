@@ -18,7 +18,13 @@ ap.add_argument("--N", type=int, default=8)
 ap.add_argument("--k", type=int, default=2)
 ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--T", type=str, default="1,4,16,128,512,4096")
+ap.add_argument("--prefill-variant", type=int, default=0,
+                help="T > 16: 0 by shape, 1 d-chunked kernel, 2 fixed-geometry kernel")
+ap.add_argument("--force", action="store_true", help="every row through the fp64 recompute")
 args = ap.parse_args()
+_lib.call("dali_route_prefill_variant", args.prefill_variant)
+_lib.call("dali_route_guard_scale", -1.0 if args.force else 1.0)
+torch.manual_seed(0)
 g = (torch.randn(args.d, args.N, device="cuda") * 0.02).to(torch.bfloat16)
 n2 = gate_norm2(g)             # the engine computes router norms once
 for T in [int(x) for x in args.T.split(",")]:
