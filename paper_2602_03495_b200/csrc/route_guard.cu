@@ -126,41 +126,96 @@ __device__ void fp64_row_cand(const uint16_t* __restrict__ hrow,
     }
     if (tid == 0) *sh_nc = base;
   }
-  for (int i = tid; i < d; i += kThreads) {      // the row in fp64 (+ residual), once
-    double x = bf16_to_f64_fast(hrow[i]);
-    if (residual) x = __dadd_rn(x, residual[i]);
-    xs64[i] = x;
-  }
   __syncthreads();
+  RG_MARK(9);
   const int nc = *sh_nc;
-  int S = 1;
-  while (2 * S * nc <= kThreads) S *= 2;         // power-of-two slices per candidate
-  const int c = tid % nc, sl = tid / nc;
-  if (sl < S) {
-    const int e = sh_cl[c];
+  if (nc <= 16) {
+    // Few candidates (the normal fire): a warp step covers R = 32 / nc
+    // router rows, lane = (row r, candidate c), so one load instruction
+    // touches R rows' lines (not 32) and the row element is a broadcast.
+    // Each thread loads its rows and router elements straight from global
+    // (16 in flight, no staging pass); partials meet in a fixed order.
+    const int R = 32 / nc;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int r = lane / nc, c = lane - r * nc;
     double acc0 = 0.0, acc1 = 0.0;
-    constexpr int kB = 16;                      // router loads in flight per thread
-    for (int i0 = sl; i0 < d; i0 += kB * S) {
-      uint16_t w[kB];
+    if (r < R) {
+      const uint16_t* gcol = gate + sh_cl[c];
+      constexpr int kB = 16;
+      const int stride = (kThreads / 32) * R;    // rows per CTA step
+      int i0 = warp * R + r;
+#pragma unroll 2
+      for (; i0 + (kB - 1) * stride < d; i0 += kB * stride) {
+        uint16_t w[kB], xb[kB];
 #pragma unroll
-      for (int b = 0; b < kB; ++b) {
-        const int i = i0 + b * S;
-        w[b] = i < d ? __ldg(gate + (int64_t)i * N + e) : (uint16_t)0;
+        for (int b = 0; b < kB; ++b) {
+          w[b] = __ldg(gcol + (int64_t)(i0 + b * stride) * N);
+          xb[b] = hrow[i0 + b * stride];
+        }
+#pragma unroll
+        for (int b = 0; b < kB; b += 2) {
+          double x0 = bf16_to_f64_fast(xb[b]), x1 = bf16_to_f64_fast(xb[b + 1]);
+          if (residual) {
+            x0 = __dadd_rn(x0, residual[i0 + b * stride]);
+            x1 = __dadd_rn(x1, residual[i0 + (b + 1) * stride]);
+          }
+          acc0 = fma(x0, bf16_to_f64_fast(w[b]), acc0);
+          acc1 = fma(x1, bf16_to_f64_fast(w[b + 1]), acc1);
+        }
       }
-#pragma unroll
-      for (int b = 0; b < kB; b += 2) {
-        const int i = i0 + b * S;
-        if (i < d) acc0 = fma(xs64[i], bf16_to_f64_fast(w[b]), acc0);
-        if (i + S < d) acc1 = fma(xs64[i + S], bf16_to_f64_fast(w[b + 1]), acc1);
+      for (int i = i0; i < d; i += stride) {
+        double x = bf16_to_f64_fast(hrow[i]);
+        if (residual) x = __dadd_rn(x, residual[i]);
+        acc0 = fma(x, bf16_to_f64_fast(__ldg(gcol + (int64_t)i * N)), acc0);
       }
     }
-    sh_part[sl * nc + c] = acc0 + acc1;
-  }
-  __syncthreads();
-  for (int half = S >> 1; half >= 1; half >>= 1) {
-    for (int i = tid; i < half * nc; i += kThreads) sh_part[i] += sh_part[i + half * nc];
+    double* part = sh_part + 64;                  // [kThreads]
+    part[tid] = acc0 + acc1;
     __syncthreads();
+    if (tid < nc) {
+      double t = 0.0;
+      for (int q = 0; q < kThreads / 32; ++q)
+        for (int rr = 0; rr < R; ++rr) t += part[q * 32 + rr * nc + tid];
+      sh_part[tid] = t;                           // candidate logits, list order
+    }
+    __syncthreads();
+  } else {
+    for (int i = tid; i < d; i += kThreads) {      // the row in fp64 (+ residual), once
+      double x = bf16_to_f64_fast(hrow[i]);
+      if (residual) x = __dadd_rn(x, residual[i]);
+      xs64[i] = x;
+    }
+    __syncthreads();
+    int S = 1;
+    while (2 * S * nc <= kThreads) S *= 2;         // power-of-two slices per candidate
+    const int c = tid % nc, sl = tid / nc;
+    if (sl < S) {
+      const int e = sh_cl[c];
+      double acc0 = 0.0, acc1 = 0.0;
+      constexpr int kB = 16;                      // router loads in flight per thread
+      for (int i0 = sl; i0 < d; i0 += kB * S) {
+        uint16_t w[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int i = i0 + b * S;
+          w[b] = i < d ? __ldg(gate + (int64_t)i * N + e) : (uint16_t)0;
+        }
+#pragma unroll
+        for (int b = 0; b < kB; b += 2) {
+          const int i = i0 + b * S;
+          if (i < d) acc0 = fma(xs64[i], bf16_to_f64_fast(w[b]), acc0);
+          if (i + S < d) acc1 = fma(xs64[i + S], bf16_to_f64_fast(w[b + 1]), acc1);
+        }
+      }
+      sh_part[sl * nc + c] = acc0 + acc1;
+    }
+    __syncthreads();
+    for (int half = S >> 1; half >= 1; half >>= 1) {
+      for (int i = tid; i < half * nc; i += kThreads) sh_part[i] += sh_part[i + half * nc];
+      __syncthreads();
+    }
   }
+  RG_MARK(10);
   if (tid < 32) {
     const int lane = tid;
     // logits: fp64 for candidates, fp32 for the rest (denominator only)

@@ -21,9 +21,11 @@ ap.add_argument("--T", type=str, default="1,4,16,128,512,4096")
 ap.add_argument("--prefill-variant", type=int, default=0,
                 help="T > 16: 0 by shape, 1 d-chunked kernel, 2 fixed-geometry kernel")
 ap.add_argument("--force", action="store_true", help="every row through the fp64 recompute")
+ap.add_argument("--scale", type=float, default=1.0,
+                help="bound scale (diagnostic: << 1 suppresses fires to time the fire-free kernel)")
 args = ap.parse_args()
 _lib.call("dali_route_prefill_variant", args.prefill_variant)
-_lib.call("dali_route_guard_scale", -1.0 if args.force else 1.0)
+_lib.call("dali_route_guard_scale", -1.0 if args.force else args.scale)
 torch.manual_seed(0)
 g = (torch.randn(args.d, args.N, device="cuda") * 0.02).to(torch.bfloat16)
 n2 = gate_norm2(g)             # the engine computes router norms once
