@@ -625,7 +625,8 @@ def run_dali(args, ws, rank, local):
                                  "link": "PCIe Gen5 x16 (64 GB/s nominal per direction)"}
                                 if eng.cm.trans_time > 0 else None),
             "copies_per_step": {k: float(np.mean([getattr(s, k) for s in st_v])) for k in
-                                ("demand_copies", "prefetch_copies", "replace_copies")},
+                                ("demand_copies", "prefetch_copies", "replace_copies",
+                                 "replace_urgent", "replace_dropped")},
             "host_ms_per_step": {k: round(float(np.mean([s.host_ms.get(k, 0.0) for s in st_v])), 2)
                                  for k in ("launch_pre", "wait_decision", "dispatch_gpu",
                                            "cpu_experts")},

@@ -191,6 +191,8 @@ class MoEExecMixin:
                 continue
             s = self.host_slot[l, e]
             if s >= 0:
+                if s in self._repl_slot:           # admitted, copy not issued yet
+                    self._issue_repl(s, urgent=True)
                 ptrs[e] = self.cache_buf[s].data_ptr()
                 maps[e] = self._map_addr(s)
                 if self.slot_ready[s] is not None:
@@ -265,7 +267,13 @@ class MoEExecMixin:
                 self.stats.prefetch_copies += 1
             self._apply_inserts(l, rec, None, None, now=False)
             # replacement: admitted experts into the victims' slots once read
-            if rec.ev_valid and rec.ev_n:
+            if rec.ev_valid and rec.ev_n and self.cfg.lazy_replace:
+                for j in range(rec.ev_n):
+                    v_, c_ = int(rec.evicted[j]), int(rec.admitted[j])
+                    s = int(self.host_slot[l, v_])
+                    self._defer_repl(l, s, c_, ffn_done)
+                    self.host_slot[l, c_], self.host_slot[l, v_] = s, -1
+            elif rec.ev_valid and rec.ev_n:
                 with torch.cuda.stream(self.repl_stream):
                     self.repl_stream.wait_event(ffn_done)
                     for j in range(rec.ev_n):
@@ -279,10 +287,77 @@ class MoEExecMixin:
                         ev = torch.cuda.Event()
                         ev.record(self.repl_stream)
                         self.slot_ready[s] = ev
+        if self._repl_slot:
+            self._pump_repl(l)
         self._last_exec = dict(hit=n_hit, pf=n_pf, dem=n_dem, t0=t0_ev,
                                rep=int(rec.ev_n) if (rec.ev_valid and not self.resident_mode) else 0,
                                done=int(rec.n_done) if not self.resident_mode else 0)
         return yp, splits, pd.data_ptr() + NL * 16
+
+    # ------------------------------------------------ deferred replacements
+    # EngineConfig.lazy_replace: a window replacement (the workload-aware
+    # cache admitting expert c into the victim's slot, simulator.py window
+    # swap) is recorded here instead of being copied at once.  The copy is
+    # issued (a) at once, on the demand stream, when a later decision hits
+    # that slot, or (b) in the background, at most REPL_INFLIGHT at a time,
+    # in next-use order (the layers after the current one first).  A slot
+    # whose pending admission is evicted again before any read is never
+    # copied.  The decisions and the bytes every FFN reads are unchanged;
+    # what changes is that a boundary token's ~8 admissions per layer no
+    # longer sit in one FIFO in front of the few the next token hits.
+    REPL_INFLIGHT = 2
+
+    def _defer_repl(self, l: int, s: int, expert: int, ev_free) -> None:
+        if s in self._repl_slot:                   # superseded before any read
+            self._drop_repl(s)
+            self.stats.replace_dropped += 1
+        self._repl_pend[l][s] = (expert, ev_free)
+        self._repl_slot[s] = l
+
+    def _drop_repl(self, s: int) -> None:
+        l = self._repl_slot.pop(s, None)
+        if l is not None:
+            del self._repl_pend[l][s]
+
+    def _issue_repl(self, s: int, urgent: bool) -> None:
+        l = self._repl_slot.pop(s)
+        expert, ev_free = self._repl_pend[l].pop(s)
+        st = self.copy_stream if urgent else self.repl_stream
+        st.wait_event(ev_free)                     # the victim's last read
+        if self.slot_ready[s] is not None:         # an earlier copy into the slot
+            st.wait_event(self.slot_ready[s])
+        h2d_block(self.cache_buf[s], self._host_block(l, expert), st, self.cfg.h2d_sm_ctas)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        self.slot_ready[s] = ev
+        self.stats.h2d_bytes += self.w.expert_bytes
+        self.stats.replace_copies += 1
+        if urgent:
+            self.stats.replace_urgent += 1
+        else:
+            self._repl_inflight.append(ev)
+
+    def _pump_repl(self, l: int) -> None:
+        """Keep REPL_INFLIGHT background replacement copies in flight, next
+        use first: layers l+1, l+2, ... (wrapping into the next token)."""
+        q = self._repl_inflight
+        while q and q[0].query():
+            q.popleft()
+        budget = self.REPL_INFLIGHT - len(q)
+        L = self.arch.num_layers
+        for dl in range(1, L + 1):
+            if budget <= 0 or not self._repl_slot:
+                return
+            pend = self._repl_pend[(l + dl) % L]
+            while pend and budget > 0:
+                self._issue_repl(next(iter(pend)), urgent=False)
+                budget -= 1
+
+    def flush_replacements(self) -> None:
+        """Issue every deferred replacement copy (background stream)."""
+        for l in range(self.arch.num_layers):
+            while self._repl_pend[l]:
+                self._issue_repl(next(iter(self._repl_pend[l])), urgent=False)
 
     def _apply_inserts(self, l: int, rec, stage_of, ffn_done, now: bool) -> set:
         """Execute the cache insertions the policy kernel made outside the
@@ -319,7 +394,12 @@ class MoEExecMixin:
             ll = l + 1 if kind == 2 else l
             v, x = int(rec.ins_victim[j]), int(rec.ins_expert[j])
             s = int(self.host_slot[ll, v])
+            if s in self._repl_slot:               # its pending admission is evicted
+                self._drop_repl(s)
+                self.stats.replace_dropped += 1
             with torch.cuda.stream(self.repl_stream):
+                if self.slot_ready[s] is not None:
+                    self.repl_stream.wait_event(self.slot_ready[s])
                 if kind == 2:
                     i, ev_src = self.prefetched.pop((ll, x))
                     self.repl_stream.wait_event(ev_src)

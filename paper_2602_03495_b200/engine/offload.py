@@ -30,6 +30,7 @@ the MoE layer lives in ``moe_exec.py``, the decode steps / CUDA graphs in
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import os
 from dataclasses import dataclass, field
@@ -96,6 +97,10 @@ class EngineConfig:
     #                                         many SMs (bounded PCIe queue depth, paused in
     #                                         the decode chain's quiet window); 0 = copy
     #                                         engine (default: measured faster end to end)
+    lazy_replace: bool = os.environ.get("DALI_LAZY_REPLACE", "1") != "0"
+    #                                         window replacement copies deferred: issued when
+    #                                         a hit needs the slot, else in the background in
+    #                                         next-use order (MoEExecMixin._defer_repl)
 
 
 @dataclass
@@ -109,6 +114,8 @@ class RunStats:
     prefetch_copies: int = 0
     replace_copies: int = 0
     insert_copies: int = 0                 # D2D staging -> slot (baseline cache policies)
+    replace_urgent: int = 0                # deferred replacements issued by a hit
+    replace_dropped: int = 0               # deferred replacements superseded before a read
     cpu_expert_calls: int = 0
     gpu_expert_calls: int = 0
     decode_host_bytes: int = 0             # expert bytes read from host DRAM while decoding
@@ -197,6 +204,9 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
                                       device=self.dev) if slots else None)
         self.host_slot = self.policy.slot_of.cpu().numpy().copy()
         self.slot_ready = [None] * (L * slots)   # per cache slot: last replacement copy
+        self._repl_pend = [dict() for _ in range(L)]   # layer -> {slot: (expert, victim read)}
+        self._repl_slot: dict = {}                      # slot -> layer of its pending copy
+        self._repl_inflight = collections.deque()       # background copies in flight
         n_stage = cfg.staging_slots or (0 if self.resident_mode else
                                         max(2 * k, N) + 2 * max(cfg.prefetch_size, 1) + 2)
         self.staging = _Staging(n_stage, weights.expert_bytes, self.dev) if n_stage else None
@@ -362,6 +372,9 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         pol.slot_of.copy_(torch.from_numpy(slot))
         self.host_slot = slot.copy()
         self.slot_ready = [None] * (L * cap)
+        self._repl_pend = [dict() for _ in range(L)]
+        self._repl_slot = {}
+        self._repl_inflight = collections.deque()
         for key in list(self.prefetched):
             i, ev = self.prefetched.pop(key)
             self.staging.release(i, ev)
