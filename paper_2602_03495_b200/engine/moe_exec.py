@@ -299,13 +299,22 @@ class MoEExecMixin:
     # cache admitting expert c into the victim's slot, simulator.py window
     # swap) is recorded here instead of being copied at once.  The copy is
     # issued (a) at once, on the demand stream, when a later decision hits
-    # that slot, or (b) in the background, at most REPL_INFLIGHT at a time,
+    # that slot, or (b) in the background, at most `_repl_max` at a time,
     # in next-use order (the layers after the current one first).  A slot
     # whose pending admission is evicted again before any read is never
     # copied.  The decisions and the bytes every FFN reads are unchanged;
     # what changes is that a boundary token's ~8 admissions per layer no
     # longer sit in one FIFO in front of the few the next token hits.
-    REPL_INFLIGHT = 2
+    # Background depth (EngineConfig.repl_inflight, -1 = by block size): 0 --
+    # copy only on a hit -- for blocks that cross PCIe in well under a layer
+    # (DSV2 17 MB, Qwen 8 MB: background copies only compete with the
+    # critical demand copies; measured 0 > 1 > 2 > 4), 1 for blocks that take
+    # longer than a layer (Mixtral 352 MB, 6.3 ms: a copy started on the hit
+    # would stall the layer for all of it).
+    @property
+    def _repl_max(self) -> int:
+        n = self.cfg.repl_inflight
+        return n if n >= 0 else (0 if self.w.expert_bytes <= (64 << 20) else 1)
 
     def _defer_repl(self, l: int, s: int, expert: int, ev_free) -> None:
         if s in self._repl_slot:                   # superseded before any read
@@ -338,12 +347,12 @@ class MoEExecMixin:
             self._repl_inflight.append(ev)
 
     def _pump_repl(self, l: int) -> None:
-        """Keep REPL_INFLIGHT background replacement copies in flight, next
+        """Keep `_repl_max` background replacement copies in flight, next
         use first: layers l+1, l+2, ... (wrapping into the next token)."""
         q = self._repl_inflight
         while q and q[0].query():
             q.popleft()
-        budget = self.REPL_INFLIGHT - len(q)
+        budget = self._repl_max - len(q)
         L = self.arch.num_layers
         for dl in range(1, L + 1):
             if budget <= 0 or not self._repl_slot:

@@ -101,6 +101,9 @@ class EngineConfig:
     #                                         window replacement copies deferred: issued when
     #                                         a hit needs the slot, else in the background in
     #                                         next-use order (MoEExecMixin._defer_repl)
+    repl_inflight: int = int(os.environ.get("DALI_REPL_INFLIGHT", "-1"))
+    #                                         deferred replacements copied in the background
+    #                                         at a time (-1: 0 for blocks <= 64 MB, else 1)
 
 
 @dataclass

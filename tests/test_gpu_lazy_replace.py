@@ -33,9 +33,8 @@ def test_lazy_replace_identical(model, slots, pf, w, inflight):
     for lazy in (False, True):
         eng = build_engine(model, EngineConfig(cache_slots_per_layer=slots, prefetch_size=pf,
                                                w_size=w, seed=3, lazy_replace=lazy,
-                                               capture_moe_io=True),
+                                               repl_inflight=inflight, capture_moe_io=True),
                            seed=5, cost_model=cm, max_seq=128)
-        eng.REPL_INFLIGHT = inflight
         out = []
         for p in prompts:                       # two requests: pending copies carry over
             toks, st = eng.generate(p, 40)
