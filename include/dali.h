@@ -399,6 +399,12 @@ int dali_host_wait_timeouts(uint64_t* out, int32_t reset);
  * queue behind expert-block DMA.  16-byte aligned pointers take the vector
  * path; unaligned copies are byte-wise and limited to 1 MiB. */
 int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream);
+/* Engine plumbing: cudaMemcpyAsync(cudaMemcpyDefault) of nbytes on `stream`
+ * -- the copy-engine expert-block transfers (pinned host store -> HBM cache
+ * slot / staging slot) without a host-side stream switch.  The H2D leg of
+ * the prefetch and cache-replacement transfers (simulator.py:398-420 times
+ * them; moesim moves no bytes). */
+int dali_memcpy_async(void* dst, const void* src, size_t nbytes, void* stream);
 
 /* Engine plumbing: bulk host->device copy (expert blocks) driven by `nctas`
  * CTAs of 512 threads reading mapped pinned memory, instead of a copy engine.

@@ -104,6 +104,7 @@ SIGNATURES = {
     "dali_cpu_submit_layer": [_P, _P, _I32, _P, _P, _P, _I32, _I32, _I32, _P, C.c_uint64, _P],
     "dali_expert_ffn_tc": [_P, _P, _I32, _P, _I32, _I32, _I64, _I32, _I32, _P, _P, _I32, _P],
     "dali_expert_maps": [_P, _I32, _I32, _P],
+    "dali_memcpy_async": [_P, _P, C.c_size_t, _P],
     "dali_init_uniform_bf16": [_P, _I64, C.c_uint64, C.c_uint64, C.c_float, _P],
     "dali_host_alloc": [C.c_size_t, _I32, C.POINTER(C.c_void_p)],
     "dali_host_free": [_P, C.c_size_t],
@@ -179,10 +180,17 @@ def check(status: int, where: str) -> None:
     raise cls(f"{where}: {msg}")
 
 
+_FNS: dict = {}
+
+
 def call(name: str, *args) -> None:
     """Invoke a status-returning entry point and raise on failure."""
-    fn = getattr(load(), name)
-    check(fn(*args), name)
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(load(), name)
+    st = fn(*args)
+    if st:
+        check(st, name)
 
 
 def launch_count() -> int:

@@ -540,6 +540,14 @@ extern "C" int dali_copy_h2d_sm(void* dst, const void* src, int64_t nbytes, int3
   return DALI_OK;
 }
 
+extern "C" int dali_memcpy_async(void* dst, const void* src, size_t nbytes, void* stream) {
+  if (nbytes == 0) return DALI_OK;
+  DALI_REQUIRE(dst && src, DALI_ECUDA, "dali_memcpy_async: null pointer");
+  const cudaError_t e = cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, as_stream(stream));
+  DALI_REQUIRE(e == cudaSuccess, DALI_ECUDA, "dali_memcpy_async: %s", cudaGetErrorString(e));
+  return DALI_OK;
+}
+
 extern "C" int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream) {
   if (nbytes <= 0) return DALI_OK;
   DALI_REQUIRE(dst && src, DALI_ECUDA, "dali_copy_mapped: null pointer");

@@ -46,8 +46,9 @@ def ffn_splits(max_rows: int, tiles: int, kb: int, n_sm: int) -> int:
 
 
 class MoEExecMixin:
-    def _shared_ffn(self, l: int, h: torch.Tensor) -> torch.Tensor:
-        """Shared expert(s) of layer l over all T tokens -> (T, d) f32."""
+    def _shared_ffn(self, l: int, h: torch.Tensor, stream=None) -> torch.Tensor:
+        """Shared expert(s) of layer l over all T tokens -> (T, d) f32, on
+        ``stream`` (default: the compute stream)."""
         a = self.arch
         T, d, fs = h.shape[0], a.hidden_dim, a.shared_ffn_dim
         offs = self._offs_cache.get(T)
@@ -60,10 +61,12 @@ class MoEExecMixin:
         sp = ffn_splits(T, tiles, kb, self.n_sm)
         hs = self._ws("sh_h", (T, fs), torch.bfloat16)
         ys = self._ws("sh_y", (sp, T, d), torch.float32)
-        cs = self._cur()
+        cs = self._cur() if stream is None else stream
         _lib.call("dali_expert_ffn_tc", h.data_ptr(), offs.data_ptr(), 1,
                   self.shared_map_ptr.data_ptr() + 8 * l, d, fs, T, T, 1, hs.data_ptr(),
                   ys.data_ptr(), sp, cs.cuda_stream)
+        if stream is not None:
+            cs = stream
         y = self._ws("sh_out", (T, d), torch.float32)
         _lib.call("dali_shared_finish", ys.data_ptr(), sp, T, d, h.data_ptr(),
                   self.w.shared_gate[l].data_ptr() if a.shared_gate else None, y.data_ptr(),
@@ -82,13 +85,12 @@ class MoEExecMixin:
         weights.h2d_block)."""
         i = self.staging.get()
         ev_prev = self.staging.free_after[i]
-        with torch.cuda.stream(self.copy_stream):
-            if ev_prev is not None:
-                self.copy_stream.wait_event(ev_prev)
-            h2d_block(self.staging.buf[i], self._host_block(l, e), self.copy_stream,
-                      0 if demand else self.cfg.h2d_sm_ctas)
-            ev = torch.cuda.Event()
-            ev.record(self.copy_stream)
+        if ev_prev is not None:
+            self.copy_stream.wait_event(ev_prev)
+        h2d_block(self.staging.buf[i], self._host_block(l, e), self.copy_stream,
+                  0 if demand else self.cfg.h2d_sm_ctas)
+        ev = torch.cuda.Event()
+        ev.record(self.copy_stream)
         self.stats.h2d_bytes += self.w.expert_bytes
         return i, ev
 
@@ -579,6 +581,16 @@ class MoEExecMixin:
         T = h.shape[0]
         R = T * k
         cs = self._cur()
+        ev_sh = y_shared = None
+        if self.shared_map_ptr is not None and self.cfg.shared_in_head:
+            # the shared expert(s) need only h: they run on a side stream beside
+            # routing + policy (joined at the end of the head, inside the
+            # per-layer decode graph), off the host's post-decision critical path
+            ss = self.shared_stream
+            ss.wait_stream(cs)
+            y_shared = self._shared_ffn(l, h, stream=ss)
+            ev_sh = torch.cuda.Event()
+            ev_sh.record(ss)
         v = self._route(l, h)
         gate_next = self.w.router[l + 1] if l + 1 < a.num_layers else None
         nn2 = self.w.router_norm2[l + 1] if l + 1 < a.num_layers else None
@@ -603,7 +615,9 @@ class MoEExecMixin:
         if self.cfg.capture:
             h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
             h_host.copy_(h, non_blocking=True)
-        return dict(v=v, hv=hv, xp_host=xp_host, h_host=h_host, ri=ri, T=T)
+        if ev_sh is not None:
+            cs.wait_event(ev_sh)
+        return dict(v=v, hv=hv, xp_host=xp_host, h_host=h_host, ri=ri, T=T, y_shared=y_shared)
 
     def _moe_tail(self, l: int, x: torch.Tensor, h: torch.Tensor, step: int, views: dict,
                   tp0: float, ev_r, out: torch.Tensor, ahead: bool = False) -> torch.Tensor:
@@ -650,7 +664,9 @@ class MoEExecMixin:
                 self.stats.captured.append((step, l, views["h_host"].clone()))
                 self.stats.topk[(step, l)] = hv["idx"].numpy().astype(np.int64).copy()
             yp, splits, gmask_p = self._exec_local(l, v["xp"], v["offsets"], wl_np, rec, R)
-            y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+            y_shared = views.get("y_shared")
+            if y_shared is None and self.shared_map_ptr is not None:
+                y_shared = self._shared_ffn(l, h)
         except BaseException:
             if job is not None and job["native"]:
                 _lib.load().dali_cpu_expert_wait()     # never leave a job in flight

@@ -85,6 +85,11 @@ class EngineConfig:
     fused_route_plan: bool = os.environ.get("DALI_FUSED_ROUTE_PLAN", "1") != "0"
     #                                         decode (T <= 16): routing + plan + permute in
     #                                         one launch (dali_route_plan_bf16)
+    shared_in_head: bool = os.environ.get("DALI_SHARED_HEAD", "1") != "0"
+    #                                         offloaded MoE layer: the shared expert(s) run
+    #                                         on a side stream beside routing + policy (in
+    #                                         the per-layer decode graph), not after the
+    #                                         host has read the decision
     fused_norm_gemv: bool = os.environ.get("DALI_FUSED_NORM", "1") != "0"
     #                                         decode (B <= 8): attention-block RMSNorms fused
     #                                         into the qkv / o projection GEMVs
@@ -198,6 +203,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
             frequency_table=cfg.frequency_table)
         self.copy_stream = torch.cuda.Stream()       # demand + prefetch expert copies
         self._gemv_ctr = None                        # fused o-projection + norm counter
+        self.shared_stream = torch.cuda.Stream()     # shared experts beside routing (head)
         self.policy_stream = torch.cuda.Stream()     # all-resident decode: policy records
         self._policy_side_used = False
         self.repl_stream = torch.cuda.Stream()       # cache replacement copies (off the
@@ -262,6 +268,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
                 device=self.dev)
         self._offs_cache: dict = {}
         self._wsd: dict = {}
+        self._wsv: dict = {}                    # (name, shape, dtype, pinned) -> view
         self._ws_retired: list = []             # outgrown workspaces, freed per request
         self._res_maps = None
         self._wl_log = None
@@ -319,6 +326,9 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         addresses; they are re-captured on the next decode step) and parks the
         old buffer until the next request starts, because queued kernels, the
         CPU worker and UVA kernel copies may still use it."""
+        v = self._wsv.get((name, shape, dtype, pinned))
+        if v is not None:                  # hot path: the same view as last time
+            return v
         n = 1
         for x in shape:
             n *= int(x)
@@ -329,11 +339,14 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
                 if self._capturing:
                     raise SimulationError(f"workspace {name!r} grew during graph capture")
                 self._ws_retired.append(t)
+                self._wsv.clear()          # views of the outgrown buffer
                 self._drop_graphs()
             t = (torch.empty((max(n, 1),), dtype=dtype, pin_memory=True) if pinned
                  else torch.empty((max(n, 1),), dtype=dtype, device=self.dev))
             self._wsd[key] = t
-        return t[:n].view(shape)
+        v = t[:n].view(shape)
+        self._wsv[(name, shape, dtype, pinned)] = v
+        return v
 
     def _drop_graphs(self) -> None:
         """Forget the captured decode graphs (re-captured on demand)."""
