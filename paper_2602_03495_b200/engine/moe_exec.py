@@ -74,7 +74,13 @@ class MoEExecMixin:
         return y
 
     def _splits_for(self, tiles: int, max_rows: int, ffn_dim: int | None = None) -> int:
-        return ffn_splits(max_rows, tiles, (ffn_dim or self.arch.ffn_dim) // 64, self.n_sm)
+        key = (tiles, max_rows, ffn_dim)
+        sp = self._splits_memo.get(key)
+        if sp is None:
+            sp = self._splits_memo[key] = ffn_splits(max_rows, tiles,
+                                                     (ffn_dim or self.arch.ffn_dim) // 64,
+                                                     self.n_sm)
+        return sp
 
     def _copy_into_staging(self, l: int, e: int, demand: bool = False
                            ) -> tuple[int, torch.cuda.Event]:
@@ -174,7 +180,7 @@ class MoEExecMixin:
         g_np = np.frombuffer(rec.G, dtype=np.int8, count=NL)
         G = np.flatnonzero(g_np).tolist()
         # numpy views of this layer's pinned row: ptrs | maps | G mask
-        ph = self.ptr_host[l]
+        pd_addr, ph_addr, row_bytes = self._ptr_rows[l]
         row = self._ptr_host_np[l]
         ptrs = row[:NL * 8].view(np.uint64)
         maps = row[NL * 8:NL * 16].view(np.uint64)
@@ -195,7 +201,7 @@ class MoEExecMixin:
             if s >= 0:
                 if s in self._repl_slot:           # admitted, copy not issued yet
                     self._issue_repl(s, urgent=True)
-                ptrs[e] = self.cache_buf[s].data_ptr()
+                ptrs[e] = self._slot_ptrs[s]
                 maps[e] = self._map_addr(s)
                 if self.slot_ready[s] is not None:
                     waits.append(self.slot_ready[s])
@@ -213,17 +219,16 @@ class MoEExecMixin:
             waits.append(ev)
             used_staging.append(i)
             stage_of[e] = i
-        pd = self.ptr_dev[l]
         # kernel copy from mapped pinned memory: never queues behind expert DMA
-        _lib.call("dali_copy_mapped", pd.data_ptr(), ph.data_ptr(), ph.numel(), cs.cuda_stream)
+        _lib.call("dali_copy_mapped", pd_addr, ph_addr, row_bytes, cs.cuda_stream)
         splits = 1
         max_rows = 0
         if G and self.use_tc:
-            wg = wl_np[G]
-            max_rows = int(wg.max())
+            wg = [int(wl_np[e]) for e in G]
+            max_rows = max(wg)
             bn = 16 if max_rows <= 16 else 32 if max_rows <= 32 else 64 if max_rows <= 64 \
                 else 128 if max_rows <= 128 else 256
-            tiles = int(((wg + bn - 1) // bn).sum()) * (d // 128)
+            tiles = sum((w_ + bn - 1) // bn for w_ in wg) * (d // 128)
             splits = self._splits_for(tiles, max_rows)
         yp = self._ws("yp", (splits, max(R, 1), d), torch.float32)
         if G and R > 0:
@@ -235,11 +240,11 @@ class MoEExecMixin:
                 t0.record(cs)
             if self.use_tc:
                 _lib.call("dali_expert_ffn_tc", xrows.data_ptr(), offsets.data_ptr(), NL,
-                          pd.data_ptr() + NL * 8, d, f, R, max_rows, len(G),
+                          pd_addr + NL * 8, d, f, R, max_rows, len(G),
                           hbuf.data_ptr(), yp.data_ptr(), splits, cs.cuda_stream)
             else:
                 _lib.call("dali_expert_ffn", xrows.data_ptr(), offsets.data_ptr(), NL,
-                          pd.data_ptr(), d, f, R, R, hbuf.data_ptr(), yp.data_ptr(),
+                          pd_addr, d, f, R, R, hbuf.data_ptr(), yp.data_ptr(),
                           cs.cuda_stream)
             if self.cfg.time_ffn:
                 t1 = torch.cuda.Event(enable_timing=True)
@@ -294,7 +299,7 @@ class MoEExecMixin:
         self._last_exec = dict(hit=n_hit, pf=n_pf, dem=n_dem, t0=t0_ev,
                                rep=int(rec.ev_n) if (rec.ev_valid and not self.resident_mode) else 0,
                                done=int(rec.n_done) if not self.resident_mode else 0)
-        return yp, splits, pd.data_ptr() + NL * 16
+        return yp, splits, pd_addr + NL * 16
 
     # ------------------------------------------------ deferred replacements
     # EngineConfig.lazy_replace: a window replacement (the workload-aware

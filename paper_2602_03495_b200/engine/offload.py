@@ -213,6 +213,8 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
                                       device=self.dev) if slots else None)
         self.host_slot = self.policy.slot_of.cpu().numpy().copy()
         self.slot_ready = [None] * (L * slots)   # per cache slot: last replacement copy
+        self._slot_ptrs = ([self.cache_buf.data_ptr() + s * weights.expert_bytes
+                            for s in range(L * slots)] if slots else [])
         self._repl_pend = [dict() for _ in range(L)]   # layer -> {slot: (expert, victim read)}
         self._repl_slot: dict = {}                      # slot -> layer of its pending copy
         self._repl_inflight = collections.deque()       # background copies in flight
@@ -238,6 +240,7 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         self._rows_flag = torch.zeros(2, dtype=torch.int64).pin_memory()
         self._rows_flag_p = self._rows_flag.data_ptr()
         self._rows_seq = self._rows_seq_checked = 0
+        self._splits_memo: dict = {}
         self._pending_cpu = None              # deferred join of the previous layer
         self._blk_tab = None                  # (L, N) host block addresses (dali_cpu_submit_layer)
         self._sub_args = {}                   # layer -> prebuilt submission arguments
@@ -248,6 +251,10 @@ class OffloadEngine(MoEExecMixin, DecodeGraphMixin, EPMoEMixin):
         self.ptr_host = torch.zeros((L, row), dtype=torch.uint8, pin_memory=True)
         self._ptr_host_np = self.ptr_host.numpy()    # same pinned memory
         self.ptr_dev = torch.zeros((L, row), dtype=torch.uint8, device=self.dev)
+        # per layer: (device row address, pinned row address, row bytes) -- the
+        # decode dispatch reads these instead of indexing the tensors per layer
+        self._ptr_rows = [(self.ptr_dev.data_ptr() + l * row, self.ptr_host.data_ptr() + l * row,
+                           row) for l in range(L)]
         self.rope = Rope(a, max_seq, self.dev)
         self.max_batch, self.max_seq = max_batch, max_seq
         self.kv = None
