@@ -399,6 +399,11 @@ int dali_host_wait_timeouts(uint64_t* out, int32_t reset);
  * queue behind expert-block DMA.  16-byte aligned pointers take the vector
  * path; unaligned copies are byte-wise and limited to 1 MiB. */
 int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void* stream);
+/* Two 16-byte aligned ranges in one kernel launch (same copies as two
+ * dali_copy_mapped calls): the decode head's D2H mirrors of the routing block
+ * and the permuted rows the CPU experts read. */
+int dali_copy_mapped2(void* dst0, const void* src0, int64_t n0, void* dst1,
+                      const void* src1, int64_t n1, void* stream);
 /* Engine plumbing: cudaMemcpyAsync(cudaMemcpyDefault) of nbytes on `stream`
  * -- the copy-engine expert-block transfers (pinned host store -> HBM cache
  * slot / staging slot) without a host-side stream switch.  The H2D leg of

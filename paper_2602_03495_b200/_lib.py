@@ -105,6 +105,7 @@ SIGNATURES = {
     "dali_expert_ffn_tc": [_P, _P, _I32, _P, _I32, _I32, _I64, _I32, _I32, _P, _P, _I32, _P],
     "dali_expert_maps": [_P, _I32, _I32, _P],
     "dali_memcpy_async": [_P, _P, C.c_size_t, _P],
+    "dali_copy_mapped2": [_P, _P, _I64, _P, _P, _I64, _P],
     "dali_init_uniform_bf16": [_P, _I64, C.c_uint64, C.c_uint64, C.c_float, _P],
     "dali_host_alloc": [C.c_size_t, _I32, C.POINTER(C.c_void_p)],
     "dali_host_free": [_P, C.c_size_t],

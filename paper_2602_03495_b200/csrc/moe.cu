@@ -487,6 +487,26 @@ __global__ void copy_mapped_kernel(uint4* __restrict__ dst, const uint4* __restr
   if (blockIdx.x == 0 && threadIdx.x < tail)
     dst_tail[threadIdx.x] = *reinterpret_cast<const volatile uint8_t*>(src_tail + threadIdx.x);
 }
+// Two independent ranges in one launch (the decode head's routing-block and
+// permuted-row mirrors): same per-element copies as copy_mapped_kernel.
+__global__ void copy_mapped2_kernel(uint4* __restrict__ d0, const uint4* __restrict__ s0,
+                                    int64_t n0, uint4* __restrict__ d1,
+                                    const uint4* __restrict__ s1, int64_t n1,
+                                    uint8_t* __restrict__ dt0, const uint8_t* __restrict__ st0,
+                                    int t0, uint8_t* __restrict__ dt1,
+                                    const uint8_t* __restrict__ st1, int t1) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) pcie_quiet(kQuietCtlNs);
+  DALI_PDL_ENTRY();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1; i += stride) {
+    if (i < n0) d0[i] = s0[i];
+    else d1[i - n0] = s1[i - n0];
+  }
+  if (blockIdx.x == 0 && threadIdx.x < t0)
+    dt0[threadIdx.x] = *reinterpret_cast<const volatile uint8_t*>(st0 + threadIdx.x);
+  if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + t1)
+    dt1[threadIdx.x - 32] = *reinterpret_cast<const volatile uint8_t*>(st1 + threadIdx.x - 32);
+}
 __global__ void copy_bytes_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
                                   int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -569,6 +589,29 @@ extern "C" int dali_copy_mapped(void* dst, const void* src, int64_t nbytes, void
       reinterpret_cast<uint8_t*>(dst) + n16 * 16, reinterpret_cast<const uint8_t*>(src) + n16 * 16,
       tail);
   DALI_LAUNCH_CHECK("copy_mapped_kernel");
+  return DALI_OK;
+}
+
+extern "C" int dali_copy_mapped2(void* dst0, const void* src0, int64_t n0, void* dst1,
+                                 const void* src1, int64_t n1, void* stream) {
+  DALI_REQUIRE(n0 >= 0 && n1 >= 0, DALI_ECUDA, "dali_copy_mapped2: negative size");
+  DALI_REQUIRE((n0 == 0 || (dst0 && src0)) && (n1 == 0 || (dst1 && src1)), DALI_ECUDA,
+               "dali_copy_mapped2: null pointer");
+  DALI_REQUIRE(((((uintptr_t)dst0 | (uintptr_t)src0) & 15) == 0 || n0 == 0) &&
+               ((((uintptr_t)dst1 | (uintptr_t)src1) & 15) == 0 || n1 == 0),
+               DALI_ECUDA, "dali_copy_mapped2: ranges must be 16-byte aligned");
+  if (n0 + n1 == 0) return DALI_OK;
+  const int64_t a16 = n0 >> 4, b16 = n1 >> 4;
+  const int64_t blocks =
+      std::max<int64_t>(1, std::min<int64_t>((a16 + b16 + 255) / 256, (int64_t)sm_count() * 4));
+  launch_pdl(copy_mapped2_kernel, dim3((unsigned)blocks), dim3(256), 0, as_stream(stream),
+             reinterpret_cast<uint4*>(dst0), reinterpret_cast<const uint4*>(src0), a16,
+             reinterpret_cast<uint4*>(dst1), reinterpret_cast<const uint4*>(src1), b16,
+             reinterpret_cast<uint8_t*>(dst0) + a16 * 16,
+             reinterpret_cast<const uint8_t*>(src0) + a16 * 16, (int)(n0 & 15),
+             reinterpret_cast<uint8_t*>(dst1) + b16 * 16,
+             reinterpret_cast<const uint8_t*>(src1) + b16 * 16, (int)(n1 & 15));
+  DALI_LAUNCH_CHECK("copy_mapped2_kernel");
   return DALI_OK;
 }
 

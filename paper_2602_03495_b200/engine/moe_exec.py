@@ -154,12 +154,25 @@ class MoEExecMixin:
         else:
             dst.copy_(src, non_blocking=True)
 
-    def _host_view(self, v, T: int):
-        """Pinned host mirror of the routing block (valid after the event wait)."""
+    def _host_view(self, v, T: int, xp=None):
+        """Pinned host mirror of the routing block (valid after the event wait).
+        xp = (pinned dst, device src): the permuted rows, mirrored in the same
+        kernel launch when both fit the kernel-copy path."""
         N, k = self.arch.num_experts, self.arch.top_k
         o_off, o_idx, o_w, nb = v["layout"]
         hb = self._ws("route_h", (nb,), torch.uint8, pinned=True)
-        self._d2h(hb, v["blk"])
+        src = v["blk"]
+        xd, xs = xp if xp is not None else (None, None)
+        nx = xs.numel() * xs.element_size() if xs is not None else 0
+        nr = src.numel() * src.element_size()
+        if xs is not None and nx + nr <= (1 << 20) and not (
+                (hb.data_ptr() | src.data_ptr() | xd.data_ptr() | xs.data_ptr()) & 15):
+            _lib.call("dali_copy_mapped2", hb.data_ptr(), src.data_ptr(), nr, xd.data_ptr(),
+                      xs.data_ptr(), nx, self._cur().cuda_stream)
+        else:
+            self._d2h(hb, src)
+            if xs is not None:
+                self._d2h(xd, xs)
         return {
             "wl": hb[:o_off].view(torch.int64),
             "offsets": hb[o_off:o_off + (N + 1) * 4].view(torch.int32),
@@ -613,9 +626,8 @@ class MoEExecMixin:
         else:
             ri = self.policy.layer_step(step, l, token_index, is_eos, v["wl"], h, gate_next,
                                         gate_this=self.w.router[l], gate_next_norm2=nn2)
-        hv = self._host_view(v, T)
         xp_host = self._ws("xp_h", (R, d), torch.bfloat16, pinned=True)
-        self._d2h(xp_host, v["xp"])
+        hv = self._host_view(v, T, xp=(xp_host, v["xp"]))
         h_host = None
         if self.cfg.capture:
             h_host = self._ws("h_h", (T, d), torch.bfloat16, pinned=True)
