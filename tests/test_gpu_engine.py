@@ -782,3 +782,40 @@ def test_tc_ffn_single_cta_wide_path_subprocess():
                         f"{__file__}::test_tc_ffn_matches_simt_and_torch"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_shared_experts_in_head_match_tail(use_graph):
+    """Shared experts launched on a side stream inside the decision head
+    (EngineConfig.shared_in_head, joined before the head ends) == launched on
+    the compute stream after the host read the decision: bit-identical tokens,
+    logits and MoE layer outputs, same decisions, over two requests (graph
+    heads captured in the first, replayed in the second)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    arch = preset("tiny-shared")
+    w = ModelWeights(arch, seed=11)
+    cm = default_cost_model(shared_expert_gpu_time=SHARED_MS["tiny-shared"],
+                            non_moe_layer_time=3.0)
+    res = np.random.default_rng(1).standard_normal((arch.num_layers - 1, arch.hidden_dim)) * 0.05
+    engs = [OffloadEngine(arch, w, cm, EngineConfig(cache_slots_per_layer=6, prefetch_size=2,
+                                                    seed=3, use_graph=use_graph,
+                                                    shared_in_head=sh, capture_moe_io=True),
+                          residuals=res, max_seq=64)
+            for sh in (True, False)]
+    g = torch.Generator().manual_seed(8)
+    for rep in range(2):
+        prompt = torch.randint(0, arch.vocab_size, (1, 10), generator=g)
+        (ta, sa), (tb, sb) = [e.generate(prompt, 8) for e in engs]
+        assert torch.equal(ta, tb), rep
+        for la, lb in zip(sa.logits, sb.logits):
+            assert torch.equal(la, lb), rep
+        assert len(sa.moe_io) == len(sb.moe_io) > 0
+        for (ka, la_, xa, oa), (kb, lb_, xb, ob) in zip(sa.moe_io, sb.moe_io):
+            assert (ka, la_) == (kb, lb_) and torch.equal(xa, xb) and torch.equal(oa, ob), rep
+        da, db = engs[0].policy.decision_log(), engs[1].policy.decision_log()
+        for a_, b_ in zip(da, db):
+            assert np.array_equal(a_["G"], b_["G"]) and np.array_equal(a_["C"], b_["C"])
+            assert a_["hits"] == b_["hits"] and a_["event"] == b_["event"]
