@@ -445,7 +445,9 @@ def run_dali(args, ws, rank, local):
     local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", ws))
     cores = len(os.sched_getaffinity(0))
     cfg = EngineConfig(cache_gb=args.cache_gb, prefetch_size=args.prefetch, w_size=4,
-                       seed=0, time_ffn=True, cpu_threads=max(1, cores // local_ws))
+                       seed=0, time_ffn=True,
+                       cpu_threads=int(os.environ.get("DALI_CPU_THREADS", 0))
+                       or max(1, cores // local_ws))
     weights = None
     ep = None
     if args.ep:
