@@ -741,6 +741,15 @@ class MoEExecMixin:
         R = T * k
         cs = self._cur()
         tp0 = time.perf_counter()
+        ev_sh = y_shared = None
+        if self.shared_map_ptr is not None and self.cfg.shared_in_head and T <= 16:
+            # decode: shared expert(s) beside routing + the routed FFN (they need
+            # only h), streaming their weights while routing leaves HBM idle
+            ss = self.shared_stream
+            ss.wait_stream(cs)
+            y_shared = self._shared_ffn(l, h, stream=ss)
+            ev_sh = torch.cuda.Event()
+            ev_sh.record(ss)
         v = self._route(l, h)
         if T == self.kv.k.shape[1] and self.stats.steps_meta:     # decode: device descriptor
             ri = self.policy.n_records + l
@@ -784,7 +793,10 @@ class MoEExecMixin:
             t1 = torch.cuda.Event(enable_timing=True)
             t1.record(cs)
             self._pending_ffn.append((t0, t1, step, l))
-        y_shared = self._shared_ffn(l, h) if self.shared_map_ptr is not None else None
+        if ev_sh is not None:
+            cs.wait_event(ev_sh)
+        elif self.shared_map_ptr is not None:
+            y_shared = self._shared_ffn(l, h)
         out = torch.empty_like(x)
         _lib.call("dali_unpermute_combine", x.data_ptr(), yp.data_ptr(), v["idx"].data_ptr(),
                   v["pos"].data_ptr(), v["wts"].data_ptr(), None, None,

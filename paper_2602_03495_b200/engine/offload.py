@@ -86,10 +86,11 @@ class EngineConfig:
     #                                         decode (T <= 16): routing + plan + permute in
     #                                         one launch (dali_route_plan_bf16)
     shared_in_head: bool = os.environ.get("DALI_SHARED_HEAD", "1") != "0"
-    #                                         offloaded MoE layer: the shared expert(s) run
-    #                                         on a side stream beside routing + policy (in
-    #                                         the per-layer decode graph), not after the
-    #                                         host has read the decision
+    #                                         the shared expert(s) run on a side stream
+    #                                         beside routing + policy (offloaded: inside the
+    #                                         per-layer decode graph, not after the host has
+    #                                         read the decision; all-resident: beside routing
+    #                                         and the routed FFN), joined before the combine
     fused_norm_gemv: bool = os.environ.get("DALI_FUSED_NORM", "1") != "0"
     #                                         decode (B <= 8): attention-block RMSNorms fused
     #                                         into the qkv / o projection GEMVs

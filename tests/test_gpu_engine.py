@@ -819,3 +819,31 @@ def test_shared_experts_in_head_match_tail(use_graph):
         for a_, b_ in zip(da, db):
             assert np.array_equal(a_["G"], b_["G"]) and np.array_equal(a_["C"], b_["C"])
             assert a_["hits"] == b_["hits"] and a_["event"] == b_["event"]
+
+
+def test_resident_shared_side_stream_matches_serial():
+    """All-resident decode with the shared experts on a side stream beside
+    routing and the routed FFN (graph-replayed) == the serial launch order:
+    bit-identical tokens and logits, same workloads, over two requests."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import dataclasses
+
+    from paper_2602_03495_b200.cost_model import default_cost_model
+    from paper_2602_03495_b200.engine import EngineConfig, ModelWeights, OffloadEngine, preset
+    arch = dataclasses.replace(preset("qwen1.5-moe-a2.7b"), name="mini-qwen", num_layers=3,
+                               vocab_size=2048)
+    w = ModelWeights(arch, seed=12, resident=True)
+    cm = default_cost_model(shared_expert_gpu_time=0.5, non_moe_layer_time=1.0)
+    engs = [OffloadEngine(arch, w, cm, EngineConfig(shared_in_head=sh), max_seq=64)
+            for sh in (True, False)]
+    g = torch.Generator().manual_seed(13)
+    for rep in range(2):
+        prompt = torch.randint(0, arch.vocab_size, (1, 9), generator=g)
+        (ta, sa), (tb, sb) = [e.generate(prompt, 10) for e in engs]
+        assert engs[0]._graph is not None
+        assert torch.equal(ta, tb), rep
+        for la, lb in zip(sa.logits, sb.logits):
+            assert torch.equal(la, lb), rep
+        for key in sa.workloads:
+            assert np.array_equal(sa.workloads[key], sb.workloads[key]), (rep, key)
