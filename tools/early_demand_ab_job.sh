@@ -1,5 +1,6 @@
 #!/bin/bash
-# Demand copies issued before the CPU submission (DALI_EARLY_DEMAND=1/0), A/B on
+# Demand copies issued before the CPU submission (DALI_EARLY_DEMAND=1/0; the toggle
+# was removed after this A/B), A/B on
 # one box: engine GPU tests, DSV2 and Qwen B=1 offloaded decode.
 set -u
 O=gpurun_out/ed
