@@ -742,9 +742,10 @@ class MoEExecMixin:
         cs = self._cur()
         tp0 = time.perf_counter()
         ev_sh = y_shared = None
-        if self.shared_map_ptr is not None and self.cfg.shared_in_head and T <= 16:
-            # decode: shared expert(s) beside routing + the routed FFN (they need
-            # only h), streaming their weights while routing leaves HBM idle
+        if self.shared_map_ptr is not None and self.cfg.shared_in_head:
+            # shared expert(s) beside routing + the routed FFN (they need only h):
+            # at decode they stream their weights while routing leaves HBM idle,
+            # at prefill they fill the SMs routing leaves free
             ss = self.shared_stream
             ss.wait_stream(cs)
             y_shared = self._shared_ffn(l, h, stream=ss)
